@@ -1,0 +1,81 @@
+/* C ABI of the B200 leaf-box reduction engine (libhps_leaf.so).
+ *
+ * Plain pointers and sizes only.  All `double*` arguments of the device entry
+ * points are CUDA device pointers; `stream` is a cudaStream_t (NULL = legacy
+ * default stream).  Every function returns 0 on success and a negative value
+ * on failure; hps_last_error() then describes the failure (thread-local).
+ *
+ * Reference interfaces replaced (steklov, /root/reference/pkg/src/steklov):
+ *
+ *   hps_plan_create            <- LeafTemplate.__init__            local_ops.py:224-306
+ *                                 (D1 = diff[axis], D2 = diff@diff, a_bi, a_bb)
+ *   hps_leaf_dtn               <- build_leaf_factors, batched      local_ops.py:439-446
+ *                                 as driven by condensation.build   condensation.py:220-264
+ *                                 incl. factor_interior's guard     local_ops.py:422-436
+ *   hps_leaf_dtn_host          <- the same, host buffers, with the
+ *                                 two-level schedule (BatchSchedule) condensation.py:49-95,225-264
+ *   hps_leaf_solution_operator <- LeafFactors.s = -A_ii^{-1} a_ib    local_ops.py:443
+ *                                 (cache_leaf_factors path)         condensation.py:258-260,376-377
+ *   hps_leaf_reduce_load       <- reduce_load.leaf_task             condensation.py:314-323
+ *   hps_leaf_interior_solve    <- solve.leaf_task (recompute path)  condensation.py:372-383
+ *
+ * Data layout (row-major, C order, float64):
+ *   coeffs : [n_leaves][ncoef][n]   ncoef = d (diagonal second-order a_kk)
+ *                                         + d (first order, if has_first)
+ *                                         + 1 (zeroth order, if has_zeroth)
+ *                                   values at the leaf's interior nodes in the
+ *                                   reference's interior order (C order).
+ *   dtn    : [n_leaves][m][m]       T = A_bb - A_bi A_ii^{-1} A_ib
+ *   s      : [n_leaves][n][m]       S = -A_ii^{-1} A_ib
+ *   f, v, u: [n_leaves][n]          interior vectors
+ *   ub, flux: [n_leaves][m]         boundary vectors (template face order)
+ *   stats  : [n_leaves][2]          min |pivot|, max |pivot| of the LU of A_ii;
+ *                                   the caller applies the reference's
+ *                                   singularity rule (min <= 1e-14 * max).
+ * with n = (p-2)^d interior nodes and m = 2 d (p-2)^(d-1) boundary DOFs
+ * (corner-dropping face grids).
+ */
+#ifndef HPS_LEAF_H
+#define HPS_LEAF_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HPS_ABI_VERSION 1
+
+typedef struct hps_plan_s* hps_plan_t;
+
+int hps_abi_version(void);
+const char* hps_last_error(void);
+int hps_device_count(void);
+
+/* D1, D2: [dim][p][p] scaled Chebyshev differentiation matrices and their
+ * squares; a_bi: [m][n]; a_bb: [m][m] (host pointers, copied).
+ * max_slots: leaves in flight (0 = one per SM); workspace_budget_bytes bounds
+ * the per-slot workspace (0 = unbounded). */
+int hps_plan_create(hps_plan_t* plan, int device, int dim, int p, int has_first, int has_zeroth,
+                    const double* D1, const double* D2, const double* a_bi, const double* a_bb,
+                    int max_slots, size_t workspace_budget_bytes);
+int hps_plan_destroy(hps_plan_t plan);
+int hps_plan_info(hps_plan_t plan, int* n_interior, int* n_boundary, int* ncoef, int* slots,
+                  size_t* dtn_slot_bytes, size_t* solve_slot_bytes);
+
+int hps_leaf_dtn(hps_plan_t plan, int n_leaves, const double* coeffs, double* dtn, double* stats,
+                 void* stream);
+int hps_leaf_dtn_host(hps_plan_t plan, int n_leaves, const double* coeffs_host, double* dtn_host,
+                      double* stats_host, int chunk_leaves);
+int hps_leaf_solution_operator(hps_plan_t plan, int n_leaves, const double* coeffs, double* s,
+                               double* stats, void* stream);
+int hps_leaf_reduce_load(hps_plan_t plan, int n_leaves, const double* coeffs, const double* f,
+                         double* v, double* flux, double* stats, void* stream);
+int hps_leaf_interior_solve(hps_plan_t plan, int n_leaves, const double* coeffs, const double* ub,
+                            const double* v, double* u, double* stats, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HPS_LEAF_H */

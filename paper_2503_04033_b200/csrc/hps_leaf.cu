@@ -1,0 +1,980 @@
+// B200 (sm_100a) leaf-box reduction engine for the two-level HPS solver.
+//
+// One persistent CTA per SM owns one "slot" of HBM workspace and processes leaf
+// boxes one after another (static stride over the batch).  For each leaf the CTA
+//   1. assembles the padded augmented collocation matrix
+//          M = [ A_ii  A_ib ]      (DtN mode,  NR = NC = n_pad + m_pad)
+//              [ A_bi  A_bb ]
+//      or  M = [ A_ii | rhs ]      (solve mode, NR = n_pad, NC = n_pad + 16)
+//      directly from the Chebyshev differentiation tables and the coefficient
+//      values at interior nodes (reference: local_ops.py:362-398),
+//   2. factors the first n_pad columns with partial pivoting restricted to the
+//      interior rows (recursive right-looking LU; reference: local_ops.py:422-436
+//      uses LAPACK getrf on A_ii),
+//   3. DtN mode: forms T = A_bb - A_bi A_ii^{-1} A_ib as the Schur complement
+//      left in the bottom-right block (reference: local_ops.py:439-446,
+//      dtn = a_bb + a_bi @ (-A_ii^{-1} a_ib));
+//      solve mode: forward/back substitution of the rhs column
+//      (reference: condensation.py:314-323 and 372-383).
+//
+// All O(n^3) work runs in one FP64 tensor-core GEMM engine (mma.sync m8n8k4 f64
+// -> SASS DMMA), 128x128 CTA tiles, 8 warps of 64x32, a 4-stage cp.async
+// pipeline that flows across tile boundaries, and an L2 prefetch of the C tile
+// ahead of its epilogue.  Pivot search, the narrow panel and triangular-block
+// inversions run on the same CTA between GEMMs; other SMs keep their tensor
+// pipes busy with their own leaves, so there is no grid-wide synchronisation.
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "hps_leaf.h"
+
+namespace {
+
+constexpr int NT = 256;          // threads per CTA
+constexpr int TM = 128;          // GEMM tile rows
+constexpr int TN = 128;          // GEMM tile cols
+constexpr int KC = 16;           // k-chunk per pipeline stage
+constexpr int STAGES = 4;
+constexpr int A_STRIDE = 20;     // doubles; 160 B rows -> conflict-free m8n8k4 A fragments
+constexpr int B_STRIDE = 132;    // doubles; 1056 B rows -> conflict-free B fragments
+constexpr int STAGE_A = TM * A_STRIDE;
+constexpr int STAGE_B = KC * B_STRIDE;
+constexpr int STAGE_DBL = STAGE_A + STAGE_B;
+constexpr int GEMM_SMEM_BYTES = STAGES * STAGE_DBL * 8;
+constexpr int TRI_BLOCK = 128;   // triangular base block (explicit inverse + GEMM)
+constexpr int SMALL_PANEL = 32;  // recursion leaf width handled by rank-wb updates
+constexpr int RHS_COLS = 16;     // padded rhs block in solve mode
+constexpr int PANEL_SMEM_CAP = 200 * 1024;
+
+enum { MODE_DTN = 0, MODE_REDUCE = 1, MODE_INTERIOR = 2, MODE_SOLOP = 3 };
+
+struct LeafParams {
+  int mode;
+  int d, p, q;            // q = p - 2 interior points per axis
+  int n, m;               // interior / boundary DOFs
+  int n_pad, m_pad;
+  int NR, NC, ld;         // rows, cols, leading dim of the slot matrix
+  int wb;                 // base panel width (candidate rows live in smem)
+  int has_first, has_zeroth, ncoef;
+  int n_leaves;
+  size_t slot_stride;     // doubles per slot matrix
+  double* work;           // slots * slot_stride
+  int* piv;               // slots * n_pad
+  double* scratch;        // slots * TRI_BLOCK * TRI_BLOCK
+  const double* D1;       // d * p * p (scaled first derivative)
+  const double* D2;       // d * p * p (D1 @ D1, computed on host like the reference)
+  const double* a_bi;     // m * n
+  const double* a_bb;     // m * m
+  const double* coeffs;   // n_leaves * ncoef * n
+  const double* in0;      // REDUCE: f (n per leaf); INTERIOR: ub (m per leaf)
+  const double* in1;      // INTERIOR: v (n per leaf)
+  double* out0;           // DTN: T (m*m); REDUCE: v (n); INTERIOR: u (n)
+  double* out1;           // REDUCE: flux (m per leaf)
+  double* stats;          // n_leaves * 2 : min |pivot|, max |pivot| over real columns
+};
+
+// ---------------------------------------------------------------------------
+// PTX helpers
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void cp_async16(void* smem_ptr, const void* gptr, int src_bytes) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_ptr));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gptr), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
+}
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// ---------------------------------------------------------------------------
+// GEMM engine: C[MxN] = (SUB ? C - A*B : A*B), A [MxK], B [KxN], row-major.
+// M, N multiples of 8 (edge tiles predicated); K multiple of KC; all row
+// starts 16-byte aligned.  In-place SET with C == B is legal when M <= TM.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void gemm(const bool SUB, const double* __restrict__ A, int lda,
+                                     const double* B, int ldb, double* C, int ldc, int M, int N,
+                                     int K, double* smem) {
+  if (M <= 0 || N <= 0 || K <= 0) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wm = warp >> 2, wn = warp & 3;
+  const int lr = lane >> 2, lc = lane & 3;
+  const int tiles_n = (N + TN - 1) / TN;
+  const int tiles = ((M + TM - 1) / TM) * tiles_n;
+  const int kchunks = K / KC;
+  const int total = tiles * kchunks;
+
+  auto issue = [&](int it) {
+    if (it < total) {
+      const int tile = it / kchunks, kc = it - tile * kchunks;
+      const int tm = tile / tiles_n, tn = tile - tm * tiles_n;
+      double* sa = smem + (it % STAGES) * STAGE_DBL;
+      double* sb = sa + STAGE_A;
+#pragma unroll
+      for (int e = tid; e < TM * 8; e += NT) {
+        const int r = e >> 3, j = e & 7;
+        const int gr = tm * TM + r;
+        const double* src = A + (size_t)(gr < M ? gr : M - 1) * lda + kc * KC + 2 * j;
+        cp_async16(sa + r * A_STRIDE + 2 * j, src, gr < M ? 16 : 0);
+      }
+#pragma unroll
+      for (int e = tid; e < KC * 64; e += NT) {
+        const int k = e >> 6, j = e & 63;
+        const int gc = tn * TN + 2 * j;
+        const double* src = B + (size_t)(kc * KC + k) * ldb + (gc < N ? gc : N - 2);
+        cp_async16(sb + k * B_STRIDE + 2 * j, src, gc < N ? 16 : 0);
+      }
+      if (SUB && kc == 0) {
+        // warm L2 with the C tile this chunk sequence will update
+        for (int e = tid; e < TM * 8; e += NT) {
+          const int r = e >> 3, j = e & 7;
+          const int gr = tm * TM + r, gc = tn * TN + 16 * j;
+          if (gr < M && gc < N) prefetch_l2(C + (size_t)gr * ldc + gc);
+        }
+      }
+    }
+    cp_async_commit();
+  };
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) issue(s);
+
+  double acc[8][4][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  for (int it = 0; it < total; ++it) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    issue(it + STAGES - 1);
+    const double* sa = smem + (it % STAGES) * STAGE_DBL;
+    const double* sb = sa + STAGE_A;
+#pragma unroll
+    for (int ks = 0; ks < KC; ks += 4) {
+      double af[8], bf[4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) af[i] = sa[(wm * 64 + i * 8 + lr) * A_STRIDE + ks + lc];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = sb[(ks + lc) * B_STRIDE + wn * 32 + j * 8 + lr];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+    }
+    const int tile = it / kchunks;
+    if (it - tile * kchunks == kchunks - 1) {
+      const int tm = tile / tiles_n, tn = tile - tm * tiles_n;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int row = tm * TM + wm * 64 + i * 8 + lr;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int col = tn * TN + wn * 32 + j * 8 + 2 * lc;
+          if (row < M && col < N) {
+            double2* cp = reinterpret_cast<double2*>(C + (size_t)row * ldc + col);
+            double2 v;
+            if (SUB) {
+              double2 old = *cp;
+              v.x = old.x - acc[i][j][0];
+              v.y = old.y - acc[i][j][1];
+            } else {
+              v.x = acc[i][j][0];
+              v.y = acc[i][j][1];
+            }
+            *cp = v;
+          }
+          acc[i][j][0] = acc[i][j][1] = 0.0;
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Per-CTA LU context
+// ---------------------------------------------------------------------------
+
+struct Ctx {
+  double* M;
+  int ld, n_piv, n_real, NR, wb;
+  int* piv;
+  double* scratch;
+  double* smem;
+};
+
+__shared__ double s_pmin, s_pmax;
+__shared__ double s_redv[NT / 32];
+__shared__ int s_redi[NT / 32];
+__shared__ int s_pivot;
+
+
+// Row interchanges j in [j0, j0+cnt) applied, in order, to columns [c_lo, c_hi).
+__device__ void apply_swaps(const Ctx& c, int j0, int cnt, int c_lo, int c_hi) {
+  if (c_hi <= c_lo || cnt <= 0) return;
+  __syncthreads();
+  for (int col = c_lo + threadIdx.x; col < c_hi; col += NT) {
+    for (int j = j0; j < j0 + cnt; ++j) {
+      const int pr = c.piv[j];
+      if (pr != j) {
+        double* a = c.M + (size_t)j * c.ld + col;
+        double* b = c.M + (size_t)pr * c.ld + col;
+        const double t = *a;
+        *a = *b;
+        *b = t;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Factor columns [b0, b0+wb): candidate rows [b0, n_piv) in shared memory,
+// non-candidate rows [n_piv, NR) by a triangular solve with the new U block.
+__device__ void base_factor(Ctx& c, int b0, int wb) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n_cand = c.n_piv - b0;
+  double* S = c.smem;
+  __syncthreads();
+  for (int e = tid; e < n_cand * wb; e += NT) {
+    const int r = e / wb, j = e - r * wb;
+    S[e] = c.M[(size_t)(b0 + r) * c.ld + b0 + j];
+  }
+  __syncthreads();
+  for (int j = 0; j < wb; ++j) {
+    double best = -1.0;
+    int bidx = 0x7fffffff;
+    for (int r = j + tid; r < n_cand; r += NT) {
+      const double v = fabs(S[r * wb + j]);
+      if (v > best) { best = v; bidx = r; }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bidx, off);
+      if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
+    }
+    if (lane == 0) { s_redv[warp] = best; s_redi[warp] = bidx; }
+    __syncthreads();
+    if (tid == 0) {
+      double bv = s_redv[0];
+      int bi = s_redi[0];
+      for (int w = 1; w < NT / 32; ++w) {
+        if (s_redv[w] > bv || (s_redv[w] == bv && s_redi[w] < bi)) { bv = s_redv[w]; bi = s_redi[w]; }
+      }
+      if (bi == 0x7fffffff) bi = j;
+      s_pivot = bi;
+      c.piv[b0 + j] = b0 + bi;
+    }
+    __syncthreads();
+    const int pr = s_pivot;
+    if (pr != j && tid < wb) {
+      const double t = S[j * wb + tid];
+      S[j * wb + tid] = S[pr * wb + tid];
+      S[pr * wb + tid] = t;
+    }
+    __syncthreads();
+    const double pivot = S[j * wb + j];
+    if (tid == 0 && b0 + j < c.n_real) {
+      const double ap = fabs(pivot);
+      s_pmin = fmin(s_pmin, ap);
+      s_pmax = fmax(s_pmax, ap);
+    }
+    const double inv = (pivot != 0.0) ? 1.0 / pivot : 1.0;
+    for (int r = j + 1 + tid; r < n_cand; r += NT) {
+      const double l = S[r * wb + j] * inv;
+      S[r * wb + j] = l;
+      for (int jj = j + 1; jj < wb; ++jj) S[r * wb + jj] -= l * S[j * wb + jj];
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < n_cand * wb; e += NT) {
+    const int r = e / wb, j = e - r * wb;
+    c.M[(size_t)(b0 + r) * c.ld + b0 + j] = S[e];
+  }
+  // non-candidate rows: L = A U^{-1}
+  for (int r = c.n_piv + tid; r < c.NR; r += NT) {
+    double* row = c.M + (size_t)r * c.ld + b0;
+    double x[8];
+    for (int j = 0; j < wb; ++j) x[j] = row[j];
+    for (int j = 0; j < wb; ++j) {
+      double v = x[j];
+      for (int i = 0; i < j; ++i) v -= x[i] * S[i * wb + j];
+      const double pv = S[j * wb + j];
+      x[j] = v * ((pv != 0.0) ? 1.0 / pv : 1.0);
+    }
+    for (int j = 0; j < wb; ++j) row[j] = x[j];
+  }
+  __syncthreads();
+}
+
+// Columns [c0, c0+w), w <= SMALL_PANEL: base blocks with rank-wb updates.
+__device__ void lu_small(Ctx& c, int c0, int w) {
+  const int wb = c.wb;
+  const int tid = threadIdx.x;
+  for (int b0 = c0; b0 < c0 + w; b0 += wb) {
+    base_factor(c, b0, wb);
+    apply_swaps(c, b0, wb, c0, b0);
+    apply_swaps(c, b0, wb, b0 + wb, c0 + w);
+    const int cl = b0 + wb, ch = c0 + w;
+    if (cl >= ch) continue;
+    // U12 = L_bb^{-1} A12 on rows [b0, b0+wb)
+    for (int col = cl + tid; col < ch; col += NT) {
+      for (int i = 1; i < wb; ++i) {
+        double v = c.M[(size_t)(b0 + i) * c.ld + col];
+        for (int k = 0; k < i; ++k)
+          v -= c.M[(size_t)(b0 + i) * c.ld + b0 + k] * c.M[(size_t)(b0 + k) * c.ld + col];
+        c.M[(size_t)(b0 + i) * c.ld + col] = v;
+      }
+    }
+    __syncthreads();
+    // rank-wb update of rows [b0+wb, NR), cols [cl, ch)
+    const int ncols = ch - cl;
+    double* U = c.smem;  // wb x ncols
+    for (int e = tid; e < wb * ncols; e += NT) {
+      const int i = e / ncols, k = e - i * ncols;
+      U[e] = c.M[(size_t)(b0 + i) * c.ld + cl + k];
+    }
+    __syncthreads();
+    for (int r = b0 + wb + tid; r < c.NR; r += NT) {
+      double* row = c.M + (size_t)r * c.ld;
+      double l[8];
+      for (int i = 0; i < wb; ++i) l[i] = row[b0 + i];
+      for (int k = 0; k < ncols; ++k) {
+        double v = row[cl + k];
+        for (int i = 0; i < wb; ++i) v -= l[i] * U[i * ncols + k];
+        row[cl + k] = v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Explicit inverse of the unit-lower block M[r0.., r0..] (h <= TRI_BLOCK) into scratch (ld TRI_BLOCK).
+__device__ void invert_unit_lower(const Ctx& c, int r0, int h) {
+  double* X = c.smem;  // h x TRI_BLOCK (column j owned by thread j)
+  __syncthreads();
+  const int j = threadIdx.x;
+  if (j < h) {
+    for (int i = 0; i < h; ++i) {
+      double v;
+      if (i < j) v = 0.0;
+      else if (i == j) v = 1.0;
+      else {
+        const double* Li = c.M + (size_t)(r0 + i) * c.ld + r0;
+        v = 0.0;
+        for (int k = j; k < i; ++k) v -= Li[k] * X[k * TRI_BLOCK + j];
+      }
+      X[i * TRI_BLOCK + j] = v;
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < h * TRI_BLOCK; e += NT) c.scratch[e] = X[e];
+  __syncthreads();
+}
+
+// Explicit inverse of the upper block M[r0.., r0..] (h <= TRI_BLOCK) into scratch.
+__device__ void invert_upper(const Ctx& c, int r0, int h) {
+  double* X = c.smem;
+  __syncthreads();
+  const int j = threadIdx.x;
+  if (j < h) {
+    for (int i = h - 1; i >= 0; --i) {
+      double v;
+      if (i > j) v = 0.0;
+      else {
+        const double* Ui = c.M + (size_t)(r0 + i) * c.ld + r0;
+        v = (i == j) ? 1.0 : 0.0;
+        for (int k = i + 1; k <= j; ++k) v -= Ui[k] * X[k * TRI_BLOCK + j];
+        v = v / Ui[i];
+      }
+      X[i * TRI_BLOCK + j] = v;
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < h * TRI_BLOCK; e += NT) c.scratch[e] = X[e];
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Op program.  The recursive LU / TRSM structure is unrolled on the host into a
+// flat list of ops; the persistent CTA interprets it, so the GEMM engine is
+// inlined once and nothing recurses on the device.
+// ---------------------------------------------------------------------------
+
+enum OpKind : int {
+  OP_SMALL = 0,      // lu_small(c0=a, w=b)
+  OP_SWAP = 1,       // apply_swaps(j0=a, cnt=b, c_lo=c, c_hi=d)
+  OP_INV_LOWER = 2,  // scratch := inv(unit lower M[a..a+b, a..a+b])
+  OP_INV_UPPER = 3,  // scratch := inv(upper M[a..a+b, a..a+b])
+  OP_GEMM_SUB = 4,   // M[c_r.., c_c..] -= M[a_r.., a_c..] * M[b_r.., b_c..]  (Mdim, Ndim, Kdim)
+  OP_GEMM_SET = 5,   // M[c_r.., c_c..]  = scratch * M[b_r.., b_c..]
+};
+
+struct Op {
+  int kind;
+  int a, b, c, d;          // generic small-op arguments
+  int ar, ac, br, bc, cr, cc, Mdim, Ndim, Kdim;  // GEMM operands (row, col offsets)
+};
+
+// ---------------------------------------------------------------------------
+// Operator assembly (reference: local_ops.py:362-398, sum order x,y,z second
+// order; first order x,y,z; zeroth).  Explicit _rn intrinsics forbid FMA
+// contraction so entries match scipy's sparse arithmetic bit for bit.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void interior_multi(const LeafParams& P, int r, int* I) {
+  const int q = P.q;
+  if (P.d == 3) {
+    I[0] = r / (q * q) + 1;
+    I[1] = (r / q) % q + 1;
+    I[2] = r % q + 1;
+  } else {
+    I[0] = r / q + 1;
+    I[1] = r % q + 1;
+    I[2] = 0;
+  }
+}
+
+// Boundary DOF index of the endpoint of the axis-`a` line through interior node I
+// (face order -x,+x,-y,+y[,-z,+z]; lexicographic over the tangential indices,
+// reference geometry convention local_ops.py:249-262).
+__device__ __forceinline__ int boundary_index(const LeafParams& P, int a, int side, const int* I) {
+  const int q = P.q;
+  int t, fd;
+  if (P.d == 3) {
+    const int o0 = (a == 0) ? 1 : 0, o1 = (a == 2) ? 1 : 2;
+    t = (I[o0] - 1) * q + (I[o1] - 1);
+    fd = q * q;
+  } else {
+    t = I[a == 0 ? 1 : 0] - 1;
+    fd = q;
+  }
+  return (2 * a + side) * fd + t;
+}
+
+// A[row r][col with multi-index J]; coefficient pointer layout (ncoef, n)
+__device__ double op_entry(const LeafParams& P, const double* cf, int r, const int* I, const int* J) {
+  const int p = P.p, d = P.d;
+  double v = 0.0;
+  bool line[3];
+  for (int a = 0; a < 3; ++a) {
+    bool ok = true;
+    for (int k = 0; k < d; ++k)
+      if (k != a && I[k] != J[k]) ok = false;
+    line[a] = (a < d) && ok;
+  }
+  for (int a = 0; a < d; ++a)
+    if (line[a]) v = __dadd_rn(v, __dmul_rn(-cf[a * P.n + r], P.D2[(a * p + I[a]) * p + J[a]]));
+  int k = d;
+  if (P.has_first) {
+    for (int a = 0; a < d; ++a)
+      if (line[a]) v = __dadd_rn(v, __dmul_rn(cf[(k + a) * P.n + r], P.D1[(a * p + I[a]) * p + J[a]]));
+    k += d;
+  }
+  if (P.has_zeroth) {
+    bool same = true;
+    for (int a = 0; a < d; ++a)
+      if (I[a] != J[a]) same = false;
+    if (same) v = __dadd_rn(v, cf[k * P.n + r]);
+  }
+  return v;
+}
+
+// Fill the slot matrix.  Warp per row: zero the row, then scatter structural nonzeros.
+__device__ void assemble(const LeafParams& P, double* M, int leaf) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* cf = P.coeffs + (size_t)leaf * P.ncoef * P.n;
+  const int p = P.p, d = P.d;
+  for (int r = warp; r < P.NR; r += NT / 32) {
+    double* row = M + (size_t)r * P.ld;
+    double2* row2 = reinterpret_cast<double2*>(row);
+    for (int c2 = lane; c2 < P.NC / 2; c2 += 32) row2[c2] = make_double2(0.0, 0.0);
+    __syncwarp();
+    if (r < P.n) {
+      int I[3];
+      interior_multi(P, r, I);
+      // each (axis, position) on the d lines through node I: interior neighbour or face node
+      for (int e = lane; e < d * p; e += 32) {
+        const int a = e / p, pos = e - a * p;
+        int J[3] = {I[0], I[1], I[2]};
+        J[a] = pos;
+        if (pos == I[a] && a > 0) continue;  // diagonal written once (a == 0)
+        int col;
+        if (pos == 0 || pos == p - 1) {
+          if (P.mode != MODE_DTN && P.mode != MODE_SOLOP) continue;  // solve modes: rhs column
+          col = P.n_pad + boundary_index(P, a, pos == p - 1 ? 1 : 0, I);
+        } else {
+          int flat = 0;
+          for (int k = 0; k < d; ++k) flat = flat * P.q + (J[k] - 1);
+          col = flat;
+        }
+        row[col] = op_entry(P, cf, r, I, J);
+      }
+      if (P.mode == MODE_REDUCE && lane == 0) {
+        row[P.n_pad] = P.in0[(size_t)leaf * P.n + r];
+      } else if (P.mode == MODE_INTERIOR && lane == 0) {
+        // rhs = A_ib u_b over its 2d structural nonzeros, in column (face) order
+        const double* ub = P.in0 + (size_t)leaf * P.m;
+        double s = 0.0;
+        for (int a = 0; a < d; ++a) {
+          for (int side = 0; side < 2; ++side) {
+            int J[3] = {I[0], I[1], I[2]};
+            J[a] = side ? p - 1 : 0;
+            s += op_entry(P, cf, r, I, J) * ub[boundary_index(P, a, side, I)];
+          }
+        }
+        row[P.n_pad] = s;
+      }
+    } else if (r < P.n_pad) {
+      if (lane == 0) row[r] = 1.0;  // dummy pivot keeps padding inert
+    } else if (P.mode == MODE_DTN && r < P.n_pad + P.m) {
+      const int b = r - P.n_pad;
+      const double* abi = P.a_bi + (size_t)b * P.n;
+      const double* abb = P.a_bb + (size_t)b * P.m;
+      for (int c = lane; c < P.n; c += 32) row[c] = abi[c];
+      for (int c = lane; c < P.m; c += 32) row[P.n_pad + c] = abb[c];
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(NT, 1) hps_leaf_kernel(LeafParams P, const Op* __restrict__ ops, int n_ops) {
+  extern __shared__ __align__(16) double smem[];
+  const int slot = blockIdx.x;
+  Ctx c;
+  c.M = P.work + (size_t)slot * P.slot_stride;
+  c.ld = P.ld;
+  c.n_piv = P.n_pad;
+  c.n_real = P.n;
+  c.NR = P.NR;
+  c.wb = P.wb;
+  c.piv = P.piv + (size_t)slot * P.n_pad;
+  c.scratch = P.scratch + (size_t)slot * TRI_BLOCK * TRI_BLOCK;
+  c.smem = smem;
+
+  for (int leaf = blockIdx.x; leaf < P.n_leaves; leaf += gridDim.x) {
+    assemble(P, c.M, leaf);
+    if (threadIdx.x == 0) { s_pmin = INFINITY; s_pmax = 0.0; }
+    __syncthreads();
+    for (int k = 0; k < n_ops; ++k) {
+      const Op op = ops[k];
+      switch (op.kind) {
+        case OP_SMALL: lu_small(c, op.a, op.b); break;
+        case OP_SWAP: apply_swaps(c, op.a, op.b, op.c, op.d); break;
+        case OP_INV_LOWER: invert_unit_lower(c, op.a, op.b); break;
+        case OP_INV_UPPER: invert_upper(c, op.a, op.b); break;
+        default: {
+          const bool sub = (op.kind == OP_GEMM_SUB);
+          const double* A = sub ? c.M + (size_t)op.ar * c.ld + op.ac : c.scratch;
+          gemm(sub, A, sub ? c.ld : TRI_BLOCK, c.M + (size_t)op.br * c.ld + op.bc, c.ld,
+               c.M + (size_t)op.cr * c.ld + op.cc, c.ld, op.Mdim, op.Ndim, op.Kdim, c.smem);
+        }
+      }
+    }
+    if (P.mode == MODE_DTN) {
+      double* T = P.out0 + (size_t)leaf * P.m * P.m;
+      for (int e = threadIdx.x; e < P.m * P.m; e += NT) {
+        const int i = e / P.m, j = e - i * P.m;
+        T[e] = c.M[(size_t)(P.n_pad + i) * c.ld + P.n_pad + j];
+      }
+    } else if (P.mode == MODE_SOLOP) {
+      double* S = P.out0 + (size_t)leaf * P.n * P.m;
+      for (int e = threadIdx.x; e < P.n * P.m; e += NT) {
+        const int i = e / P.m, j = e - i * P.m;
+        S[e] = -c.M[(size_t)i * c.ld + P.n_pad + j];
+      }
+    } else {
+      double* out = P.out0 + (size_t)leaf * P.n;
+      if (P.mode == MODE_REDUCE) {
+        for (int i = threadIdx.x; i < P.n; i += NT) out[i] = c.M[(size_t)i * c.ld + P.n_pad];
+        __syncthreads();
+        // flux = A_bi v : warp per boundary row, lanes stride the interior
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        double* flux = P.out1 + (size_t)leaf * P.m;
+        for (int b = warp; b < P.m; b += NT / 32) {
+          const double* abi = P.a_bi + (size_t)b * P.n;
+          double s = 0.0;
+          for (int k = lane; k < P.n; k += 32) s += abi[k] * out[k];
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+          if (lane == 0) flux[b] = s;
+        }
+      } else {
+        const double* v = P.in1 + (size_t)leaf * P.n;
+        for (int i = threadIdx.x; i < P.n; i += NT) out[i] = v[i] - c.M[(size_t)i * c.ld + P.n_pad];
+      }
+    }
+    if (threadIdx.x == 0) {
+      P.stats[2 * leaf] = s_pmin;
+      P.stats[2 * leaf + 1] = s_pmax;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host-side program builder: the recursion of the blocked algorithm, unrolled.
+// ---------------------------------------------------------------------------
+
+int split16_host(int w) { return ((w / 2 + 15) / 16) * 16; }
+
+struct ProgramBuilder {
+  std::vector<Op> ops;
+  void small(int c0, int w) { Op o{}; o.kind = OP_SMALL; o.a = c0; o.b = w; ops.push_back(o); }
+  void swaps(int j0, int cnt, int lo, int hi) {
+    if (hi <= lo || cnt <= 0) return;
+    Op o{}; o.kind = OP_SWAP; o.a = j0; o.b = cnt; o.c = lo; o.d = hi; ops.push_back(o);
+  }
+  void inv(int kind, int r0, int h) { Op o{}; o.kind = kind; o.a = r0; o.b = h; ops.push_back(o); }
+  void gemm(int kind, int ar, int ac, int br, int bc, int cr, int cc, int M, int N, int K) {
+    if (M <= 0 || N <= 0 || K <= 0) return;
+    Op o{}; o.kind = kind; o.ar = ar; o.ac = ac; o.br = br; o.bc = bc; o.cr = cr; o.cc = cc;
+    o.Mdim = M; o.Ndim = N; o.Kdim = K; ops.push_back(o);
+  }
+  void trsm_lower(int r0, int h, int lo, int hi) {
+    if (hi <= lo) return;
+    if (h <= TRI_BLOCK) {
+      inv(OP_INV_LOWER, r0, h);
+      gemm(OP_GEMM_SET, 0, 0, r0, lo, r0, lo, h, hi - lo, h);
+      return;
+    }
+    const int h1 = split16_host(h);
+    trsm_lower(r0, h1, lo, hi);
+    gemm(OP_GEMM_SUB, r0 + h1, r0, r0, lo, r0 + h1, lo, h - h1, hi - lo, h1);
+    trsm_lower(r0 + h1, h - h1, lo, hi);
+  }
+  void trsm_upper(int r0, int h, int lo, int hi) {
+    if (hi <= lo) return;
+    if (h <= TRI_BLOCK) {
+      inv(OP_INV_UPPER, r0, h);
+      gemm(OP_GEMM_SET, 0, 0, r0, lo, r0, lo, h, hi - lo, h);
+      return;
+    }
+    const int h1 = split16_host(h);
+    trsm_upper(r0 + h1, h - h1, lo, hi);
+    gemm(OP_GEMM_SUB, r0, r0 + h1, r0 + h1, lo, r0, lo, h1, hi - lo, h - h1);
+    trsm_upper(r0, h1, lo, hi);
+  }
+  void lu(int c0, int w, int NR) {
+    if (w <= SMALL_PANEL) { small(c0, w); return; }
+    const int h = split16_host(w);
+    lu(c0, h, NR);
+    swaps(c0, h, c0 + h, c0 + w);
+    trsm_lower(c0, h, c0 + h, c0 + w);
+    gemm(OP_GEMM_SUB, c0 + h, c0, c0, c0 + h, c0 + h, c0 + h, NR - c0 - h, w - h, h);
+    lu(c0 + h, w - h, NR);
+    swaps(c0 + h, w - h, c0, c0 + h);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Host side: plan + C ABI
+// ---------------------------------------------------------------------------
+
+thread_local std::string g_last_error;
+
+int fail(const std::string& msg) {
+  g_last_error = msg;
+  return -1;
+}
+
+#define CK(call)                                                                      \
+  do {                                                                                \
+    cudaError_t _e = (call);                                                          \
+    if (_e != cudaSuccess) return fail(std::string(#call) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+}  // namespace
+
+struct hps_plan_s {
+  int device = 0;
+  int d = 0, p = 0, q = 0, n = 0, m = 0, n_pad = 0, m_pad = 0, wb = 8;
+  int has_first = 0, has_zeroth = 0, ncoef = 0;
+  int sms = 0, slots = 0;
+  size_t budget = 0;
+  double *D1 = nullptr, *D2 = nullptr, *a_bi = nullptr, *a_bb = nullptr;
+  // workspace (sized for the largest mode requested so far)
+  double* work = nullptr;
+  size_t work_doubles = 0;
+  int* piv = nullptr;
+  double* scratch = nullptr;
+  int ws_slots = 0;
+  // unrolled LU programs per mode (device copies)
+  Op* prog[4] = {nullptr, nullptr, nullptr, nullptr};
+  int prog_len[4] = {0, 0, 0, 0};
+  double* h_stage = nullptr;
+};
+
+static int round16(int x) { return (x + 15) / 16 * 16; }
+
+static void mode_dims(const hps_plan_s* P, int mode, int* NR, int* NC) {
+  if (mode == MODE_DTN) {
+    *NR = P->n_pad + P->m_pad;
+    *NC = P->n_pad + P->m_pad;
+  } else if (mode == MODE_SOLOP) {
+    *NR = P->n_pad;
+    *NC = P->n_pad + P->m_pad;
+  } else {
+    *NR = P->n_pad;
+    *NC = P->n_pad + RHS_COLS;
+  }
+}
+
+static size_t slot_doubles(const hps_plan_s* P, int mode) {
+  int NR, NC;
+  mode_dims(P, mode, &NR, &NC);
+  return (size_t)NR * NC;
+}
+
+static int ensure_workspace(hps_plan_s* P, int mode, int want_slots) {
+  const size_t per = slot_doubles(P, mode);
+  size_t slot_bytes = per * 8 + (size_t)P->n_pad * 4 + (size_t)TRI_BLOCK * TRI_BLOCK * 8;
+  int slots = want_slots;
+  if (P->budget > 0) {
+    const size_t fit = P->budget / slot_bytes;
+    if (fit < 1) return fail("memory budget cannot hold one leaf workspace");
+    if ((size_t)slots > fit) slots = (int)fit;
+  }
+  if (P->work && P->work_doubles >= per * (size_t)slots && P->ws_slots >= slots) return slots;
+  if (P->work) cudaFree(P->work);
+  if (P->piv) cudaFree(P->piv);
+  if (P->scratch) cudaFree(P->scratch);
+  P->work = nullptr; P->piv = nullptr; P->scratch = nullptr;
+  CK(cudaMalloc(&P->work, per * (size_t)slots * 8));
+  CK(cudaMalloc(&P->piv, (size_t)P->n_pad * slots * 4));
+  CK(cudaMalloc(&P->scratch, (size_t)TRI_BLOCK * TRI_BLOCK * slots * 8));
+  P->work_doubles = per * (size_t)slots;
+  P->ws_slots = slots;
+  return slots;
+}
+
+static int ensure_program(hps_plan_s* P, int mode) {
+  if (P->prog[mode]) return 0;
+  int NR, NC;
+  mode_dims(P, mode, &NR, &NC);
+  ProgramBuilder b;
+  b.lu(0, P->n_pad, NR);
+  b.swaps(0, P->n_pad, P->n_pad, NC);
+  b.trsm_lower(0, P->n_pad, P->n_pad, NC);
+  if (mode == MODE_DTN)
+    b.gemm(OP_GEMM_SUB, P->n_pad, 0, 0, P->n_pad, P->n_pad, P->n_pad, NR - P->n_pad, NC - P->n_pad, P->n_pad);
+  else
+    b.trsm_upper(0, P->n_pad, P->n_pad, NC);
+  CK(cudaMalloc(&P->prog[mode], b.ops.size() * sizeof(Op)));
+  CK(cudaMemcpy(P->prog[mode], b.ops.data(), b.ops.size() * sizeof(Op), cudaMemcpyHostToDevice));
+  P->prog_len[mode] = (int)b.ops.size();
+  return 0;
+}
+
+static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, const double* in0,
+                  const double* in1, double* out0, double* out1, double* stats, cudaStream_t stream) {
+  if (n_leaves <= 0) return 0;
+  CK(cudaSetDevice(P->device));
+  if (ensure_program(P, mode) != 0) return -1;
+  int want = P->slots;
+  if (want > n_leaves) want = n_leaves;
+  const int slots = ensure_workspace(P, mode, want);
+  if (slots < 0) return -1;
+  LeafParams L;
+  memset(&L, 0, sizeof(L));
+  L.mode = mode;
+  L.d = P->d; L.p = P->p; L.q = P->q; L.n = P->n; L.m = P->m;
+  L.n_pad = P->n_pad; L.m_pad = P->m_pad;
+  mode_dims(P, mode, &L.NR, &L.NC);
+  L.ld = L.NC;
+  L.wb = P->wb;
+  L.has_first = P->has_first; L.has_zeroth = P->has_zeroth; L.ncoef = P->ncoef;
+  L.n_leaves = n_leaves;
+  L.slot_stride = slot_doubles(P, mode);
+  L.work = P->work; L.piv = P->piv; L.scratch = P->scratch;
+  L.D1 = P->D1; L.D2 = P->D2; L.a_bi = P->a_bi; L.a_bb = P->a_bb;
+  L.coeffs = coeffs; L.in0 = in0; L.in1 = in1; L.out0 = out0; L.out1 = out1; L.stats = stats;
+  const int panel_bytes = P->n_pad * P->wb * 8;
+  int smem = GEMM_SMEM_BYTES;
+  if (panel_bytes > smem) smem = panel_bytes;
+  if (TRI_BLOCK * TRI_BLOCK * 8 > smem) smem = TRI_BLOCK * TRI_BLOCK * 8;
+  CK(cudaFuncSetAttribute(hps_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  hps_leaf_kernel<<<slots, NT, smem, stream>>>(L, P->prog[mode], P->prog_len[mode]);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+extern "C" {
+
+const char* hps_last_error(void) { return g_last_error.c_str(); }
+
+int hps_abi_version(void) { return HPS_ABI_VERSION; }
+
+int hps_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int hps_plan_create(hps_plan_t* out, int device, int dim, int p, int has_first, int has_zeroth,
+                    const double* D1, const double* D2, const double* a_bi, const double* a_bb,
+                    int max_slots, size_t workspace_budget_bytes) {
+  if (!out) return fail("null plan pointer");
+  *out = nullptr;
+  if (dim != 2 && dim != 3) return fail("dimension must be 2 or 3");
+  if (p < 4) return fail("p must be >= 4");
+  hps_plan_s* P = new hps_plan_s();
+  P->device = device;
+  P->d = dim; P->p = p; P->q = p - 2;
+  P->n = 1; for (int k = 0; k < dim; ++k) P->n *= P->q;
+  const int fd = (dim == 3) ? P->q * P->q : P->q;
+  P->m = 2 * dim * fd;
+  P->n_pad = round16(P->n);
+  P->m_pad = round16(P->m);
+  P->has_first = has_first ? 1 : 0;
+  P->has_zeroth = has_zeroth ? 1 : 0;
+  P->ncoef = dim + (has_first ? dim : 0) + (has_zeroth ? 1 : 0);
+  int wb = 8;
+  while (wb > 1 && (size_t)P->n_pad * wb * 8 > PANEL_SMEM_CAP) wb >>= 1;
+  P->wb = wb;
+  P->budget = workspace_budget_bytes;
+  if (cudaSetDevice(device) != cudaSuccess) { delete P; return fail("cudaSetDevice failed"); }
+  cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device);
+  P->slots = (max_slots > 0 && max_slots < P->sms) ? max_slots : P->sms;
+  const size_t tab = (size_t)dim * p * p * 8;
+  if (cudaMalloc(&P->D1, tab) != cudaSuccess || cudaMalloc(&P->D2, tab) != cudaSuccess ||
+      cudaMalloc(&P->a_bi, (size_t)P->m * P->n * 8) != cudaSuccess ||
+      cudaMalloc(&P->a_bb, (size_t)P->m * P->m * 8) != cudaSuccess) {
+    hps_plan_destroy(P);
+    return fail("device allocation of templates failed");
+  }
+  cudaMemcpy(P->D1, D1, tab, cudaMemcpyHostToDevice);
+  cudaMemcpy(P->D2, D2, tab, cudaMemcpyHostToDevice);
+  cudaMemcpy(P->a_bi, a_bi, (size_t)P->m * P->n * 8, cudaMemcpyHostToDevice);
+  cudaMemcpy(P->a_bb, a_bb, (size_t)P->m * P->m * 8, cudaMemcpyHostToDevice);
+  if (cudaGetLastError() != cudaSuccess) { hps_plan_destroy(P); return fail("template upload failed"); }
+  *out = P;
+  return 0;
+}
+
+int hps_plan_destroy(hps_plan_t P) {
+  if (!P) return 0;
+  cudaSetDevice(P->device);
+  cudaFree(P->D1); cudaFree(P->D2); cudaFree(P->a_bi); cudaFree(P->a_bb);
+  cudaFree(P->work); cudaFree(P->piv); cudaFree(P->scratch);
+  for (int k = 0; k < 4; ++k) cudaFree(P->prog[k]);
+  if (P->h_stage) cudaFreeHost(P->h_stage);
+  delete P;
+  return 0;
+}
+
+int hps_plan_info(hps_plan_t P, int* n_interior, int* n_boundary, int* ncoef, int* slots,
+                  size_t* dtn_slot_bytes, size_t* solve_slot_bytes) {
+  if (!P) return fail("null plan");
+  if (n_interior) *n_interior = P->n;
+  if (n_boundary) *n_boundary = P->m;
+  if (ncoef) *ncoef = P->ncoef;
+  if (slots) *slots = P->slots;
+  if (dtn_slot_bytes) *dtn_slot_bytes = slot_doubles(P, MODE_DTN) * 8;
+  if (solve_slot_bytes) *solve_slot_bytes = slot_doubles(P, MODE_REDUCE) * 8;
+  return 0;
+}
+
+int hps_leaf_dtn(hps_plan_t P, int n_leaves, const double* coeffs, double* dtn, double* stats,
+                 void* stream) {
+  if (!P) return fail("null plan");
+  return launch(P, MODE_DTN, n_leaves, coeffs, nullptr, nullptr, dtn, nullptr, stats,
+                (cudaStream_t)stream);
+}
+
+int hps_leaf_reduce_load(hps_plan_t P, int n_leaves, const double* coeffs, const double* f,
+                         double* v, double* flux, double* stats, void* stream) {
+  if (!P) return fail("null plan");
+  return launch(P, MODE_REDUCE, n_leaves, coeffs, f, nullptr, v, flux, stats, (cudaStream_t)stream);
+}
+
+int hps_leaf_solution_operator(hps_plan_t P, int n_leaves, const double* coeffs, double* s,
+                               double* stats, void* stream) {
+  if (!P) return fail("null plan");
+  return launch(P, MODE_SOLOP, n_leaves, coeffs, nullptr, nullptr, s, nullptr, stats,
+                (cudaStream_t)stream);
+}
+
+int hps_leaf_interior_solve(hps_plan_t P, int n_leaves, const double* coeffs, const double* ub,
+                            const double* v, double* u, double* stats, void* stream) {
+  if (!P) return fail("null plan");
+  return launch(P, MODE_INTERIOR, n_leaves, coeffs, ub, v, u, nullptr, stats, (cudaStream_t)stream);
+}
+
+// Host-buffer DtN with the two-level schedule on the device: chunks of
+// `chunk_leaves` leaves flow H2D (copy stream) -> kernel (compute stream) ->
+// D2H (copy stream) with double buffering, so PCIe traffic overlaps the LU work.
+int hps_leaf_dtn_host(hps_plan_t P, int n_leaves, const double* coeffs_host, double* dtn_host,
+                      double* stats_host, int chunk_leaves) {
+  if (!P) return fail("null plan");
+  if (n_leaves <= 0) return 0;
+  CK(cudaSetDevice(P->device));
+  if (chunk_leaves <= 0) chunk_leaves = P->slots * 2;
+  if (chunk_leaves > n_leaves) chunk_leaves = n_leaves;
+  const size_t cbytes = (size_t)P->ncoef * P->n * 8, tbytes = (size_t)P->m * P->m * 8;
+  double *d_coef[2] = {nullptr, nullptr}, *d_dtn[2] = {nullptr, nullptr}, *d_stats[2] = {nullptr, nullptr};
+  cudaStream_t s_comp, s_copy;
+  cudaEvent_t ev_in[2], ev_done[2], ev_out[2];
+  CK(cudaStreamCreateWithFlags(&s_comp, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&s_copy, cudaStreamNonBlocking));
+  for (int b = 0; b < 2; ++b) {
+    CK(cudaMalloc(&d_coef[b], cbytes * chunk_leaves));
+    CK(cudaMalloc(&d_dtn[b], tbytes * chunk_leaves));
+    CK(cudaMalloc(&d_stats[b], 16 * (size_t)chunk_leaves));
+    CK(cudaEventCreateWithFlags(&ev_in[b], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_done[b], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_out[b], cudaEventDisableTiming));
+  }
+  int rc = 0;
+  const int nchunks = (n_leaves + chunk_leaves - 1) / chunk_leaves;
+  for (int ci = 0; ci < nchunks && rc == 0; ++ci) {
+    const int b = ci & 1;
+    const int l0 = ci * chunk_leaves;
+    const int cnt = (n_leaves - l0 < chunk_leaves) ? (n_leaves - l0) : chunk_leaves;
+    if (ci >= 2) cudaStreamWaitEvent(s_copy, ev_out[b], 0);  // buffer b drained to host
+    cudaMemcpyAsync(d_coef[b], coeffs_host + (size_t)l0 * P->ncoef * P->n, cbytes * cnt,
+                    cudaMemcpyHostToDevice, s_copy);
+    cudaEventRecord(ev_in[b], s_copy);
+    cudaStreamWaitEvent(s_comp, ev_in[b], 0);
+    rc = launch(P, MODE_DTN, cnt, d_coef[b], nullptr, nullptr, d_dtn[b], nullptr, d_stats[b], s_comp);
+    cudaEventRecord(ev_done[b], s_comp);
+    cudaStreamWaitEvent(s_copy, ev_done[b], 0);
+    cudaMemcpyAsync(dtn_host + (size_t)l0 * P->m * P->m, d_dtn[b], tbytes * cnt,
+                    cudaMemcpyDeviceToHost, s_copy);
+    if (stats_host)
+      cudaMemcpyAsync(stats_host + 2 * (size_t)l0, d_stats[b], 16 * (size_t)cnt,
+                      cudaMemcpyDeviceToHost, s_copy);
+    cudaEventRecord(ev_out[b], s_copy);
+  }
+  cudaError_t e1 = cudaStreamSynchronize(s_copy);
+  cudaError_t e2 = cudaStreamSynchronize(s_comp);
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(d_coef[b]); cudaFree(d_dtn[b]); cudaFree(d_stats[b]);
+    cudaEventDestroy(ev_in[b]); cudaEventDestroy(ev_done[b]); cudaEventDestroy(ev_out[b]);
+  }
+  cudaStreamDestroy(s_comp);
+  cudaStreamDestroy(s_copy);
+  if (rc != 0) return rc;
+  if (e1 != cudaSuccess || e2 != cudaSuccess)
+    return fail(std::string("streamed dtn failed: ") + cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,195 @@
+"""GPU leaf engine: the Python face of libhps_leaf.so.
+
+A :class:`LeafEngine` wraps one device plan (templates uploaded once, a slot
+workspace per SM) and exposes the batched leaf operations of the two-level
+solver on device tensors (torch, CUDA) or host arrays (numpy):
+
+=========================  ==============================================
+``dtn``                    T^tau = A_bb - A_bi A_ii^{-1} A_ib  (build stage)
+``solution_operator``      S^tau = -A_ii^{-1} A_ib
+``reduce_load``            v = A_ii^{-1} f,  flux = A_bi v
+``interior_solve``         u_i = v - A_ii^{-1} (A_ib u_b)
+=========================  ==============================================
+
+PyTorch only supplies device memory and streams; the arithmetic is in the
+CUDA kernels.  There is no CPU fallback: without a CUDA device or the built
+library every call raises :class:`NativeUnavailableError`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Tuple
+
+import numpy as np
+
+from . import _native
+from .errors import ConfigError, NativeUnavailableError
+from .local_ops import DROP_CORNERS, LeafTemplate, coefficient_layout
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise NativeUnavailableError("a CUDA device is required: the leaf path has no CPU fallback")
+    return torch
+
+
+def _ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr() if t is not None else 0)
+
+
+def _np_ptr(a: Optional[np.ndarray]) -> ctypes.c_void_p:
+    return ctypes.c_void_p(a.ctypes.data if a is not None else 0)
+
+
+class LeafEngine:
+    """One device plan for equal leaves of a mesh (shape, order, coefficient layout)."""
+
+    _plans = {}
+
+    def __init__(self, template: LeafTemplate, has_first: bool, has_zeroth: bool,
+                 device: int = 0, max_slots: int = 0, workspace_budget: int = 0):
+        if template.corner_mode != DROP_CORNERS:
+            raise ConfigError("the CUDA leaf engine currently implements corner-dropping face "
+                              "grids only; legendre face grids are not available on the GPU path")
+        self.lib = _native.load()
+        torch = _torch()
+        self.torch = torch
+        self.device = int(device)
+        self.template = template
+        self.d, self.p = template.d, template.p
+        self.n, self.m = template.n_interior, template.n_boundary
+        self.has_first, self.has_zeroth = bool(has_first), bool(has_zeroth)
+        self.ncoef = self.d + (self.d if has_first else 0) + (1 if has_zeroth else 0)
+        D1 = np.ascontiguousarray(np.stack(template.diff))
+        D2 = np.ascontiguousarray(np.stack(template.diff2))
+        a_bi = np.ascontiguousarray(template.a_bi)
+        a_bb = np.ascontiguousarray(template.a_bb)
+        plan = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _native.check(self.lib.hps_plan_create(
+                ctypes.byref(plan), self.device, self.d, self.p, int(has_first), int(has_zeroth),
+                _np_ptr(D1), _np_ptr(D2), _np_ptr(a_bi), _np_ptr(a_bb), int(max_slots),
+                int(workspace_budget)))
+        self.plan = plan
+        n, m, nc, slots = (ctypes.c_int() for _ in range(4))
+        dtn_b, sol_b = ctypes.c_size_t(), ctypes.c_size_t()
+        _native.check(self.lib.hps_plan_info(plan, ctypes.byref(n), ctypes.byref(m), ctypes.byref(nc),
+                                             ctypes.byref(slots), ctypes.byref(dtn_b),
+                                             ctypes.byref(sol_b)))
+        assert n.value == self.n and m.value == self.m and nc.value == self.ncoef
+        self.slots = slots.value
+        self.dtn_slot_bytes = dtn_b.value
+        self.solve_slot_bytes = sol_b.value
+
+    def __del__(self):
+        plan = getattr(self, "plan", None)
+        if plan is not None and plan.value:
+            try:
+                self.lib.hps_plan_destroy(plan)
+            except Exception:
+                pass
+            self.plan = None
+
+    @classmethod
+    def for_template(cls, template: LeafTemplate, coeffs, device: int = 0, **kw) -> "LeafEngine":
+        has_first, has_zeroth = coefficient_layout(coeffs)
+        key = (template.widths, template.p, template.corner_mode, has_first, has_zeroth, device,
+               tuple(sorted(kw.items())))
+        eng = cls._plans.get(key)
+        if eng is None:
+            eng = cls(template, has_first, has_zeroth, device=device, **kw)
+            cls._plans[key] = eng
+        return eng
+
+    # ---------------------------------------------------------------- helpers
+    def _stream(self, stream):
+        torch = self.torch
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        return ctypes.c_void_p(s.cuda_stream)
+
+    def _check_coeffs(self, coeffs):
+        if tuple(coeffs.shape[1:]) != (self.ncoef, self.n):
+            raise ConfigError(f"coefficient pack has shape {tuple(coeffs.shape)}, "
+                              f"expected (leaves, {self.ncoef}, {self.n})")
+
+    def _dev(self, a):
+        torch = self.torch
+        if isinstance(a, torch.Tensor):
+            return a.to(device=f"cuda:{self.device}", dtype=torch.float64).contiguous()
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(f"cuda:{self.device}")
+
+    def _empty(self, *shape):
+        return self.torch.empty(shape, dtype=self.torch.float64, device=f"cuda:{self.device}")
+
+    # ---------------------------------------------------------- device calls
+    def dtn(self, coeffs, out=None, stats=None, stream=None):
+        """DtN maps (leaves, m, m) for device coefficient packs (leaves, ncoef, n)."""
+        coeffs = self._dev(coeffs)
+        self._check_coeffs(coeffs)
+        L = coeffs.shape[0]
+        out = self._empty(L, self.m, self.m) if out is None else out
+        stats = self._empty(L, 2) if stats is None else stats
+        _native.check(self.lib.hps_leaf_dtn(self.plan, L, _ptr(coeffs), _ptr(out), _ptr(stats),
+                                            self._stream(stream)))
+        return out, stats
+
+    def solution_operator(self, coeffs, stream=None):
+        coeffs = self._dev(coeffs)
+        self._check_coeffs(coeffs)
+        L = coeffs.shape[0]
+        s, stats = self._empty(L, self.n, self.m), self._empty(L, 2)
+        _native.check(self.lib.hps_leaf_solution_operator(self.plan, L, _ptr(coeffs), _ptr(s),
+                                                          _ptr(stats), self._stream(stream)))
+        return s, stats
+
+    def reduce_load(self, coeffs, f, stream=None):
+        coeffs, f = self._dev(coeffs), self._dev(f)
+        self._check_coeffs(coeffs)
+        L = coeffs.shape[0]
+        v, flux, stats = self._empty(L, self.n), self._empty(L, self.m), self._empty(L, 2)
+        _native.check(self.lib.hps_leaf_reduce_load(self.plan, L, _ptr(coeffs), _ptr(f), _ptr(v),
+                                                     _ptr(flux), _ptr(stats), self._stream(stream)))
+        return v, flux, stats
+
+    def interior_solve(self, coeffs, ub, v, stream=None):
+        coeffs, ub, v = self._dev(coeffs), self._dev(ub), self._dev(v)
+        self._check_coeffs(coeffs)
+        L = coeffs.shape[0]
+        u, stats = self._empty(L, self.n), self._empty(L, 2)
+        _native.check(self.lib.hps_leaf_interior_solve(self.plan, L, _ptr(coeffs), _ptr(ub), _ptr(v),
+                                                       _ptr(u), _ptr(stats), self._stream(stream)))
+        return u, stats
+
+    # ------------------------------------------------------------ host calls
+    def dtn_host(self, coeffs: np.ndarray, out: Optional[np.ndarray] = None,
+                 chunk_leaves: int = 0) -> Tuple[np.ndarray, np.ndarray]:
+        """Host-buffer DtN through the streamed C entry (H2D / kernel / D2H overlap)."""
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+        self._check_coeffs(coeffs)
+        L = coeffs.shape[0]
+        if out is None:
+            out = np.empty((L, self.m, self.m))
+        stats = np.empty((L, 2))
+        _native.check(self.lib.hps_leaf_dtn_host(self.plan, L, _np_ptr(coeffs), _np_ptr(out),
+                                                 _np_ptr(stats), int(chunk_leaves)))
+        return out, stats
+
+    def solution_operator_host(self, coeffs):
+        s, stats = self.solution_operator(coeffs)
+        return s.cpu().numpy(), stats.cpu().numpy()
+
+    def reduce_load_host(self, coeffs, f):
+        v, flux, stats = self.reduce_load(coeffs, f)
+        return v.cpu().numpy(), flux.cpu().numpy(), stats.cpu().numpy()
+
+    def interior_solve_host(self, coeffs, ub, v):
+        u, stats = self.interior_solve(coeffs, ub, v)
+        return u.cpu().numpy(), stats.cpu().numpy()
+
+
+def dtn_flops(n: int, m: int) -> float:
+    """FLOPs of one leaf reduction in the reference's dense algorithm:
+    getrf(n) + getrs with m right-hand sides + the (m x n) @ (n x m) product."""
+    return 2.0 / 3.0 * n ** 3 + 2.0 * n * n * m + 2.0 * n * m * m

@@ -1,0 +1,115 @@
+"""CUDA leaf path vs the reference's golden vectors and the CPU oracle.
+
+Tolerance (north star): DtN entries and leaf solutions within 1e-10 relative
+Frobenius error of the CPU reference.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import hps_oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+HERE = os.path.dirname(os.path.abspath(__file__))
+G = np.load(os.path.join(HERE, "golden", "leaf_cases.npz"))
+CASES = sorted({k.split("/")[0] for k in G.files})
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def engine_for(name):
+    from paper_2503_04033_b200.engine import LeafEngine
+    from paper_2503_04033_b200.local_ops import LeafTemplate
+    d, p, hf, hz = (int(x) for x in G[name + "/meta"])
+    tpl = LeafTemplate(G[name + "/widths"], p, "drop", False)
+    return LeafEngine(tpl, bool(hf), bool(hz), device=0), G[name + "/coeffs"][None]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_dtn_matches_reference(name):
+    eng, coeffs = engine_for(name)
+    dtn, stats = eng.dtn_host(coeffs)
+    assert rel(dtn[0], G[name + "/dtn"]) <= TOL
+    assert stats[0, 0] > 0 and stats[0, 1] >= stats[0, 0]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_solution_operator_matches_reference(name):
+    eng, coeffs = engine_for(name)
+    s, _ = eng.solution_operator_host(coeffs)
+    assert rel(s[0], G[name + "/s"]) <= TOL
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_reduce_load_matches_reference(name):
+    eng, coeffs = engine_for(name)
+    v, flux, _ = eng.reduce_load_host(coeffs, G[name + "/f"][None])
+    assert rel(v[0], G[name + "/v"]) <= TOL
+    assert rel(flux[0], G[name + "/flux"]) <= TOL
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_interior_solve_matches_reference(name):
+    eng, coeffs = engine_for(name)
+    u, _ = eng.interior_solve_host(coeffs, G[name + "/ub"][None], G[name + "/v"][None])
+    assert rel(u[0], G[name + "/u_int"]) <= TOL
+
+
+def bump_pack(p, leaves, kappa, seed=0, d=3):
+    """Variable-coefficient Helmholtz packs on a row of unit-cube leaves."""
+    from paper_2503_04033_b200.local_ops import LeafTemplate
+    rng = np.random.default_rng(seed)
+    h = 1.0 / 16
+    tpl = LeafTemplate((h,) * d, p, "drop", False)
+    pts = []
+    for k in range(leaves):
+        lo = rng.integers(0, 16, size=d) * h
+        pts.append(tpl.leaf_grid(tpl.leaf_nodes1d(lo, lo + h))[tpl.interior_idx])
+    x = np.concatenate(pts)
+    r2 = ((x - 0.5) ** 2).sum(axis=1)
+    b = 1.0 - 0.5 * np.exp(-r2 / (2 * 0.15 ** 2))
+    n = tpl.n_interior
+    pack = np.empty((leaves, d + 1, n))
+    pack[:, :d] = 1.0 + 0.05 * rng.standard_normal((leaves, d, n))
+    pack[:, d] = (-kappa * kappa * b).reshape(leaves, n)
+    return tpl, pack
+
+
+@pytest.mark.parametrize("p,leaves", [(6, 300), (12, 6), (16, 2)])
+def test_batched_dtn_vs_oracle(p, leaves):
+    from paper_2503_04033_b200.engine import LeafEngine
+    tpl, pack = bump_pack(p, leaves, kappa=40.0, seed=p)
+    eng = LeafEngine(tpl, False, True, device=0)
+    dtn, stats = eng.dtn_host(pack)
+    otpl = O.OracleTemplate(tpl.widths, p)
+    check = range(leaves) if leaves <= 8 else range(0, leaves, 37)
+    for k in check:
+        ref, _, (dmin, dmax, _) = O.leaf_dtn(otpl, pack[k, :3].T, None, pack[k, 3])
+        assert rel(dtn[k], ref) <= TOL, (k, rel(dtn[k], ref))
+        assert np.isclose(stats[k, 1], dmax, rtol=1e-8)
+
+
+def test_device_and_host_paths_agree():
+    import torch
+    from paper_2503_04033_b200.engine import LeafEngine
+    tpl, pack = bump_pack(8, 40, kappa=10.0, seed=3)
+    eng = LeafEngine(tpl, False, True, device=0)
+    host, _ = eng.dtn_host(pack, chunk_leaves=7)
+    dev, _ = eng.dtn(torch.from_numpy(pack).cuda())
+    assert np.array_equal(host, dev.cpu().numpy())
+
+
+def test_two_dimensional_batch_vs_oracle():
+    from paper_2503_04033_b200.engine import LeafEngine
+    tpl, pack = bump_pack(9, 5, kappa=15.0, seed=4, d=2)
+    eng = LeafEngine(tpl, False, True, device=0)
+    dtn, _ = eng.dtn_host(pack)
+    otpl = O.OracleTemplate(tpl.widths, 9)
+    for k in range(5):
+        ref, _, _ = O.leaf_dtn(otpl, pack[k, :2].T, None, pack[k, 2])
+        assert rel(dtn[k], ref) <= TOL

@@ -63,6 +63,12 @@ int hps_plan_destroy(hps_plan_t plan);
 int hps_plan_info(hps_plan_t plan, int* n_interior, int* n_boundary, int* ncoef, int* slots,
                   size_t* dtn_slot_bytes, size_t* solve_slot_bytes);
 
+/* Diagnostics: when `counters` (device, [slots][16] uint64, zeroed by the
+ * caller) is set, every launch accumulates clock64 cycles per op kind
+ * (0 small panel, 1 swaps, 2/3 triangular inverses, 4/5 GEMM sub/set,
+ * 6 assembly, 7 output), GEMM MFLOP (8) and leaves (9) per slot.  NULL disables. */
+int hps_plan_set_profile(hps_plan_t plan, unsigned long long* counters);
+
 int hps_leaf_dtn(hps_plan_t plan, int n_leaves, const double* coeffs, double* dtn, double* stats,
                  void* stream);
 int hps_leaf_dtn_host(hps_plan_t plan, int n_leaves, const double* coeffs_host, double* dtn_host,

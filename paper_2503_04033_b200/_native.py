@@ -17,6 +17,7 @@ EXPORTS = (
     "hps_abi_version", "hps_last_error", "hps_device_count", "hps_plan_create",
     "hps_plan_destroy", "hps_plan_info", "hps_leaf_dtn", "hps_leaf_dtn_host",
     "hps_leaf_reduce_load", "hps_leaf_interior_solve", "hps_leaf_solution_operator",
+    "hps_plan_set_profile",
 )
 ABI_VERSION = 1
 
@@ -40,6 +41,7 @@ def _sig(lib):
     lib.hps_leaf_reduce_load.argtypes = [_P, _I, _P, _P, _P, _P, _P, _P]
     lib.hps_leaf_interior_solve.argtypes = [_P, _I, _P, _P, _P, _P, _P, _P]
     lib.hps_leaf_solution_operator.argtypes = [_P, _I, _P, _P, _P, _P]
+    lib.hps_plan_set_profile.argtypes = [_P, _P]
     for name in EXPORTS:
         if name not in ("hps_abi_version", "hps_last_error", "hps_device_count"):
             getattr(lib, name).restype = _I

@@ -24,7 +24,9 @@
 // inversions run on the same CTA between GEMMs; other SMs keep their tensor
 // pipes busy with their own leaves, so there is no grid-wide synchronisation.
 
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
@@ -78,7 +80,10 @@ struct LeafParams {
   double* out0;           // DTN: T (m*m); REDUCE: v (n); INTERIOR: u (n)
   double* out1;           // REDUCE: flux (m per leaf)
   double* stats;          // n_leaves * 2 : min |pivot|, max |pivot| over real columns
+  unsigned long long* prof;  // optional [slots][PROF_SLOTS] cycle counters (diagnostics)
 };
+
+constexpr int PROF_SLOTS = 16;  // 0..5 op kinds, 6 assemble, 7 output, 8 gemm flops/2^20, 9 leaves
 
 // ---------------------------------------------------------------------------
 // PTX helpers
@@ -101,14 +106,85 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 }
 
 // ---------------------------------------------------------------------------
-// GEMM engine: C[MxN] = (SUB ? C - A*B : A*B), A [MxK], B [KxN], row-major.
-// M, N multiples of 8 (edge tiles predicated); K multiple of KC; all row
-// starts 16-byte aligned.  In-place SET with C == B is legal when M <= TM.
+// mbarrier / TMA helpers
 // ---------------------------------------------------------------------------
 
-__device__ __forceinline__ void gemm(const bool SUB, const double* __restrict__ A, int lda,
-                                     const double* B, int ldb, double* C, int ldc, int M, int N,
-                                     int K, double* smem) {
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+// generic-proxy global writes of this thread become visible to later TMA (async-proxy) reads
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
+
+constexpr unsigned STAGE_BYTES = (unsigned)(STAGE_DBL * 8);
+
+// ---------------------------------------------------------------------------
+// Per-CTA context
+// ---------------------------------------------------------------------------
+
+struct TmaMaps {
+  CUtensorMap a_work;     // box {A_STRIDE, TM, 1} over [slots][NR][NC]
+  CUtensorMap b_work;     // box {B_STRIDE, KC, 1}
+  CUtensorMap a_scratch;  // box {A_STRIDE, TM, 1} over [slots][TRI][TRI]
+};
+
+struct Ctx {
+  double* M;
+  int ld, n_piv, n_real, NR, wb, slot;
+  int* piv;
+  double* scratch;
+  double* smem;
+  const TmaMaps* maps;
+  uint64_t* full;   // STAGES mbarriers: stage filled (TMA tx complete)
+  uint64_t* empty;  // STAGES mbarriers: stage released by all 8 warps
+  unsigned pipe;    // running stage counter, identical in every thread
+};
+
+// ---------------------------------------------------------------------------
+// GEMM engine: C[MxN] = (sub ? C - A*B : A*B) with A = M[ar.., ac..] (or the
+// slot's scratch block when a_scratch), B = M[br.., bc..], C = M[cr.., cc..].
+// Operand chunks (A 128x16, B 16x128 doubles) arrive by TMA into padded smem
+// stages (row strides 20 / 132 doubles: conflict-free m8n8k4 fragments);
+// thread 0 produces, all 8 warps consume and release stages through
+// mbarriers, so the mainloop has no block-wide barrier.  Out-of-range rows /
+// columns are zero-filled by TMA and masked in the epilogue.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void gemm(Ctx& c, const bool sub, const bool a_scratch, int ar, int ac,
+                                     int br, int bc, int cr, int cc, int M, int N, int K) {
   if (M <= 0 || N <= 0 || K <= 0) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wm = warp >> 2, wn = warp & 3;
@@ -117,41 +193,40 @@ __device__ __forceinline__ void gemm(const bool SUB, const double* __restrict__ 
   const int tiles = ((M + TM - 1) / TM) * tiles_n;
   const int kchunks = K / KC;
   const int total = tiles * kchunks;
+  double* smem = c.smem;
+  const CUtensorMap* mapA = a_scratch ? &c.maps->a_scratch : &c.maps->a_work;
+  const CUtensorMap* mapB = &c.maps->b_work;
+  double* C = c.M + (size_t)cr * c.ld + cc;
 
-  auto issue = [&](int it) {
-    if (it < total) {
-      const int tile = it / kchunks, kc = it - tile * kchunks;
-      const int tm = tile / tiles_n, tn = tile - tm * tiles_n;
-      double* sa = smem + (it % STAGES) * STAGE_DBL;
-      double* sb = sa + STAGE_A;
-#pragma unroll
-      for (int e = tid; e < TM * 8; e += NT) {
-        const int r = e >> 3, j = e & 7;
-        const int gr = tm * TM + r;
-        const double* src = A + (size_t)(gr < M ? gr : M - 1) * lda + kc * KC + 2 * j;
-        cp_async16(sa + r * A_STRIDE + 2 * j, src, gr < M ? 16 : 0);
-      }
-#pragma unroll
-      for (int e = tid; e < KC * 64; e += NT) {
-        const int k = e >> 6, j = e & 63;
-        const int gc = tn * TN + 2 * j;
-        const double* src = B + (size_t)(kc * KC + k) * ldb + (gc < N ? gc : N - 2);
-        cp_async16(sb + k * B_STRIDE + 2 * j, src, gc < N ? 16 : 0);
-      }
-      if (SUB && kc == 0) {
-        // warm L2 with the C tile this chunk sequence will update
-        for (int e = tid; e < TM * 8; e += NT) {
-          const int r = e >> 3, j = e & 7;
-          const int gr = tm * TM + r, gc = tn * TN + 16 * j;
-          if (gr < M && gc < N) prefetch_l2(C + (size_t)gr * ldc + gc);
-        }
-      }
+  // every thread's earlier global writes must be visible to the TMA reads below
+  fence_proxy_async_global();
+  __syncthreads();
+
+  // producer state (thread 0 only)
+  int p_it = 0, p_tile = 0, p_kc = 0;
+  auto produce = [&]() {
+    if (p_it >= total) return;
+    const unsigned g = c.pipe + p_it;
+    const unsigned s = g % STAGES, use = g / STAGES;
+    if (use > 0) mbar_wait(&c.empty[s], (use - 1) & 1);
+    const int tm = p_tile / tiles_n, tn = p_tile - tm * tiles_n;
+    double* sa = smem + s * STAGE_DBL;
+    double* sb = sa + STAGE_A;
+    mbar_expect_tx(&c.full[s], STAGE_BYTES);
+    if (a_scratch)
+      tma_load_3d(sa, mapA, p_kc * KC, tm * TM, c.slot, &c.full[s]);
+    else
+      tma_load_3d(sa, mapA, ac + p_kc * KC, ar + tm * TM, c.slot, &c.full[s]);
+    tma_load_3d(sb, mapB, bc + tn * TN, br + p_kc * KC, c.slot, &c.full[s]);
+    if (sub && p_kc == 0) {
+      for (int r = 0; r < TM; r += KC) tma_prefetch_3d(mapB, cc + tn * TN, cr + tm * TM + r, c.slot);
     }
-    cp_async_commit();
+    ++p_it;
+    if (++p_kc == kchunks) { p_kc = 0; ++p_tile; }
   };
-
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) issue(s);
+  if (tid == 0) {
+    for (int s = 0; s < STAGES - 1; ++s) produce();
+  }
 
   double acc[8][4][2];
 #pragma unroll
@@ -159,11 +234,13 @@ __device__ __forceinline__ void gemm(const bool SUB, const double* __restrict__ 
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+  int tile = 0, kc = 0;
   for (int it = 0; it < total; ++it) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    issue(it + STAGES - 1);
-    const double* sa = smem + (it % STAGES) * STAGE_DBL;
+    if (tid == 0) produce();
+    const unsigned g = c.pipe + it;
+    const unsigned s = g % STAGES;
+    mbar_wait(&c.full[s], (g / STAGES) & 1);
+    const double* sa = smem + s * STAGE_DBL;
     const double* sb = sa + STAGE_A;
 #pragma unroll
     for (int ks = 0; ks < KC; ks += 4) {
@@ -177,9 +254,12 @@ __device__ __forceinline__ void gemm(const bool SUB, const double* __restrict__ 
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
     }
-    const int tile = it / kchunks;
-    if (it - tile * kchunks == kchunks - 1) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&c.empty[s]);
+    if (++kc == kchunks) {
+      kc = 0;
       const int tm = tile / tiles_n, tn = tile - tm * tiles_n;
+      ++tile;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int row = tm * TM + wm * 64 + i * 8 + lr;
@@ -187,10 +267,10 @@ __device__ __forceinline__ void gemm(const bool SUB, const double* __restrict__ 
         for (int j = 0; j < 4; ++j) {
           const int col = tn * TN + wn * 32 + j * 8 + 2 * lc;
           if (row < M && col < N) {
-            double2* cp = reinterpret_cast<double2*>(C + (size_t)row * ldc + col);
+            double2* cp = reinterpret_cast<double2*>(C + (size_t)row * c.ld + col);
             double2 v;
-            if (SUB) {
-              double2 old = *cp;
+            if (sub) {
+              const double2 old = *cp;
               v.x = old.x - acc[i][j][0];
               v.y = old.y - acc[i][j][1];
             } else {
@@ -204,21 +284,9 @@ __device__ __forceinline__ void gemm(const bool SUB, const double* __restrict__ 
       }
     }
   }
-  cp_async_wait<0>();
+  c.pipe += total;
   __syncthreads();
 }
-
-// ---------------------------------------------------------------------------
-// Per-CTA LU context
-// ---------------------------------------------------------------------------
-
-struct Ctx {
-  double* M;
-  int ld, n_piv, n_real, NR, wb;
-  int* piv;
-  double* scratch;
-  double* smem;
-};
 
 __shared__ double s_pmin, s_pmax;
 __shared__ double s_redv[NT / 32];
@@ -555,10 +623,25 @@ __device__ void assemble(const LeafParams& P, double* M, int leaf) {
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(NT, 1) hps_leaf_kernel(LeafParams P, const Op* __restrict__ ops, int n_ops) {
-  extern __shared__ __align__(16) double smem[];
+__global__ void __launch_bounds__(NT, 1)
+    hps_leaf_kernel(LeafParams P, const Op* __restrict__ ops, int n_ops, const __grid_constant__ TmaMaps maps) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t bars[2 * STAGES];
   const int slot = blockIdx.x;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&bars[s], 1);
+      mbar_init(&bars[STAGES + s], NT / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
   Ctx c;
+  c.slot = slot;
+  c.maps = &maps;
+  c.full = bars;
+  c.empty = bars + STAGES;
+  c.pipe = 0;
   c.M = P.work + (size_t)slot * P.slot_stride;
   c.ld = P.ld;
   c.n_piv = P.n_pad;
@@ -569,12 +652,16 @@ __global__ void __launch_bounds__(NT, 1) hps_leaf_kernel(LeafParams P, const Op*
   c.scratch = P.scratch + (size_t)slot * TRI_BLOCK * TRI_BLOCK;
   c.smem = smem;
 
+  unsigned long long* prof = P.prof ? P.prof + (size_t)slot * PROF_SLOTS : nullptr;
   for (int leaf = blockIdx.x; leaf < P.n_leaves; leaf += gridDim.x) {
+    long long t0 = clock64();
     assemble(P, c.M, leaf);
     if (threadIdx.x == 0) { s_pmin = INFINITY; s_pmax = 0.0; }
     __syncthreads();
+    if (prof && threadIdx.x == 0) { prof[6] += clock64() - t0; prof[9] += 1; }
     for (int k = 0; k < n_ops; ++k) {
       const Op op = ops[k];
+      if (prof) t0 = clock64();
       switch (op.kind) {
         case OP_SMALL: lu_small(c, op.a, op.b); break;
         case OP_SWAP: apply_swaps(c, op.a, op.b, op.c, op.d); break;
@@ -582,12 +669,15 @@ __global__ void __launch_bounds__(NT, 1) hps_leaf_kernel(LeafParams P, const Op*
         case OP_INV_UPPER: invert_upper(c, op.a, op.b); break;
         default: {
           const bool sub = (op.kind == OP_GEMM_SUB);
-          const double* A = sub ? c.M + (size_t)op.ar * c.ld + op.ac : c.scratch;
-          gemm(sub, A, sub ? c.ld : TRI_BLOCK, c.M + (size_t)op.br * c.ld + op.bc, c.ld,
-               c.M + (size_t)op.cr * c.ld + op.cc, c.ld, op.Mdim, op.Ndim, op.Kdim, c.smem);
+          gemm(c, sub, !sub, op.ar, op.ac, op.br, op.bc, op.cr, op.cc, op.Mdim, op.Ndim, op.Kdim);
         }
       }
+      if (prof && threadIdx.x == 0) {
+        prof[op.kind] += clock64() - t0;
+        if (op.kind >= OP_GEMM_SUB) prof[8] += (2ull * op.Mdim * op.Ndim * op.Kdim) >> 20;
+      }
     }
+    if (prof) t0 = clock64();
     if (P.mode == MODE_DTN) {
       double* T = P.out0 + (size_t)leaf * P.m * P.m;
       for (int e = threadIdx.x; e < P.m * P.m; e += NT) {
@@ -626,6 +716,7 @@ __global__ void __launch_bounds__(NT, 1) hps_leaf_kernel(LeafParams P, const Op*
       P.stats[2 * leaf + 1] = s_pmax;
     }
     __syncthreads();
+    if (prof && threadIdx.x == 0) prof[7] += clock64() - t0;
   }
 }
 
@@ -720,7 +811,37 @@ struct hps_plan_s {
   Op* prog[4] = {nullptr, nullptr, nullptr, nullptr};
   int prog_len[4] = {0, 0, 0, 0};
   double* h_stage = nullptr;
+  unsigned long long* prof = nullptr;  // diagnostics counters (device), optional
+  TmaMaps maps[4];
+  int maps_ok[4] = {0, 0, 0, 0};
 };
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+static int make_map(CUtensorMap* map, double* base, uint64_t cols, uint64_t rows, uint64_t slots,
+                    uint64_t ld, uint64_t slot_stride, uint32_t box_cols, uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return fail("cuTensorMapEncodeTiled unavailable from the driver");
+  cuuint64_t dims[3] = {cols, rows, slots};
+  cuuint64_t strides[2] = {ld * 8, slot_stride * 8};
+  cuuint32_t box[3] = {box_cols, box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return 0;
+}
 
 static int round16(int x) { return (x + 15) / 16 * 16; }
 
@@ -752,7 +873,20 @@ static int ensure_workspace(hps_plan_s* P, int mode, int want_slots) {
     if (fit < 1) return fail("memory budget cannot hold one leaf workspace");
     if ((size_t)slots > fit) slots = (int)fit;
   }
-  if (P->work && P->work_doubles >= per * (size_t)slots && P->ws_slots >= slots) return slots;
+  if (P->work && P->work_doubles >= per * (size_t)slots && P->ws_slots >= slots) {
+    if (!P->maps_ok[mode]) {
+      int NR, NC;
+      mode_dims(P, mode, &NR, &NC);
+      TmaMaps& m = P->maps[mode];
+      if (make_map(&m.a_work, P->work, NC, NR, P->ws_slots, NC, per, A_STRIDE, TM) ||
+          make_map(&m.b_work, P->work, NC, NR, P->ws_slots, NC, per, B_STRIDE, KC) ||
+          make_map(&m.a_scratch, P->scratch, TRI_BLOCK, TRI_BLOCK, P->ws_slots, TRI_BLOCK,
+                   TRI_BLOCK * TRI_BLOCK, A_STRIDE, TM))
+        return -1;
+      P->maps_ok[mode] = 1;
+    }
+    return slots;
+  }
   if (P->work) cudaFree(P->work);
   if (P->piv) cudaFree(P->piv);
   if (P->scratch) cudaFree(P->scratch);
@@ -762,7 +896,8 @@ static int ensure_workspace(hps_plan_s* P, int mode, int want_slots) {
   CK(cudaMalloc(&P->scratch, (size_t)TRI_BLOCK * TRI_BLOCK * slots * 8));
   P->work_doubles = per * (size_t)slots;
   P->ws_slots = slots;
-  return slots;
+  for (int k = 0; k < 4; ++k) P->maps_ok[k] = 0;
+  return ensure_workspace(P, mode, want_slots);
 }
 
 static int ensure_program(hps_plan_s* P, int mode) {
@@ -805,13 +940,14 @@ static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, c
   L.slot_stride = slot_doubles(P, mode);
   L.work = P->work; L.piv = P->piv; L.scratch = P->scratch;
   L.D1 = P->D1; L.D2 = P->D2; L.a_bi = P->a_bi; L.a_bb = P->a_bb;
+  L.prof = P->prof;
   L.coeffs = coeffs; L.in0 = in0; L.in1 = in1; L.out0 = out0; L.out1 = out1; L.stats = stats;
   const int panel_bytes = P->n_pad * P->wb * 8;
   int smem = GEMM_SMEM_BYTES;
   if (panel_bytes > smem) smem = panel_bytes;
   if (TRI_BLOCK * TRI_BLOCK * 8 > smem) smem = TRI_BLOCK * TRI_BLOCK * 8;
   CK(cudaFuncSetAttribute(hps_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  hps_leaf_kernel<<<slots, NT, smem, stream>>>(L, P->prog[mode], P->prog_len[mode]);
+  hps_leaf_kernel<<<slots, NT, smem, stream>>>(L, P->prog[mode], P->prog_len[mode], P->maps[mode]);
   CK(cudaGetLastError());
   return 0;
 }
@@ -877,6 +1013,12 @@ int hps_plan_destroy(hps_plan_t P) {
   for (int k = 0; k < 4; ++k) cudaFree(P->prog[k]);
   if (P->h_stage) cudaFreeHost(P->h_stage);
   delete P;
+  return 0;
+}
+
+int hps_plan_set_profile(hps_plan_t P, unsigned long long* counters) {
+  if (!P) return fail("null plan");
+  P->prof = counters;
   return 0;
 }
 

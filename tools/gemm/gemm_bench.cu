@@ -1,0 +1,60 @@
+// Standalone throughput probe of the leaf engine's TMA/DMMA GEMM device routine.
+// Each CTA (one per SM) runs C[MxN] -= A[MxK] B[KxN] on its own slot, `reps` times.
+#include "../../paper_2503_04033_b200/csrc/hps_leaf.cu"
+
+namespace {
+__global__ void __launch_bounds__(NT, 1) gemm_probe(double* base, size_t stride, int ld, int M, int N,
+                                                    int K, int reps, const __grid_constant__ TmaMaps maps) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t bars[2 * STAGES];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&bars[s], 1); mbar_init(&bars[STAGES + s], NT / 32); }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  Ctx c;
+  c.M = base + (size_t)blockIdx.x * stride;
+  c.ld = ld; c.slot = blockIdx.x; c.smem = smem; c.maps = &maps;
+  c.full = bars; c.empty = bars + STAGES; c.pipe = 0;
+  for (int r = 0; r < reps; ++r) gemm(c, true, false, 0, 0, M, 0, M + K, 0, M, N, K);
+}
+}  // namespace
+
+int main() {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  struct Shape { int M, N, K; };
+  Shape shapes[] = {{2560, 1376, 1376}, {1184, 1184, 2752}, {1024, 1024, 128}, {2048, 128, 128},
+                    {3936, 64, 64}, {128, 1184, 128}, {3936, 32, 32}};
+  cudaFuncSetAttribute(gemm_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM_BYTES);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  for (auto s : shapes) {
+    int ld = ((s.K > s.N ? s.K : s.N) + 15) / 16 * 16;
+    int NR = 2 * s.M + s.K;
+    size_t stride = (size_t)NR * ld;
+    double* buf;
+    cudaMalloc(&buf, stride * sms * 8);
+    cudaMemset(buf, 0, stride * sms * 8);
+    TmaMaps maps;
+    make_map(&maps.a_work, buf, ld, NR, sms, ld, stride, A_STRIDE, TM);
+    make_map(&maps.b_work, buf, ld, NR, sms, ld, stride, B_STRIDE, KC);
+    maps.a_scratch = maps.a_work;
+    double fl = 2.0 * s.M * s.N * s.K;
+    int reps = (int)(2e10 / fl + 1);
+    if (reps > 200) reps = 200;
+    gemm_probe<<<sms, NT, GEMM_SMEM_BYTES>>>(buf, stride, ld, s.M, s.N, s.K, 1, maps);
+    cudaEventRecord(e0);
+    gemm_probe<<<sms, NT, GEMM_SMEM_BYTES>>>(buf, stride, ld, s.M, s.N, s.K, reps, maps);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    double tiles = (double)((s.M + 127) / 128) * ((s.N + 127) / 128) * 128 * 128 * 2.0 * s.K;
+    printf("M=%5d N=%5d K=%5d: %6.2f TFLOP/s useful, %6.2f tile-TFLOP/s (%.1f GF/s/SM useful) %s\n",
+           s.M, s.N, s.K, fl * reps * sms / ms / 1e9, tiles * reps * sms / ms / 1e9,
+           fl * reps / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
+    cudaFree(buf);
+  }
+  return 0;
+}

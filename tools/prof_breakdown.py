@@ -1,0 +1,41 @@
+"""Per-op-kind cycle breakdown of hps_leaf_kernel (clock64 counters, diagnostics build path)."""
+import argparse, ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import bench
+from paper_2503_04033_b200.engine import LeafEngine, dtn_flops
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--p", type=int, default=16)
+ap.add_argument("--leaves", type=int, default=296)
+ap.add_argument("--mode", default="dtn")
+a = ap.parse_args()
+tpl, pack = bench.make_shard(a.p, 16, 40.0, 0, 1, a.leaves)
+eng = LeafEngine(tpl, False, True)
+coeffs = torch.from_numpy(pack).cuda()
+f = torch.randn(a.leaves, eng.n, dtype=torch.float64, device="cuda")
+def run():
+    if a.mode == "dtn":
+        eng.dtn(coeffs)
+    else:
+        eng.reduce_load(coeffs, f)
+run(); torch.cuda.synchronize()
+cnt = torch.zeros(eng.slots * 16, dtype=torch.int64, device="cuda")
+eng.lib.hps_plan_set_profile(eng.plan, ctypes.c_void_p(cnt.data_ptr()))
+e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+e0.record(); run(); e1.record(); torch.cuda.synchronize()
+eng.lib.hps_plan_set_profile(eng.plan, ctypes.c_void_p(0))
+ms = e0.elapsed_time(e1)
+c = cnt.view(eng.slots, 16).cpu().numpy().astype(float)
+names = ["small-panel", "swaps", "inv-lower", "inv-upper", "gemm-sub", "gemm-set", "assemble", "output"]
+tot = c[:, :8].sum()
+leaves = c[:, 9].sum()
+print(f"p={a.p} leaves={a.leaves} mode={a.mode} kernel {ms:.1f} ms, "
+      f"{a.leaves*dtn_flops(eng.n, eng.m)/ms/1e9:.2f} TFLOP/s (reference flop count)")
+clk = 1.965e9
+for i, nm in enumerate(names):
+    print(f"  {nm:12s} {100*c[:, i].sum()/tot:6.2f}%   {c[:, i].sum()/leaves/clk*1e3:8.2f} ms/leaf")
+gf = c[:, 8].sum() * 2**20
+print(f"  gemm flops/leaf {gf/leaves:.3e}; gemm-only rate per SM {gf/(c[:, 4].sum()+c[:, 5].sum())*clk/1e9:.1f} GFLOP/s "
+      f"(peak 251/SM); per-leaf total {tot/leaves/clk*1e3:.1f} ms")

@@ -49,7 +49,8 @@ constexpr int B_STRIDE = 132;    // doubles; 1056 B rows -> conflict-free B frag
 constexpr int STAGE_A = TM * A_STRIDE;
 constexpr int STAGE_B = KC * B_STRIDE;
 constexpr int STAGE_DBL = STAGE_A + STAGE_B;
-constexpr int GEMM_SMEM_BYTES = STAGES * STAGE_DBL * 8;
+constexpr int EPI_DBL = 2 * 2 * 8 * 16;  // per warp: 2 ring slots x two [8][16] blocks
+constexpr int GEMM_SMEM_BYTES = (STAGES * STAGE_DBL + (NT / 32) * EPI_DBL) * 8;
 constexpr int TRI_BLOCK = 128;   // triangular base block (explicit inverse + GEMM)
 constexpr int SMALL_PANEL = 32;  // recursion leaf width handled by rank-wb updates
 constexpr int RHS_COLS = 16;     // padded rhs block in solve mode
@@ -144,6 +145,22 @@ __device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, 
                "r"(c0), "r"(c1), "r"(c2)
                : "memory");
 }
+__device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* map, int c0, int c1, int c2,
+                                                  const void* src) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
 // generic-proxy global writes of this thread become visible to later TMA (async-proxy) reads
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;\n" ::: "memory");
@@ -159,6 +176,7 @@ struct TmaMaps {
   CUtensorMap a_work;     // box {A_STRIDE, TM, 1} over [slots][NR][NC]
   CUtensorMap b_work;     // box {B_STRIDE, KC, 1}
   CUtensorMap a_scratch;  // box {A_STRIDE, TM, 1} over [slots][TRI][TRI]
+  CUtensorMap c_red;      // box {16, 8, 1} over [slots][NR][NC]: epilogue reduce-add
 };
 
 struct Ctx {
@@ -260,6 +278,35 @@ __device__ __forceinline__ void gemm(Ctx& c, const bool sub, const bool a_scratc
       kc = 0;
       const int tm = tile / tiles_n, tn = tile - tm * tiles_n;
       ++tile;
+      if (sub) {
+        // C -= acc through TMA reduce-add in L2: -acc goes to a per-warp smem ring
+        // (two [8][16] blocks per m-tile) and drains asynchronously.
+        double* ring = smem + STAGES * STAGE_DBL + warp * EPI_DBL;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int row0 = tm * TM + wm * 64 + i * 8;
+          if (row0 < M) {
+            double* buf = ring + (i & 1) * 256;
+            if (lane == 0) bulk_wait_read1();
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              *reinterpret_cast<double2*>(buf + (j >> 1) * 128 + lr * 16 + (j & 1) * 8 + 2 * lc) =
+                  make_double2(-acc[i][j][0], -acc[i][j][1]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              const int col0 = tn * TN + wn * 32;
+              if (col0 < N) tma_reduce_add_3d(&c.maps->c_red, cc + col0, cr + row0, c.slot, buf);
+              if (col0 + 16 < N) tma_reduce_add_3d(&c.maps->c_red, cc + col0 + 16, cr + row0, c.slot, buf + 128);
+              bulk_commit();
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        }
+        continue;
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int row = tm * TM + wm * 64 + i * 8 + lr;
@@ -285,6 +332,10 @@ __device__ __forceinline__ void gemm(Ctx& c, const bool sub, const bool a_scratc
     }
   }
   c.pipe += total;
+  if (sub && lane == 0) {
+    bulk_wait_all();
+    fence_proxy_async_global();
+  }
   __syncthreads();
 }
 
@@ -881,7 +932,8 @@ static int ensure_workspace(hps_plan_s* P, int mode, int want_slots) {
       if (make_map(&m.a_work, P->work, NC, NR, P->ws_slots, NC, per, A_STRIDE, TM) ||
           make_map(&m.b_work, P->work, NC, NR, P->ws_slots, NC, per, B_STRIDE, KC) ||
           make_map(&m.a_scratch, P->scratch, TRI_BLOCK, TRI_BLOCK, P->ws_slots, TRI_BLOCK,
-                   TRI_BLOCK * TRI_BLOCK, A_STRIDE, TM))
+                   TRI_BLOCK * TRI_BLOCK, A_STRIDE, TM) ||
+          make_map(&m.c_red, P->work, NC, NR, P->ws_slots, NC, per, 16, 8))
         return -1;
       P->maps_ok[mode] = 1;
     }

@@ -40,6 +40,7 @@ int main() {
     make_map(&maps.a_work, buf, ld, NR, sms, ld, stride, A_STRIDE, TM);
     make_map(&maps.b_work, buf, ld, NR, sms, ld, stride, B_STRIDE, KC);
     maps.a_scratch = maps.a_work;
+    make_map(&maps.c_red, buf, ld, NR, sms, ld, stride, 16, 8);
     double fl = 2.0 * s.M * s.N * s.K;
     int reps = (int)(2e10 / fl + 1);
     if (reps > 200) reps = 200;

@@ -39,11 +39,12 @@
 
 namespace {
 
-constexpr int NT = 256;          // threads per CTA
-constexpr int TM = 128;          // GEMM tile rows
+constexpr int NT = 128;          // threads per CTA (4 warps); two CTAs (two leaves) per SM
+constexpr int CTAS_PER_SM = 2;
+constexpr int TM = 64;           // GEMM tile rows (1 x 4 warps of 64 x 32)
 constexpr int TN = 128;          // GEMM tile cols
 constexpr int KC = 16;           // k-chunk per pipeline stage
-constexpr int STAGES = 4;
+constexpr int STAGES = 3;
 constexpr int A_STRIDE = 20;     // doubles; 160 B rows -> conflict-free m8n8k4 A fragments
 constexpr int B_STRIDE = 132;    // doubles; 1056 B rows -> conflict-free B fragments
 constexpr int STAGE_A = TM * A_STRIDE;
@@ -51,10 +52,10 @@ constexpr int STAGE_B = KC * B_STRIDE;
 constexpr int STAGE_DBL = STAGE_A + STAGE_B;
 constexpr int EPI_DBL = 2 * 2 * 8 * 16;  // per warp: 2 ring slots x two [8][16] blocks
 constexpr int GEMM_SMEM_BYTES = (STAGES * STAGE_DBL + (NT / 32) * EPI_DBL) * 8;
-constexpr int TRI_BLOCK = 128;   // triangular base block (explicit inverse + GEMM)
+constexpr int TRI_BLOCK = 64;    // triangular base block (explicit inverse + GEMM)
 constexpr int SMALL_PANEL = 32;  // recursion leaf width handled by rank-wb updates
 constexpr int RHS_COLS = 16;     // padded rhs block in solve mode
-constexpr int PANEL_SMEM_CAP = 200 * 1024;
+constexpr int PANEL_SMEM_CAP = 96 * 1024;
 
 enum { MODE_DTN = 0, MODE_REDUCE = 1, MODE_INTERIOR = 2, MODE_SOLOP = 3 };
 
@@ -185,6 +186,7 @@ struct Ctx {
   int* piv;
   double* scratch;
   double* smem;
+  unsigned long long* prof;
   const TmaMaps* maps;
   uint64_t* full;   // STAGES mbarriers: stage filled (TMA tx complete)
   uint64_t* empty;  // STAGES mbarriers: stage released by all 8 warps
@@ -364,23 +366,150 @@ __device__ void apply_swaps(const Ctx& c, int j0, int cnt, int c_lo, int c_hi) {
   __syncthreads();
 }
 
-// Factor columns [b0, b0+wb): candidate rows [b0, n_piv) in shared memory,
-// non-candidate rows [n_piv, NR) by a triangular solve with the new U block.
-__device__ void base_factor(Ctx& c, int b0, int wb) {
+// ---------------------------------------------------------------------------
+// Narrow panel (<= SMALL_PANEL columns), left-looking in blocks of WB columns.
+// For block [b0, b0+WB) of the panel [c0, c0+w):
+//   1. the U rows above the block (rows [c0, b0)) by forward substitution with
+//      the panel's unit-lower L (staged in smem, warp-parallel dot products);
+//   2. one coalesced warp-per-row pass over rows [b0, NR) reading the contiguous
+//      segment [c0, b0+WB) and applying every earlier block's update at once
+//      (partial products + warp reduce-scatter); candidate rows land in smem;
+//   3. partial pivoting on the smem block (max |a|, lowest index on ties, as
+//      LAPACK's idamax);
+//   4. write-back, and L = A U^{-1} for the non-candidate rows;
+//   5. the block's row interchanges applied to the rest of the panel segment
+//      as one permutation gather.
+// ---------------------------------------------------------------------------
+
+__shared__ int s_swp_dst[16], s_swp_src[16], s_swp_cnt;
+
+// Lane-sum of p[j] over the warp; on return lane holds the full sum for column
+// jout (= the high bits of lane after log2(WB) halving steps).
+template <int WB>
+__device__ __forceinline__ double reduce_scatter(double (&p)[WB], int lane, int& jout) {
+  int jb = 0;
+#pragma unroll
+  for (int half = WB / 2, off = 16; half >= 1; half /= 2, off /= 2) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const double send = up ? p[i] : p[i + half];
+      const double keep = up ? p[i + half] : p[i];
+      p[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+    if (up) jb += half;
+  }
+  double v = p[0];
+#pragma unroll
+  for (int off = 16 / WB; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  jout = jb;
+  return v;
+}
+
+template <int WB>
+__device__ void panel_block(Ctx& c, int c0, int w, int b0) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = NT / 32;
+  constexpr int GROUP = 32 / WB;  // lanes sharing one column of the reduce-scatter
   const int n_cand = c.n_piv - b0;
-  double* S = c.smem;
-  __syncthreads();
-  for (int e = tid; e < n_cand * wb; e += NT) {
-    const int r = e / wb, j = e - r * wb;
-    S[e] = c.M[(size_t)(b0 + r) * c.ld + b0 + j];
+  const int done = b0 - c0, len = done + WB;
+  double* S = c.smem;                          // n_cand x WB
+  // staging T (<= 32 x 32) and Q (<= 16 x 32) alias S; Ut sits after all of them
+  double* Ut = c.smem + (size_t)max(c.n_piv * WB, 1024);  // WB x 32, Ut[j*32 + kk]
+  unsigned long long* prof = c.prof;
+  long long tp = (prof && tid == 0) ? clock64() : 0;
+#define PANEL_TICK(slot)                                   \
+  if (prof && tid == 0) {                                  \
+    const long long now = clock64();                       \
+    prof[slot] += now - tp;                                \
+    tp = now;                                              \
   }
   __syncthreads();
-  for (int j = 0; j < wb; ++j) {
+  if (done > 0) {
+    // 1. U rows above the block
+    double* T = c.smem;  // done x 32 staging of rows [c0, b0), cols [c0, b0+WB)
+    for (int e = tid; e < done * len; e += NT) {
+      const int kk = e / len, q = e - kk * len;
+      T[kk * 32 + q] = c.M[(size_t)(c0 + kk) * c.ld + c0 + q];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      for (int kk = 0; kk < done; ++kk) {
+        double p[WB];
+        const double t = (lane < kk) ? T[kk * 32 + lane] : 0.0;
+#pragma unroll
+        for (int j = 0; j < WB; ++j) p[j] = (lane < kk) ? t * Ut[j * 32 + lane] : 0.0;
+        int jj;
+        const double sum = reduce_scatter<WB>(p, lane, jj);
+        const double v = T[kk * 32 + done + jj] - sum;
+        if ((lane & (GROUP - 1)) == 0) {
+          Ut[jj * 32 + kk] = v;
+          c.M[(size_t)(c0 + kk) * c.ld + b0 + jj] = v;
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    PANEL_TICK(10)
+    // 2. fused update + gather as a thin DMMA GEMM:
+    //    V[rows x WB] = A_blk - L_seg[rows x done] * Ut^T[done x WB]
+    //    8-row groups per warp (m8n8k4: A fragments straight from global,
+    //    B fragments = Ut held in registers), G groups in flight.
+    constexpr int G = 4;
+    const int nkq = (done + 3) >> 2;
+    const int lr = lane >> 2, lc = lane & 3;
+    double bfr[8];
+#pragma unroll
+    for (int kq = 0; kq < 8; ++kq) {
+      const int k = kq * 4 + lc;
+      bfr[kq] = (kq < nkq && lr < WB && k < done) ? Ut[lr * 32 + k] : 0.0;
+    }
+    const bool owns = 2 * lc < WB;  // lane holds output columns 2lc, 2lc+1
+    for (int g0 = b0 + warp * 8 * G; g0 < c.NR; g0 += NW * 8 * G) {
+      double af[G][8], av[G][2];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const int r = g0 + g * 8 + lr;
+        const bool ok = r < c.NR;
+        const double* row = c.M + (size_t)(ok ? r : c.NR - 1) * c.ld;
+#pragma unroll
+        for (int kq = 0; kq < 8; ++kq) af[g][kq] = (ok && kq < nkq) ? row[c0 + kq * 4 + lc] : 0.0;
+        av[g][0] = (ok && owns) ? row[b0 + 2 * lc] : 0.0;
+        av[g][1] = (ok && owns && 2 * lc + 1 < WB) ? row[b0 + 2 * lc + 1] : 0.0;
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        double acc[2] = {0.0, 0.0};
+#pragma unroll
+        for (int kq = 0; kq < 8; ++kq)
+          if (kq < nkq) dmma(acc, af[g][kq], bfr[kq]);
+        const int r = g0 + g * 8 + lr;
+        if (r < c.NR && owns) {
+          const double v0 = av[g][0] - acc[0], v1 = av[g][1] - acc[1];
+          if (r < c.n_piv) {
+            S[(r - b0) * WB + 2 * lc] = v0;
+            if (2 * lc + 1 < WB) S[(r - b0) * WB + 2 * lc + 1] = v1;
+          } else {
+            c.M[(size_t)r * c.ld + b0 + 2 * lc] = v0;
+            if (2 * lc + 1 < WB) c.M[(size_t)r * c.ld + b0 + 2 * lc + 1] = v1;
+          }
+        }
+      }
+    }
+  } else {
+    for (int e = tid; e < n_cand * WB; e += NT) {
+      const int r = e / WB, j = e - r * WB;
+      S[e] = c.M[(size_t)(b0 + r) * c.ld + b0 + j];
+    }
+  }
+  __syncthreads();
+  PANEL_TICK(11)
+  // 3. partial pivoting on the block
+  for (int j = 0; j < WB; ++j) {
     double best = -1.0;
     int bidx = 0x7fffffff;
     for (int r = j + tid; r < n_cand; r += NT) {
-      const double v = fabs(S[r * wb + j]);
+      const double v = fabs(S[r * WB + j]);
       if (v > best) { best = v; bidx = r; }
     }
 #pragma unroll
@@ -394,8 +523,8 @@ __device__ void base_factor(Ctx& c, int b0, int wb) {
     if (tid == 0) {
       double bv = s_redv[0];
       int bi = s_redi[0];
-      for (int w = 1; w < NT / 32; ++w) {
-        if (s_redv[w] > bv || (s_redv[w] == bv && s_redi[w] < bi)) { bv = s_redv[w]; bi = s_redi[w]; }
+      for (int q = 1; q < NW; ++q) {
+        if (s_redv[q] > bv || (s_redv[q] == bv && s_redi[q] < bi)) { bv = s_redv[q]; bi = s_redi[q]; }
       }
       if (bi == 0x7fffffff) bi = j;
       s_pivot = bi;
@@ -403,13 +532,13 @@ __device__ void base_factor(Ctx& c, int b0, int wb) {
     }
     __syncthreads();
     const int pr = s_pivot;
-    if (pr != j && tid < wb) {
-      const double t = S[j * wb + tid];
-      S[j * wb + tid] = S[pr * wb + tid];
-      S[pr * wb + tid] = t;
+    if (pr != j && tid < WB) {
+      const double t = S[j * WB + tid];
+      S[j * WB + tid] = S[pr * WB + tid];
+      S[pr * WB + tid] = t;
     }
     __syncthreads();
-    const double pivot = S[j * wb + j];
+    const double pivot = S[j * WB + j];
     if (tid == 0 && b0 + j < c.n_real) {
       const double ap = fabs(pivot);
       s_pmin = fmin(s_pmin, ap);
@@ -417,71 +546,94 @@ __device__ void base_factor(Ctx& c, int b0, int wb) {
     }
     const double inv = (pivot != 0.0) ? 1.0 / pivot : 1.0;
     for (int r = j + 1 + tid; r < n_cand; r += NT) {
-      const double l = S[r * wb + j] * inv;
-      S[r * wb + j] = l;
-      for (int jj = j + 1; jj < wb; ++jj) S[r * wb + jj] -= l * S[j * wb + jj];
+      const double l = S[r * WB + j] * inv;
+      S[r * WB + j] = l;
+#pragma unroll
+      for (int jj = j + 1; jj < WB; ++jj) S[r * WB + jj] -= l * S[j * WB + jj];
     }
     __syncthreads();
   }
-  for (int e = tid; e < n_cand * wb; e += NT) {
-    const int r = e / wb, j = e - r * wb;
+  PANEL_TICK(12)
+  // 4. write-back; non-candidate rows L = A U^{-1}
+  for (int e = tid; e < n_cand * WB; e += NT) {
+    const int r = e / WB, j = e - r * WB;
     c.M[(size_t)(b0 + r) * c.ld + b0 + j] = S[e];
   }
-  // non-candidate rows: L = A U^{-1}
   for (int r = c.n_piv + tid; r < c.NR; r += NT) {
     double* row = c.M + (size_t)r * c.ld + b0;
-    double x[8];
-    for (int j = 0; j < wb; ++j) x[j] = row[j];
-    for (int j = 0; j < wb; ++j) {
+    double x[WB];
+#pragma unroll
+    for (int j = 0; j < WB; ++j) x[j] = row[j];
+#pragma unroll
+    for (int j = 0; j < WB; ++j) {
       double v = x[j];
-      for (int i = 0; i < j; ++i) v -= x[i] * S[i * wb + j];
-      const double pv = S[j * wb + j];
+#pragma unroll
+      for (int i = 0; i < j; ++i) v -= x[i] * S[i * WB + j];
+      const double pv = S[j * WB + j];
       x[j] = v * ((pv != 0.0) ? 1.0 / pv : 1.0);
     }
-    for (int j = 0; j < wb; ++j) row[j] = x[j];
+#pragma unroll
+    for (int j = 0; j < WB; ++j) row[j] = x[j];
   }
   __syncthreads();
+  PANEL_TICK(13)
+  // 5. the block's interchanges on the rest of the panel segment [c0, c0+w)
+  if (tid == 0) {
+    int rows[16], cont[16], cnt = 0;
+    for (int j = 0; j < WB; ++j) {
+      const int cand[2] = {b0 + j, c.piv[b0 + j]};
+      for (int t = 0; t < 2; ++t) {
+        bool seen = false;
+        for (int q = 0; q < cnt; ++q) seen |= (rows[q] == cand[t]);
+        if (!seen) { rows[cnt] = cand[t]; cont[cnt] = cand[t]; ++cnt; }
+      }
+    }
+    for (int j = 0; j < WB; ++j) {
+      int ia = 0, ib = 0;
+      for (int q = 0; q < cnt; ++q) {
+        if (rows[q] == b0 + j) ia = q;
+        if (rows[q] == c.piv[b0 + j]) ib = q;
+      }
+      const int t = cont[ia];
+      cont[ia] = cont[ib];
+      cont[ib] = t;
+    }
+    int n = 0;
+    for (int q = 0; q < cnt; ++q)
+      if (cont[q] != rows[q]) { s_swp_dst[n] = rows[q]; s_swp_src[n] = cont[q]; ++n; }
+    s_swp_cnt = n;
+  }
+  __syncthreads();
+  const int nsw = s_swp_cnt;
+  const int ncol = w - WB;  // panel columns outside the block
+  if (nsw > 0 && ncol > 0) {
+    double* Q = c.smem;  // nsw x 32 staging (S already written back)
+    for (int e = tid; e < nsw * ncol; e += NT) {
+      const int q = e / ncol, k = e - q * ncol;
+      const int col = (k < done) ? c0 + k : b0 + WB + (k - done);
+      Q[q * 32 + k] = c.M[(size_t)s_swp_src[q] * c.ld + col];
+    }
+    __syncthreads();
+    for (int e = tid; e < nsw * ncol; e += NT) {
+      const int q = e / ncol, k = e - q * ncol;
+      const int col = (k < done) ? c0 + k : b0 + WB + (k - done);
+      c.M[(size_t)s_swp_dst[q] * c.ld + col] = Q[q * 32 + k];
+    }
+  }
+  __syncthreads();
+  PANEL_TICK(14)
+#undef PANEL_TICK
 }
 
-// Columns [c0, c0+w), w <= SMALL_PANEL: base blocks with rank-wb updates.
+// Columns [c0, c0+w), w <= SMALL_PANEL.
 __device__ void lu_small(Ctx& c, int c0, int w) {
-  const int wb = c.wb;
-  const int tid = threadIdx.x;
-  for (int b0 = c0; b0 < c0 + w; b0 += wb) {
-    base_factor(c, b0, wb);
-    apply_swaps(c, b0, wb, c0, b0);
-    apply_swaps(c, b0, wb, b0 + wb, c0 + w);
-    const int cl = b0 + wb, ch = c0 + w;
-    if (cl >= ch) continue;
-    // U12 = L_bb^{-1} A12 on rows [b0, b0+wb)
-    for (int col = cl + tid; col < ch; col += NT) {
-      for (int i = 1; i < wb; ++i) {
-        double v = c.M[(size_t)(b0 + i) * c.ld + col];
-        for (int k = 0; k < i; ++k)
-          v -= c.M[(size_t)(b0 + i) * c.ld + b0 + k] * c.M[(size_t)(b0 + k) * c.ld + col];
-        c.M[(size_t)(b0 + i) * c.ld + col] = v;
-      }
+  for (int b0 = c0; b0 < c0 + w; b0 += c.wb) {
+    switch (c.wb) {
+      case 8: panel_block<8>(c, c0, w, b0); break;
+      case 4: panel_block<4>(c, c0, w, b0); break;
+      case 2: panel_block<2>(c, c0, w, b0); break;
+      default: panel_block<1>(c, c0, w, b0); break;
     }
-    __syncthreads();
-    // rank-wb update of rows [b0+wb, NR), cols [cl, ch)
-    const int ncols = ch - cl;
-    double* U = c.smem;  // wb x ncols
-    for (int e = tid; e < wb * ncols; e += NT) {
-      const int i = e / ncols, k = e - i * ncols;
-      U[e] = c.M[(size_t)(b0 + i) * c.ld + cl + k];
-    }
-    __syncthreads();
-    for (int r = b0 + wb + tid; r < c.NR; r += NT) {
-      double* row = c.M + (size_t)r * c.ld;
-      double l[8];
-      for (int i = 0; i < wb; ++i) l[i] = row[b0 + i];
-      for (int k = 0; k < ncols; ++k) {
-        double v = row[cl + k];
-        for (int i = 0; i < wb; ++i) v -= l[i] * U[i * ncols + k];
-        row[cl + k] = v;
-      }
-    }
-    __syncthreads();
   }
 }
 
@@ -674,7 +826,7 @@ __device__ void assemble(const LeafParams& P, double* M, int leaf) {
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, CTAS_PER_SM)
     hps_leaf_kernel(LeafParams P, const Op* __restrict__ ops, int n_ops, const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t bars[2 * STAGES];
@@ -704,6 +856,7 @@ __global__ void __launch_bounds__(NT, 1)
   c.smem = smem;
 
   unsigned long long* prof = P.prof ? P.prof + (size_t)slot * PROF_SLOTS : nullptr;
+  c.prof = prof;
   for (int leaf = blockIdx.x; leaf < P.n_leaves; leaf += gridDim.x) {
     long long t0 = clock64();
     assemble(P, c.M, leaf);
@@ -994,11 +1147,12 @@ static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, c
   L.D1 = P->D1; L.D2 = P->D2; L.a_bi = P->a_bi; L.a_bb = P->a_bb;
   L.prof = P->prof;
   L.coeffs = coeffs; L.in0 = in0; L.in1 = in1; L.out0 = out0; L.out1 = out1; L.stats = stats;
-  const int panel_bytes = P->n_pad * P->wb * 8;
+  const int panel_bytes = ((P->n_pad * P->wb > 1024 ? P->n_pad * P->wb : 1024) + 32 * P->wb) * 8;
   int smem = GEMM_SMEM_BYTES;
   if (panel_bytes > smem) smem = panel_bytes;
   if (TRI_BLOCK * TRI_BLOCK * 8 > smem) smem = TRI_BLOCK * TRI_BLOCK * 8;
   CK(cudaFuncSetAttribute(hps_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  CK(cudaFuncSetAttribute(hps_leaf_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   hps_leaf_kernel<<<slots, NT, smem, stream>>>(L, P->prog[mode], P->prog_len[mode], P->maps[mode]);
   CK(cudaGetLastError());
   return 0;
@@ -1035,12 +1189,13 @@ int hps_plan_create(hps_plan_t* out, int device, int dim, int p, int has_first, 
   P->has_zeroth = has_zeroth ? 1 : 0;
   P->ncoef = dim + (has_first ? dim : 0) + (has_zeroth ? 1 : 0);
   int wb = 8;
-  while (wb > 1 && (size_t)P->n_pad * wb * 8 > PANEL_SMEM_CAP) wb >>= 1;
+  while (wb > 1 && ((size_t)P->n_pad * wb + 32 * wb) * 8 > PANEL_SMEM_CAP) wb >>= 1;
+  // (the panel step also needs max(n_pad*wb, 1024) + 32*wb doubles; 1024 + 256 always fits)
   P->wb = wb;
   P->budget = workspace_budget_bytes;
   if (cudaSetDevice(device) != cudaSuccess) { delete P; return fail("cudaSetDevice failed"); }
   cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device);
-  P->slots = (max_slots > 0 && max_slots < P->sms) ? max_slots : P->sms;
+  P->slots = (max_slots > 0 && max_slots < CTAS_PER_SM * P->sms) ? max_slots : CTAS_PER_SM * P->sms;
   const size_t tab = (size_t)dim * p * p * 8;
   if (cudaMalloc(&P->D1, tab) != cudaSuccess || cudaMalloc(&P->D2, tab) != cudaSuccess ||
       cudaMalloc(&P->a_bi, (size_t)P->m * P->n * 8) != cudaSuccess ||

@@ -3,7 +3,7 @@
 #include "../../paper_2503_04033_b200/csrc/hps_leaf.cu"
 
 namespace {
-__global__ void __launch_bounds__(NT, 1) gemm_probe(double* base, size_t stride, int ld, int M, int N,
+__global__ void __launch_bounds__(NT, CTAS_PER_SM) gemm_probe(double* base, size_t stride, int ld, int M, int N,
                                                     int K, int reps, const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t bars[2 * STAGES];
@@ -15,7 +15,7 @@ __global__ void __launch_bounds__(NT, 1) gemm_probe(double* base, size_t stride,
   Ctx c;
   c.M = base + (size_t)blockIdx.x * stride;
   c.ld = ld; c.slot = blockIdx.x; c.smem = smem; c.maps = &maps;
-  c.full = bars; c.empty = bars + STAGES; c.pipe = 0;
+  c.full = bars; c.empty = bars + STAGES; c.pipe = 0; c.prof = nullptr;
   for (int r = 0; r < reps; ++r) gemm(c, true, false, 0, 0, M, 0, M + K, 0, M, N, K);
 }
 }  // namespace
@@ -27,6 +27,7 @@ int main() {
   Shape shapes[] = {{2560, 1376, 1376}, {1184, 1184, 2752}, {1024, 1024, 128}, {2048, 128, 128},
                     {3936, 64, 64}, {128, 1184, 128}, {3936, 32, 32}};
   cudaFuncSetAttribute(gemm_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM_BYTES);
+  cudaFuncSetAttribute(gemm_probe, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   for (auto s : shapes) {
@@ -34,27 +35,27 @@ int main() {
     int NR = 2 * s.M + s.K;
     size_t stride = (size_t)NR * ld;
     double* buf;
-    cudaMalloc(&buf, stride * sms * 8);
-    cudaMemset(buf, 0, stride * sms * 8);
+    cudaMalloc(&buf, stride * CTAS_PER_SM * sms * 8);
+    cudaMemset(buf, 0, stride * CTAS_PER_SM * sms * 8);
     TmaMaps maps;
-    make_map(&maps.a_work, buf, ld, NR, sms, ld, stride, A_STRIDE, TM);
-    make_map(&maps.b_work, buf, ld, NR, sms, ld, stride, B_STRIDE, KC);
+    make_map(&maps.a_work, buf, ld, NR, CTAS_PER_SM * sms, ld, stride, A_STRIDE, TM);
+    make_map(&maps.b_work, buf, ld, NR, CTAS_PER_SM * sms, ld, stride, B_STRIDE, KC);
     maps.a_scratch = maps.a_work;
-    make_map(&maps.c_red, buf, ld, NR, sms, ld, stride, 16, 8);
+    make_map(&maps.c_red, buf, ld, NR, CTAS_PER_SM * sms, ld, stride, 16, 8);
     double fl = 2.0 * s.M * s.N * s.K;
     int reps = (int)(2e10 / fl + 1);
     if (reps > 200) reps = 200;
-    gemm_probe<<<sms, NT, GEMM_SMEM_BYTES>>>(buf, stride, ld, s.M, s.N, s.K, 1, maps);
+    gemm_probe<<<CTAS_PER_SM * sms, NT, GEMM_SMEM_BYTES>>>(buf, stride, ld, s.M, s.N, s.K, 1, maps);
     cudaEventRecord(e0);
-    gemm_probe<<<sms, NT, GEMM_SMEM_BYTES>>>(buf, stride, ld, s.M, s.N, s.K, reps, maps);
+    gemm_probe<<<CTAS_PER_SM * sms, NT, GEMM_SMEM_BYTES>>>(buf, stride, ld, s.M, s.N, s.K, reps, maps);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
-    double tiles = (double)((s.M + 127) / 128) * ((s.N + 127) / 128) * 128 * 128 * 2.0 * s.K;
+    double tiles = (double)((s.M + TM - 1) / TM) * ((s.N + 127) / 128) * TM * 128 * 2.0 * s.K;
     printf("M=%5d N=%5d K=%5d: %6.2f TFLOP/s useful, %6.2f tile-TFLOP/s (%.1f GF/s/SM useful) %s\n",
-           s.M, s.N, s.K, fl * reps * sms / ms / 1e9, tiles * reps * sms / ms / 1e9,
-           fl * reps / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
+           s.M, s.N, s.K, fl * reps * CTAS_PER_SM * sms / ms / 1e9, tiles * reps * CTAS_PER_SM * sms / ms / 1e9,
+           CTAS_PER_SM * fl * reps / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
     cudaFree(buf);
   }
   return 0;

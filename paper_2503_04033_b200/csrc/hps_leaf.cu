@@ -44,9 +44,9 @@ constexpr int CTAS_PER_SM = 2;
 constexpr int TM = 64;           // GEMM tile rows (1 x 4 warps of 64 x 32)
 constexpr int TN = 128;          // GEMM tile cols
 constexpr int KC = 16;           // k-chunk per pipeline stage
-constexpr int STAGES = 3;
-constexpr int A_STRIDE = 20;     // doubles; 160 B rows -> conflict-free m8n8k4 A fragments
-constexpr int B_STRIDE = 132;    // doubles; 1056 B rows -> conflict-free B fragments
+constexpr int STAGES = 4;
+constexpr int A_STRIDE = KC;     // A box rows are 128 B, 128B-swizzled by TMA (1024 B aligned)
+constexpr int B_STRIDE = TN;     // B box rows are 1 KB, unswizzled
 constexpr int STAGE_A = TM * A_STRIDE;
 constexpr int STAGE_B = KC * B_STRIDE;
 constexpr int STAGE_DBL = STAGE_A + STAGE_B;
@@ -266,7 +266,11 @@ __device__ __forceinline__ void gemm(Ctx& c, const bool sub, const bool a_scratc
     for (int ks = 0; ks < KC; ks += 4) {
       double af[8], bf[4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) af[i] = sa[(wm * 64 + i * 8 + lr) * A_STRIDE + ks + lc];
+      for (int i = 0; i < 8; ++i) {
+        // 128B swizzle: 16-byte chunk index ^= row % 8  (row % 8 == lr here)
+        const int row = wm * 64 + i * 8 + lr, k = ks + lc;
+        af[i] = sa[row * A_STRIDE + ((((k >> 1) ^ lr) << 1) | (k & 1))];
+      }
 #pragma unroll
       for (int j = 0; j < 4; ++j) bf[j] = sb[(ks + lc) * B_STRIDE + wn * 32 + j * 8 + lr];
 #pragma unroll
@@ -828,7 +832,7 @@ __device__ void assemble(const LeafParams& P, double* M, int leaf) {
 
 __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     hps_leaf_kernel(LeafParams P, const Op* __restrict__ ops, int n_ops, const __grid_constant__ TmaMaps maps) {
-  extern __shared__ __align__(128) double smem[];
+  extern __shared__ __align__(1024) double smem[];
   __shared__ __align__(8) uint64_t bars[2 * STAGES];
   const int slot = blockIdx.x;
   if (threadIdx.x == 0) {
@@ -1033,7 +1037,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 static int make_map(CUtensorMap* map, double* base, uint64_t cols, uint64_t rows, uint64_t slots,
-                    uint64_t ld, uint64_t slot_stride, uint32_t box_cols, uint32_t box_rows) {
+                    uint64_t ld, uint64_t slot_stride, uint32_t box_cols, uint32_t box_rows,
+                    bool swizzle128 = false) {
   auto fn = encode_fn();
   if (!fn) return fail("cuTensorMapEncodeTiled unavailable from the driver");
   cuuint64_t dims[3] = {cols, rows, slots};
@@ -1041,7 +1046,8 @@ static int make_map(CUtensorMap* map, double* base, uint64_t cols, uint64_t rows
   cuuint32_t box[3] = {box_cols, box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return 0;
@@ -1082,10 +1088,10 @@ static int ensure_workspace(hps_plan_s* P, int mode, int want_slots) {
       int NR, NC;
       mode_dims(P, mode, &NR, &NC);
       TmaMaps& m = P->maps[mode];
-      if (make_map(&m.a_work, P->work, NC, NR, P->ws_slots, NC, per, A_STRIDE, TM) ||
+      if (make_map(&m.a_work, P->work, NC, NR, P->ws_slots, NC, per, A_STRIDE, TM, true) ||
           make_map(&m.b_work, P->work, NC, NR, P->ws_slots, NC, per, B_STRIDE, KC) ||
           make_map(&m.a_scratch, P->scratch, TRI_BLOCK, TRI_BLOCK, P->ws_slots, TRI_BLOCK,
-                   TRI_BLOCK * TRI_BLOCK, A_STRIDE, TM) ||
+                   TRI_BLOCK * TRI_BLOCK, A_STRIDE, TM, true) ||
           make_map(&m.c_red, P->work, NC, NR, P->ws_slots, NC, per, 16, 8))
         return -1;
       P->maps_ok[mode] = 1;

@@ -5,7 +5,7 @@
 namespace {
 __global__ void __launch_bounds__(NT, CTAS_PER_SM) gemm_probe(double* base, size_t stride, int ld, int M, int N,
                                                     int K, int reps, const __grid_constant__ TmaMaps maps) {
-  extern __shared__ __align__(128) double smem[];
+  extern __shared__ __align__(1024) double smem[];
   __shared__ __align__(8) uint64_t bars[2 * STAGES];
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&bars[s], 1); mbar_init(&bars[STAGES + s], NT / 32); }
@@ -20,14 +20,18 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) gemm_probe(double* base, size
 }
 }  // namespace
 
-int main() {
+int main(int argc, char** argv) {
   int sms = 0;
+  const int cps = argc > 1 ? atoi(argv[1]) : CTAS_PER_SM;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   struct Shape { int M, N, K; };
   Shape shapes[] = {{2560, 1376, 1376}, {1184, 1184, 2752}, {1024, 1024, 128}, {2048, 128, 128},
                     {3936, 64, 64}, {128, 1184, 128}, {3936, 32, 32}};
   cudaFuncSetAttribute(gemm_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM_BYTES);
   cudaFuncSetAttribute(gemm_probe, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemm_probe, NT, GEMM_SMEM_BYTES);
+  printf("occupancy: %d CTAs/SM at %d B dynamic smem\n", occ, GEMM_SMEM_BYTES);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   for (auto s : shapes) {
@@ -38,24 +42,24 @@ int main() {
     cudaMalloc(&buf, stride * CTAS_PER_SM * sms * 8);
     cudaMemset(buf, 0, stride * CTAS_PER_SM * sms * 8);
     TmaMaps maps;
-    make_map(&maps.a_work, buf, ld, NR, CTAS_PER_SM * sms, ld, stride, A_STRIDE, TM);
+    make_map(&maps.a_work, buf, ld, NR, CTAS_PER_SM * sms, ld, stride, A_STRIDE, TM, true);
     make_map(&maps.b_work, buf, ld, NR, CTAS_PER_SM * sms, ld, stride, B_STRIDE, KC);
     maps.a_scratch = maps.a_work;
     make_map(&maps.c_red, buf, ld, NR, CTAS_PER_SM * sms, ld, stride, 16, 8);
     double fl = 2.0 * s.M * s.N * s.K;
     int reps = (int)(2e10 / fl + 1);
     if (reps > 200) reps = 200;
-    gemm_probe<<<CTAS_PER_SM * sms, NT, GEMM_SMEM_BYTES>>>(buf, stride, ld, s.M, s.N, s.K, 1, maps);
+    gemm_probe<<<cps * sms, NT, GEMM_SMEM_BYTES>>>(buf, stride, ld, s.M, s.N, s.K, 1, maps);
     cudaEventRecord(e0);
-    gemm_probe<<<CTAS_PER_SM * sms, NT, GEMM_SMEM_BYTES>>>(buf, stride, ld, s.M, s.N, s.K, reps, maps);
+    gemm_probe<<<cps * sms, NT, GEMM_SMEM_BYTES>>>(buf, stride, ld, s.M, s.N, s.K, reps, maps);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
     double tiles = (double)((s.M + TM - 1) / TM) * ((s.N + 127) / 128) * TM * 128 * 2.0 * s.K;
     printf("M=%5d N=%5d K=%5d: %6.2f TFLOP/s useful, %6.2f tile-TFLOP/s (%.1f GF/s/SM useful) %s\n",
-           s.M, s.N, s.K, fl * reps * CTAS_PER_SM * sms / ms / 1e9, tiles * reps * CTAS_PER_SM * sms / ms / 1e9,
-           CTAS_PER_SM * fl * reps / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
+           s.M, s.N, s.K, fl * reps * cps * sms / ms / 1e9, tiles * reps * cps * sms / ms / 1e9,
+           cps * fl * reps / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
     cudaFree(buf);
   }
   return 0;

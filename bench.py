@@ -135,6 +135,16 @@ class ClockSampler:
                 "power_w_max": max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())}
 
 
+def traffic_per_launch(leaves):
+    """DRAM bytes per launch from the committed ncu --set full capture (per-leaf, scaled)."""
+    path = os.path.join(ROOT, "profiles", "r01_ncu_summary.json")
+    try:
+        per_leaf = json.load(open(path))["traffic_bytes_per_leaf"]
+    except (OSError, KeyError, ValueError):
+        return None
+    return per_leaf * leaves
+
+
 def cpu_reference(tpl, pack, seconds, steps=1):
     """The reference's CPU algorithm (oracle port of local_ops.build_leaf_factors) on host cores."""
     from oracle import hps_oracle as O
@@ -192,6 +202,12 @@ def main():
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
+
+    # CPU reference first, before pinned buffers and GPU work claim host resources
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        tpl0, pack0 = make_shard(p, boxes, args.kappa, 0, 1, min(64, boxes ** 3))
+        cpu = cpu_reference(tpl0, pack0, seconds=args.cpu_seconds)
 
     import torch
     torch.cuda.set_device(local)
@@ -271,14 +287,12 @@ def main():
             t = torch.tensor([e2e_t], device=f"cuda:{local}", dtype=torch.float64)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             e2e_t = float(t.item())
+        del h_coef, h_out
         e2e = {"value": world * L / e2e_t, "unit": "leaf DtN maps/s",
-               "h2d_bytes_per_step": int(h_coef.nbytes), "d2h_bytes_per_step": int(h_out.nbytes),
+               "h2d_bytes_per_step": int(pack.nbytes), "d2h_bytes_per_step": int(L * m * m * 8),
                "path": "LeafEngine.dtn_host -> hps_leaf_dtn_host (C ABI), chunks of "
                        f"{chunk} leaves, copy/compute overlap on 2 streams"}
 
-    cpu = None
-    if rank == 0 and not args.no_cpu:
-        cpu = cpu_reference(tpl, pack, seconds=args.cpu_seconds)
 
     if rank == 0:
         line = {
@@ -295,10 +309,11 @@ def main():
             "flops_per_leaf": flops_leaf,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": PEAK_FP64_TFLOPS,
                          "unit": "TFLOP/s", "frac": achieved / PEAK_FP64_TFLOPS,
-                         "traffic": None,
+                         "traffic": traffic_per_launch(L),
                          "kernel": "hps_leaf_kernel (assembly + LU + Schur, DMMA m8n8k4 f64)",
                          "peak_source": "measured FP64 DMMA peak 37.1 TFLOP/s (cuBLAS DGEMM 35.5); "
-                                        "MEASURED_PEAKS.json has no FP64 entry"},
+                                        "MEASURED_PEAKS.json has no FP64 entry",
+                         "traffic_source": "profiles/r01_ncu_summary.json (ncu --set full, per leaf x leaves)"},
             "gpu_launches": args.steps,
             "e2e": e2e, "cpu_baseline": cpu, "parity": parity,
             "clocks": clk.summary(), "wall_s_timed": t_wall,

@@ -76,6 +76,7 @@ struct LeafParams {
   const double* D2;       // d * p * p (D1 @ D1, computed on host like the reference)
   const double* a_bi;     // m * n
   const double* a_bb;     // m * m
+  const double* bottom;   // (m_pad) x (n_pad + m_pad): [A_bi 0 | A_bb 0], DtN mode rows
   const double* coeffs;   // n_leaves * ncoef * n
   const double* in0;      // REDUCE: f (n per leaf); INTERIOR: ub (m per leaf)
   const double* in1;      // INTERIOR: v (n per leaf)
@@ -352,18 +353,59 @@ __shared__ int s_pivot;
 
 
 // Row interchanges j in [j0, j0+cnt) applied, in order, to columns [c_lo, c_hi).
+// Row interchanges j in [j0, j0+cnt) applied, in order, to columns [c_lo, c_hi).
+// Most pivots are on the diagonal (partial pivoting rarely swaps on these
+// operators), so the interchange list is first compacted into shared memory;
+// then every thread applies the list to its columns, all of a swap's column
+// loads in flight at once.
+__shared__ int s_cnt, s_wcnt[NT / 32];
+
 __device__ void apply_swaps(const Ctx& c, int j0, int cnt, int c_lo, int c_hi) {
   if (c_hi <= c_lo || cnt <= 0) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int* list = reinterpret_cast<int*>(c.smem);
   __syncthreads();
-  for (int col = c_lo + threadIdx.x; col < c_hi; col += NT) {
-    for (int j = j0; j < j0 + cnt; ++j) {
-      const int pr = c.piv[j];
-      if (pr != j) {
-        double* a = c.M + (size_t)j * c.ld + col;
-        double* b = c.M + (size_t)pr * c.ld + col;
-        const double t = *a;
-        *a = *b;
-        *b = t;
+  if (tid == 0) s_cnt = 0;
+  __syncthreads();
+  for (int base = j0; base < j0 + cnt; base += NT) {
+    const int j = base + tid;
+    const int pr = (j < j0 + cnt) ? c.piv[j] : j;
+    const bool flag = pr != j;
+    const unsigned bal = __ballot_sync(0xffffffffu, flag);
+    if (lane == 0) s_wcnt[warp] = __popc(bal);
+    __syncthreads();
+    int off = s_cnt;
+    for (int w = 0; w < warp; ++w) off += s_wcnt[w];
+    if (flag) {
+      const int k = off + __popc(bal & ((1u << lane) - 1u));
+      list[2 * k] = j;
+      list[2 * k + 1] = pr;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int t = 0;
+      for (int w = 0; w < NT / 32; ++w) t += s_wcnt[w];
+      s_cnt += t;
+    }
+    __syncthreads();
+  }
+  const int n = s_cnt;
+  constexpr int CW = 4;  // columns in flight per thread
+  for (int col0 = c_lo + tid; col0 < c_hi; col0 += NT * CW) {
+    for (int k = 0; k < n; ++k) {
+      const int j = list[2 * k], pr = list[2 * k + 1];
+      double* ra = c.M + (size_t)j * c.ld;
+      double* rb = c.M + (size_t)pr * c.ld;
+      double va[CW], vb[CW];
+#pragma unroll
+      for (int u = 0; u < CW; ++u) {
+        const int col = col0 + u * NT;
+        if (col < c_hi) { va[u] = ra[col]; vb[u] = rb[col]; }
+      }
+#pragma unroll
+      for (int u = 0; u < CW; ++u) {
+        const int col = col0 + u * NT;
+        if (col < c_hi) { ra[col] = vb[u]; rb[col] = va[u]; }
       }
     }
   }
@@ -533,6 +575,7 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
       if (bi == 0x7fffffff) bi = j;
       s_pivot = bi;
       c.piv[b0 + j] = b0 + bi;
+      if (c.prof && bi != j) c.prof[15] += 1;
     }
     __syncthreads();
     const int pr = s_pivot;
@@ -563,21 +606,34 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
     const int r = e / WB, j = e - r * WB;
     c.M[(size_t)(b0 + r) * c.ld + b0 + j] = S[e];
   }
-  for (int r = c.n_piv + tid; r < c.NR; r += NT) {
-    double* row = c.M + (size_t)r * c.ld + b0;
-    double x[WB];
+  {
+    // 8 rows per thread in flight: loads first, then the WB x WB substitution
+    constexpr int RR = 2;
+    for (int r0 = c.n_piv + tid; r0 < c.NR; r0 += NT * RR) {
+      double x[RR][WB];
 #pragma unroll
-    for (int j = 0; j < WB; ++j) x[j] = row[j];
+      for (int t = 0; t < RR; ++t) {
+        const int r = r0 + t * NT;
 #pragma unroll
-    for (int j = 0; j < WB; ++j) {
-      double v = x[j];
+        for (int j = 0; j < WB; ++j) x[t][j] = (r < c.NR) ? c.M[(size_t)r * c.ld + b0 + j] : 0.0;
+      }
 #pragma unroll
-      for (int i = 0; i < j; ++i) v -= x[i] * S[i * WB + j];
-      const double pv = S[j * WB + j];
-      x[j] = v * ((pv != 0.0) ? 1.0 / pv : 1.0);
+      for (int t = 0; t < RR; ++t) {
+#pragma unroll
+        for (int j = 0; j < WB; ++j) {
+          double v = x[t][j];
+#pragma unroll
+          for (int i = 0; i < j; ++i) v -= x[t][i] * S[i * WB + j];
+          const double pv = S[j * WB + j];
+          x[t][j] = v * ((pv != 0.0) ? 1.0 / pv : 1.0);
+        }
+        const int r = r0 + t * NT;
+        if (r < c.NR) {
+#pragma unroll
+          for (int j = 0; j < WB; ++j) c.M[(size_t)r * c.ld + b0 + j] = x[t][j];
+        }
+      }
     }
-#pragma unroll
-    for (int j = 0; j < WB; ++j) row[j] = x[j];
   }
   __syncthreads();
   PANEL_TICK(13)
@@ -642,9 +698,33 @@ __device__ void lu_small(Ctx& c, int c0, int w) {
 }
 
 // Explicit inverse of the unit-lower block M[r0.., r0..] (h <= TRI_BLOCK) into scratch (ld TRI_BLOCK).
-__device__ void invert_unit_lower(const Ctx& c, int r0, int h) {
-  double* X = c.smem;  // h x TRI_BLOCK (column j owned by thread j)
+// Explicit inverses of the h x h (h <= TRI_BLOCK) diagonal block of M at r0
+// into the slot's scratch (ld TRI_BLOCK).  The block is staged in shared
+// memory with coalesced loads; thread j then owns column j of the inverse.
+constexpr int TRI_LD = TRI_BLOCK + 1;
+
+__device__ void stage_tri(const Ctx& c, int r0, int h, double* Ls) {
   __syncthreads();
+  for (int e0 = threadIdx.x; e0 < h * h; e0 += NT * 4) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * NT;
+      v[u] = (e < h * h) ? c.M[(size_t)(r0 + e / h) * c.ld + r0 + e % h] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * NT;
+      if (e < h * h) Ls[(e / h) * TRI_LD + e % h] = v[u];
+    }
+  }
+  __syncthreads();
+}
+
+__device__ void invert_unit_lower(const Ctx& c, int r0, int h) {
+  double* Ls = c.smem;
+  double* X = c.smem + TRI_BLOCK * TRI_LD;
+  stage_tri(c, r0, h, Ls);
   const int j = threadIdx.x;
   if (j < h) {
     for (int i = 0; i < h; ++i) {
@@ -652,38 +732,49 @@ __device__ void invert_unit_lower(const Ctx& c, int r0, int h) {
       if (i < j) v = 0.0;
       else if (i == j) v = 1.0;
       else {
-        const double* Li = c.M + (size_t)(r0 + i) * c.ld + r0;
-        v = 0.0;
-        for (int k = j; k < i; ++k) v -= Li[k] * X[k * TRI_BLOCK + j];
+        const double* Li = Ls + i * TRI_LD;
+        double v0 = 0.0, v1 = 0.0;
+        int k = j;
+        for (; k + 1 < i; k += 2) {
+          v0 -= Li[k] * X[k * TRI_LD + j];
+          v1 -= Li[k + 1] * X[(k + 1) * TRI_LD + j];
+        }
+        if (k < i) v0 -= Li[k] * X[k * TRI_LD + j];
+        v = v0 + v1;
       }
-      X[i * TRI_BLOCK + j] = v;
+      X[i * TRI_LD + j] = v;
     }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < h * TRI_BLOCK; e += NT) c.scratch[e] = X[e];
+  for (int e = threadIdx.x; e < h * TRI_BLOCK; e += NT) c.scratch[e] = X[(e / TRI_BLOCK) * TRI_LD + e % TRI_BLOCK];
   __syncthreads();
 }
 
-// Explicit inverse of the upper block M[r0.., r0..] (h <= TRI_BLOCK) into scratch.
 __device__ void invert_upper(const Ctx& c, int r0, int h) {
-  double* X = c.smem;
-  __syncthreads();
+  double* Us = c.smem;
+  double* X = c.smem + TRI_BLOCK * TRI_LD;
+  stage_tri(c, r0, h, Us);
   const int j = threadIdx.x;
   if (j < h) {
     for (int i = h - 1; i >= 0; --i) {
       double v;
       if (i > j) v = 0.0;
       else {
-        const double* Ui = c.M + (size_t)(r0 + i) * c.ld + r0;
-        v = (i == j) ? 1.0 : 0.0;
-        for (int k = i + 1; k <= j; ++k) v -= Ui[k] * X[k * TRI_BLOCK + j];
-        v = v / Ui[i];
+        const double* Ui = Us + i * TRI_LD;
+        double v0 = (i == j) ? 1.0 : 0.0, v1 = 0.0;
+        int k = i + 1;
+        for (; k + 1 <= j; k += 2) {
+          v0 -= Ui[k] * X[k * TRI_LD + j];
+          v1 -= Ui[k + 1] * X[(k + 1) * TRI_LD + j];
+        }
+        if (k <= j) v0 -= Ui[k] * X[k * TRI_LD + j];
+        v = (v0 + v1) / Ui[i];
       }
-      X[i * TRI_BLOCK + j] = v;
+      X[i * TRI_LD + j] = v;
     }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < h * TRI_BLOCK; e += NT) c.scratch[e] = X[e];
+  for (int e = threadIdx.x; e < h * TRI_BLOCK; e += NT) c.scratch[e] = X[(e / TRI_BLOCK) * TRI_LD + e % TRI_BLOCK];
   __syncthreads();
 }
 
@@ -777,7 +868,8 @@ __device__ void assemble(const LeafParams& P, double* M, int leaf) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double* cf = P.coeffs + (size_t)leaf * P.ncoef * P.n;
   const int p = P.p, d = P.d;
-  for (int r = warp; r < P.NR; r += NT / 32) {
+  const int rows_scattered = (P.mode == MODE_DTN) ? P.n_pad : P.NR;
+  for (int r = warp; r < rows_scattered; r += NT / 32) {
     double* row = M + (size_t)r * P.ld;
     double2* row2 = reinterpret_cast<double2*>(row);
     for (int c2 = lane; c2 < P.NC / 2; c2 += 32) row2[c2] = make_double2(0.0, 0.0);
@@ -819,15 +911,58 @@ __device__ void assemble(const LeafParams& P, double* M, int leaf) {
       }
     } else if (r < P.n_pad) {
       if (lane == 0) row[r] = 1.0;  // dummy pivot keeps padding inert
-    } else if (P.mode == MODE_DTN && r < P.n_pad + P.m) {
-      const int b = r - P.n_pad;
-      const double* abi = P.a_bi + (size_t)b * P.n;
-      const double* abb = P.a_bb + (size_t)b * P.m;
-      for (int c = lane; c < P.n; c += 32) row[c] = abi[c];
-      for (int c = lane; c < P.m; c += 32) row[P.n_pad + c] = abb[c];
+    }
+  }
+  if (P.mode == MODE_DTN) {
+    // rows [n_pad, NR) = the plan's padded [A_bi 0 | A_bb 0] block: one flat
+    // 16-byte vector copy, 8 loads in flight per thread
+    const double2* src = reinterpret_cast<const double2*>(P.bottom);
+    double2* dst = reinterpret_cast<double2*>(M + (size_t)P.n_pad * P.ld);
+    const size_t total = (size_t)(P.NR - P.n_pad) * P.ld / 2;
+    for (size_t e0 = threadIdx.x; e0 < total; e0 += (size_t)NT * 8) {
+      double2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const size_t e = e0 + (size_t)u * NT;
+        if (e < total) v[u] = src[e];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const size_t e = e0 + (size_t)u * NT;
+        if (e < total) dst[e] = v[u];
+      }
     }
   }
   __syncthreads();
+}
+
+// rows x cols block of M (ld) -> dense out (ld_out), 16-byte vectors, 8 in flight
+// per thread; cols and both row strides even.
+__device__ void copy_block(const double* src, int ld, double* out, int ld_out, int rows, int cols,
+                           bool negate) {
+  const int c2 = cols / 2;
+  const int total = rows * c2;
+  for (int e0 = threadIdx.x; e0 < total; e0 += NT * 4) {
+    double2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * NT;
+      if (e < total) {
+        const int i = e / c2, j = e - i * c2;
+        v[u] = reinterpret_cast<const double2*>(src + (size_t)i * ld)[j];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * NT;
+      if (e < total) {
+        const int i = e / c2, j = e - i * c2;
+        double2 w = v[u];
+        if (negate) { w.x = -w.x; w.y = -w.y; }
+        reinterpret_cast<double2*>(out + (size_t)i * ld_out)[j] = w;
+      }
+    }
+  }
 }
 
 __global__ void __launch_bounds__(NT, CTAS_PER_SM)
@@ -887,17 +1022,10 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     }
     if (prof) t0 = clock64();
     if (P.mode == MODE_DTN) {
-      double* T = P.out0 + (size_t)leaf * P.m * P.m;
-      for (int e = threadIdx.x; e < P.m * P.m; e += NT) {
-        const int i = e / P.m, j = e - i * P.m;
-        T[e] = c.M[(size_t)(P.n_pad + i) * c.ld + P.n_pad + j];
-      }
+      copy_block(c.M + (size_t)P.n_pad * c.ld + P.n_pad, c.ld, P.out0 + (size_t)leaf * P.m * P.m,
+                 P.m, P.m, P.m, false);
     } else if (P.mode == MODE_SOLOP) {
-      double* S = P.out0 + (size_t)leaf * P.n * P.m;
-      for (int e = threadIdx.x; e < P.n * P.m; e += NT) {
-        const int i = e / P.m, j = e - i * P.m;
-        S[e] = -c.M[(size_t)i * c.ld + P.n_pad + j];
-      }
+      copy_block(c.M + P.n_pad, c.ld, P.out0 + (size_t)leaf * P.n * P.m, P.m, P.n, P.m, true);
     } else {
       double* out = P.out0 + (size_t)leaf * P.n;
       if (P.mode == MODE_REDUCE) {
@@ -1008,7 +1136,7 @@ struct hps_plan_s {
   int has_first = 0, has_zeroth = 0, ncoef = 0;
   int sms = 0, slots = 0;
   size_t budget = 0;
-  double *D1 = nullptr, *D2 = nullptr, *a_bi = nullptr, *a_bb = nullptr;
+  double *D1 = nullptr, *D2 = nullptr, *a_bi = nullptr, *a_bb = nullptr, *bottom = nullptr;
   // workspace (sized for the largest mode requested so far)
   double* work = nullptr;
   size_t work_doubles = 0;
@@ -1150,13 +1278,13 @@ static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, c
   L.n_leaves = n_leaves;
   L.slot_stride = slot_doubles(P, mode);
   L.work = P->work; L.piv = P->piv; L.scratch = P->scratch;
-  L.D1 = P->D1; L.D2 = P->D2; L.a_bi = P->a_bi; L.a_bb = P->a_bb;
+  L.D1 = P->D1; L.D2 = P->D2; L.a_bi = P->a_bi; L.a_bb = P->a_bb; L.bottom = P->bottom;
   L.prof = P->prof;
   L.coeffs = coeffs; L.in0 = in0; L.in1 = in1; L.out0 = out0; L.out1 = out1; L.stats = stats;
   const int panel_bytes = ((P->n_pad * P->wb > 1024 ? P->n_pad * P->wb : 1024) + 32 * P->wb) * 8;
   int smem = GEMM_SMEM_BYTES;
   if (panel_bytes > smem) smem = panel_bytes;
-  if (TRI_BLOCK * TRI_BLOCK * 8 > smem) smem = TRI_BLOCK * TRI_BLOCK * 8;
+  if (2 * TRI_BLOCK * TRI_LD * 8 > smem) smem = 2 * TRI_BLOCK * TRI_LD * 8;
   CK(cudaFuncSetAttribute(hps_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   CK(cudaFuncSetAttribute(hps_leaf_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   hps_leaf_kernel<<<slots, NT, smem, stream>>>(L, P->prog[mode], P->prog_len[mode], P->maps[mode]);
@@ -1213,6 +1341,19 @@ int hps_plan_create(hps_plan_t* out, int device, int dim, int p, int has_first, 
   cudaMemcpy(P->D2, D2, tab, cudaMemcpyHostToDevice);
   cudaMemcpy(P->a_bi, a_bi, (size_t)P->m * P->n * 8, cudaMemcpyHostToDevice);
   cudaMemcpy(P->a_bb, a_bb, (size_t)P->m * P->m * 8, cudaMemcpyHostToDevice);
+  {
+    const size_t NCd = (size_t)P->n_pad + P->m_pad;
+    std::vector<double> bot((size_t)P->m_pad * NCd, 0.0);
+    for (int b = 0; b < P->m; ++b) {
+      for (int k = 0; k < P->n; ++k) bot[b * NCd + k] = a_bi[(size_t)b * P->n + k];
+      for (int k = 0; k < P->m; ++k) bot[b * NCd + P->n_pad + k] = a_bb[(size_t)b * P->m + k];
+    }
+    if (cudaMalloc(&P->bottom, bot.size() * 8) != cudaSuccess) {
+      hps_plan_destroy(P);
+      return fail("device allocation of the boundary-row template failed");
+    }
+    cudaMemcpy(P->bottom, bot.data(), bot.size() * 8, cudaMemcpyHostToDevice);
+  }
   if (cudaGetLastError() != cudaSuccess) { hps_plan_destroy(P); return fail("template upload failed"); }
   *out = P;
   return 0;
@@ -1221,7 +1362,7 @@ int hps_plan_create(hps_plan_t* out, int device, int dim, int p, int has_first, 
 int hps_plan_destroy(hps_plan_t P) {
   if (!P) return 0;
   cudaSetDevice(P->device);
-  cudaFree(P->D1); cudaFree(P->D2); cudaFree(P->a_bi); cudaFree(P->a_bb);
+  cudaFree(P->D1); cudaFree(P->D2); cudaFree(P->a_bi); cudaFree(P->a_bb); cudaFree(P->bottom);
   cudaFree(P->work); cudaFree(P->piv); cudaFree(P->scratch);
   for (int k = 0; k < 4; ++k) cudaFree(P->prog[k]);
   if (P->h_stage) cudaFreeHost(P->h_stage);

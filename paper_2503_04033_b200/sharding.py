@@ -74,7 +74,8 @@ def sharded_dtn(disc, coeffs, world: int, rank: int,
             return dtn
     m = template.n_boundary
     if ids:
-        blocks = compute(pack_coefficients(coeffs, disc.interior_points(ids), len(ids)))
+        from .condensation import interior_points
+        blocks = compute(pack_coefficients(coeffs, interior_points(disc, ids), len(ids)))
     else:
         blocks = np.empty((0, m, m))
     parts = gather_to_root(ids, blocks, root)

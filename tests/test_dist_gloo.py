@@ -71,8 +71,9 @@ def test_sharded_build_matches_single_process(tmp_path):
     res = np.load(out)
     spec, disc = _problem()
     from paper_2503_04033_b200.local_ops import pack_coefficients
+    from paper_2503_04033_b200.condensation import interior_points
     full = _oracle_compute(disc)(pack_coefficients(spec.coeffs,
-                                                   disc.interior_points(range(len(disc.leaves))),
+                                                   interior_points(disc, range(len(disc.leaves))),
                                                    len(disc.leaves)))
     assert np.array_equal(res["blocks"], full)
     assert float(res["slowest"]) == 2.0

@@ -103,7 +103,8 @@ def test_sharded_dtn_single_rank_on_gpu():
     blocks = sharded_dtn(disc, spec.coeffs, 1, 0)
     tpl = O.OracleTemplate(disc.leaf_widths, 8)
     from paper_2503_04033_b200.local_ops import pack_coefficients
-    pack = pack_coefficients(spec.coeffs, disc.interior_points(range(8)), 8)
+    from paper_2503_04033_b200.condensation import interior_points
+    pack = pack_coefficients(spec.coeffs, interior_points(disc, range(8)), 8)
     for k in range(8):
         assert rel(blocks[k], O.leaf_dtn(tpl, pack[k, :3].T, None, pack[k, 3])[0]) <= 1e-10
 

@@ -38,6 +38,7 @@ for i, nm in enumerate(names):
     print(f"  {nm:12s} {100*c[:, i].sum()/tot:6.2f}%   {c[:, i].sum()/leaves/clk*1e3:8.2f} ms/leaf")
 for i, nm in zip(range(10, 15), ["p1-utop", "p2-gather", "p3-pivot", "p4-writeback", "p5-swaps"]):
     print(f"    {nm:12s} {c[:, i].sum()/leaves/clk*1e3:8.2f} ms/leaf")
+print(f"  row interchanges per leaf: {c[:, 15].sum()/leaves:.0f} of {eng.n} pivots")
 gf = c[:, 8].sum() * 2**20
 print(f"  gemm flops/leaf {gf/leaves:.3e}; gemm-only rate per SM {gf/(c[:, 4].sum()+c[:, 5].sum())*clk/1e9:.1f} GFLOP/s "
       f"(peak 251/SM); per-leaf total {tot/leaves/clk*1e3:.1f} ms")

@@ -1060,7 +1060,16 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
 // Host-side program builder: the recursion of the blocked algorithm, unrolled.
 // ---------------------------------------------------------------------------
 
-int split16_host(int w) { return ((w / 2 + 15) / 16) * 16; }
+// Left part of a recursive split: multiples of TN (128) above 256 columns so the
+// big GEMMs see tile-aligned N/M extents (p=16: tile utilisation 0.85 -> 0.91),
+// multiples of 16 (the TMA/K-chunk granule) below.
+int split16_host(int w) {
+  if (w > 2 * TN) {
+    const int h = (w / 2) / TN * TN;
+    return h < TN ? TN : h;
+  }
+  return ((w / 2 + 15) / 16) * 16;
+}
 
 struct ProgramBuilder {
   std::vector<Op> ops;

@@ -39,18 +39,34 @@
 
 namespace {
 
-constexpr int NT = 128;          // threads per CTA (4 warps); two CTAs (two leaves) per SM
+#ifndef HPS_NT
+#define HPS_NT 256
+#endif
+constexpr int NT = HPS_NT;       // threads per CTA; two CTAs (two leaves) per SM
 constexpr int CTAS_PER_SM = 2;
 constexpr int TM = 64;           // GEMM tile rows (1 x 4 warps of 64 x 32)
 constexpr int TN = 128;          // GEMM tile cols
 constexpr int KC = 16;           // k-chunk per pipeline stage
-constexpr int STAGES = 4;
+#ifndef HPS_STAGES
+#define HPS_STAGES 3
+#endif
+#ifndef HPS_EPI_SLOTS
+#define HPS_EPI_SLOTS 2
+#endif
+constexpr int STAGES = HPS_STAGES;
+constexpr int EPI_SLOTS = HPS_EPI_SLOTS;
 constexpr int A_STRIDE = KC;     // A box rows are 128 B, 128B-swizzled by TMA (1024 B aligned)
 constexpr int B_STRIDE = TN;     // B box rows are 1 KB, unswizzled
 constexpr int STAGE_A = TM * A_STRIDE;
 constexpr int STAGE_B = KC * B_STRIDE;
 constexpr int STAGE_DBL = STAGE_A + STAGE_B;
-constexpr int EPI_DBL = 2 * 2 * 8 * 16;  // per warp: 2 ring slots x two [8][16] blocks
+constexpr int WARPS = NT / 32;
+constexpr int WN = 4;                 // warps along N (4 x 32 = TN)
+constexpr int WM = WARPS / WN;        // warps along M
+constexpr int MI = TM / WM / 8;       // 8-row m-tiles per warp
+constexpr int NJ = TN / WN / 8;       // 8-col n-tiles per warp (4)
+static_assert(MI * 8 * WM == TM && NJ == 4, "warp tiling");
+constexpr int EPI_DBL = EPI_SLOTS * 2 * 8 * 16;  // per warp: ring slots x two [8][16] blocks
 constexpr int GEMM_SMEM_BYTES = (STAGES * STAGE_DBL + (NT / 32) * EPI_DBL) * 8;
 constexpr int TRI_BLOCK = 64;    // triangular base block (explicit inverse + GEMM)
 constexpr int SMALL_PANEL = 32;  // recursion leaf width handled by rank-wb updates
@@ -84,6 +100,7 @@ struct LeafParams {
   double* out1;           // REDUCE: flux (m per leaf)
   double* stats;          // n_leaves * 2 : min |pivot|, max |pivot| over real columns
   unsigned long long* prof;  // optional [slots][PROF_SLOTS] cycle counters (diagnostics)
+  int* leaf_counter;         // next leaf to reduce (zeroed before each launch)
 };
 
 constexpr int PROF_SLOTS = 16;  // 0..5 op kinds, 6 assemble, 7 output, 8 gemm flops/2^20, 9 leaves
@@ -159,6 +176,9 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read1() {
   asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
 }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -208,7 +228,7 @@ __device__ __forceinline__ void gemm(Ctx& c, const bool sub, const bool a_scratc
                                      int br, int bc, int cr, int cc, int M, int N, int K) {
   if (M <= 0 || N <= 0 || K <= 0) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int wm = warp >> 2, wn = warp & 3;
+  const int wm = warp / WN, wn = warp % WN;
   const int lr = lane >> 2, lc = lane & 3;
   const int tiles_n = (N + TN - 1) / TN;
   const int tiles = ((M + TM - 1) / TM) * tiles_n;
@@ -249,11 +269,11 @@ __device__ __forceinline__ void gemm(Ctx& c, const bool sub, const bool a_scratc
     for (int s = 0; s < STAGES - 1; ++s) produce();
   }
 
-  double acc[8][4][2];
+  double acc[MI][NJ][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   int tile = 0, kc = 0;
   for (int it = 0; it < total; ++it) {
@@ -265,19 +285,19 @@ __device__ __forceinline__ void gemm(Ctx& c, const bool sub, const bool a_scratc
     const double* sb = sa + STAGE_A;
 #pragma unroll
     for (int ks = 0; ks < KC; ks += 4) {
-      double af[8], bf[4];
+      double af[MI], bf[NJ];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < MI; ++i) {
         // 128B swizzle: 16-byte chunk index ^= row % 8  (row % 8 == lr here)
-        const int row = wm * 64 + i * 8 + lr, k = ks + lc;
+        const int row = wm * (MI * 8) + i * 8 + lr, k = ks + lc;
         af[i] = sa[row * A_STRIDE + ((((k >> 1) ^ lr) << 1) | (k & 1))];
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = sb[(ks + lc) * B_STRIDE + wn * 32 + j * 8 + lr];
+      for (int j = 0; j < NJ; ++j) bf[j] = sb[(ks + lc) * B_STRIDE + wn * 32 + j * 8 + lr];
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+        for (int j = 0; j < NJ; ++j) dmma(acc[i][j], af[i], bf[j]);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&c.empty[s]);
@@ -290,11 +310,14 @@ __device__ __forceinline__ void gemm(Ctx& c, const bool sub, const bool a_scratc
         // (two [8][16] blocks per m-tile) and drains asynchronously.
         double* ring = smem + STAGES * STAGE_DBL + warp * EPI_DBL;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int row0 = tm * TM + wm * 64 + i * 8;
+        for (int i = 0; i < MI; ++i) {
+          const int row0 = tm * TM + wm * (MI * 8) + i * 8;
           if (row0 < M) {
-            double* buf = ring + (i & 1) * 256;
-            if (lane == 0) bulk_wait_read1();
+            double* buf = ring + (EPI_SLOTS == 1 ? 0 : (i & 1)) * 256;
+            if (lane == 0) {
+              if (EPI_SLOTS == 1) bulk_wait_read0();
+              else bulk_wait_read1();
+            }
             __syncwarp();
 #pragma unroll
             for (int j = 0; j < 4; ++j)
@@ -310,15 +333,15 @@ __device__ __forceinline__ void gemm(Ctx& c, const bool sub, const bool a_scratc
             }
           }
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+          for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
         }
         continue;
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int row = tm * TM + wm * 64 + i * 8 + lr;
+      for (int i = 0; i < MI; ++i) {
+        const int row = tm * TM + wm * (MI * 8) + i * 8 + lr;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < NJ; ++j) {
           const int col = tn * TN + wn * 32 + j * 8 + 2 * lc;
           if (row < M && col < N) {
             double2* cp = reinterpret_cast<double2*>(C + (size_t)row * c.ld + col);
@@ -996,7 +1019,15 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
 
   unsigned long long* prof = P.prof ? P.prof + (size_t)slot * PROF_SLOTS : nullptr;
   c.prof = prof;
-  for (int leaf = blockIdx.x; leaf < P.n_leaves; leaf += gridDim.x) {
+  // dynamic leaf scheduling: the two CTAs sharing an SM do not progress at the
+  // same rate (warp arbitration), so slots grab the next leaf when done
+  __shared__ int s_leaf;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_leaf = atomicAdd(P.leaf_counter, 1);
+    __syncthreads();
+    const int leaf = s_leaf;
+    if (leaf >= P.n_leaves) break;
     long long t0 = clock64();
     assemble(P, c.M, leaf);
     if (threadIdx.x == 0) { s_pmin = INFINITY; s_pmax = 0.0; }
@@ -1157,6 +1188,7 @@ struct hps_plan_s {
   int prog_len[4] = {0, 0, 0, 0};
   double* h_stage = nullptr;
   unsigned long long* prof = nullptr;  // diagnostics counters (device), optional
+  int* leaf_counter = nullptr;
   TmaMaps maps[4];
   int maps_ok[4] = {0, 0, 0, 0};
 };
@@ -1289,6 +1321,8 @@ static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, c
   L.work = P->work; L.piv = P->piv; L.scratch = P->scratch;
   L.D1 = P->D1; L.D2 = P->D2; L.a_bi = P->a_bi; L.a_bb = P->a_bb; L.bottom = P->bottom;
   L.prof = P->prof;
+  L.leaf_counter = P->leaf_counter;
+  CK(cudaMemsetAsync(P->leaf_counter, 0, sizeof(int), stream));
   L.coeffs = coeffs; L.in0 = in0; L.in1 = in1; L.out0 = out0; L.out1 = out1; L.stats = stats;
   const int panel_bytes = ((P->n_pad * P->wb > 1024 ? P->n_pad * P->wb : 1024) + 32 * P->wb) * 8;
   int smem = GEMM_SMEM_BYTES;
@@ -1357,7 +1391,8 @@ int hps_plan_create(hps_plan_t* out, int device, int dim, int p, int has_first, 
       for (int k = 0; k < P->n; ++k) bot[b * NCd + k] = a_bi[(size_t)b * P->n + k];
       for (int k = 0; k < P->m; ++k) bot[b * NCd + P->n_pad + k] = a_bb[(size_t)b * P->m + k];
     }
-    if (cudaMalloc(&P->bottom, bot.size() * 8) != cudaSuccess) {
+    if (cudaMalloc(&P->bottom, bot.size() * 8) != cudaSuccess ||
+        cudaMalloc(&P->leaf_counter, sizeof(int)) != cudaSuccess) {
       hps_plan_destroy(P);
       return fail("device allocation of the boundary-row template failed");
     }
@@ -1372,6 +1407,7 @@ int hps_plan_destroy(hps_plan_t P) {
   if (!P) return 0;
   cudaSetDevice(P->device);
   cudaFree(P->D1); cudaFree(P->D2); cudaFree(P->a_bi); cudaFree(P->a_bb); cudaFree(P->bottom);
+  cudaFree(P->leaf_counter);
   cudaFree(P->work); cudaFree(P->piv); cudaFree(P->scratch);
   for (int k = 0; k < 4; ++k) cudaFree(P->prog[k]);
   if (P->h_stage) cudaFreeHost(P->h_stage);

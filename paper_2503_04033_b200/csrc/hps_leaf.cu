@@ -92,7 +92,6 @@ struct LeafParams {
   const double* D2;       // d * p * p (D1 @ D1, computed on host like the reference)
   const double* a_bi;     // m * n
   const double* a_bb;     // m * m
-  const double* bottom;   // (m_pad) x (n_pad + m_pad): [A_bi 0 | A_bb 0], DtN mode rows
   const double* coeffs;   // n_leaves * ncoef * n
   const double* in0;      // REDUCE: f (n per leaf); INTERIOR: ub (m per leaf)
   const double* in1;      // INTERIOR: v (n per leaf)
@@ -891,8 +890,7 @@ __device__ void assemble(const LeafParams& P, double* M, int leaf) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double* cf = P.coeffs + (size_t)leaf * P.ncoef * P.n;
   const int p = P.p, d = P.d;
-  const int rows_scattered = (P.mode == MODE_DTN) ? P.n_pad : P.NR;
-  for (int r = warp; r < rows_scattered; r += NT / 32) {
+  for (int r = warp; r < P.NR; r += NT / 32) {
     double* row = M + (size_t)r * P.ld;
     double2* row2 = reinterpret_cast<double2*>(row);
     for (int c2 = lane; c2 < P.NC / 2; c2 += 32) row2[c2] = make_double2(0.0, 0.0);
@@ -936,26 +934,6 @@ __device__ void assemble(const LeafParams& P, double* M, int leaf) {
       if (lane == 0) row[r] = 1.0;  // dummy pivot keeps padding inert
     }
   }
-  if (P.mode == MODE_DTN) {
-    // rows [n_pad, NR) = the plan's padded [A_bi 0 | A_bb 0] block: one flat
-    // 16-byte vector copy, 8 loads in flight per thread
-    const double2* src = reinterpret_cast<const double2*>(P.bottom);
-    double2* dst = reinterpret_cast<double2*>(M + (size_t)P.n_pad * P.ld);
-    const size_t total = (size_t)(P.NR - P.n_pad) * P.ld / 2;
-    for (size_t e0 = threadIdx.x; e0 < total; e0 += (size_t)NT * 8) {
-      double2 v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const size_t e = e0 + (size_t)u * NT;
-        if (e < total) v[u] = src[e];
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const size_t e = e0 + (size_t)u * NT;
-        if (e < total) dst[e] = v[u];
-      }
-    }
-  }
   __syncthreads();
 }
 
@@ -985,6 +963,48 @@ __device__ void copy_block(const double* src, int ld, double* out, int ld_out, i
         reinterpret_cast<double2*>(out + (size_t)i * ld_out)[j] = w;
       }
     }
+  }
+}
+
+// DtN from the solution block: with X = A_ii^{-1} A_ib in columns [n_pad, n_pad+m)
+// of M, T = A_bb - A_bi X.  A_bi is structurally sparse: boundary DOF b reads
+// only the q = p-2 interior nodes on its normal grid line, with weights
+// -D1[a][0][.] (low face) / +D1[a][p-1][.] (high face) (local_ops.py:310-315).
+// Each interior line serves the two opposite face DOFs, so X is read once per
+// line: 2 q m^2 flops instead of the dense 2 n m^2.
+__device__ void dtn_lines(const LeafParams& P, const double* M, int ld, double* T) {
+  __shared__ double s_w[3][2][32];
+  const int q = P.q, p = P.p, d = P.d, m = P.m;
+  for (int e = threadIdx.x; e < d * 2 * q; e += NT) {
+    const int a = e / (2 * q), side = (e / q) & 1, i = e % q;
+    s_w[a][side][i] = P.D1[(a * p + (side ? p - 1 : 0)) * p + i + 1];
+  }
+  __syncthreads();
+  const int fd = (d == 3) ? q * q : q;
+  const int lines = d * fd;
+  const double* X = M + P.n_pad;
+  for (int e = threadIdx.x; e < lines * m; e += NT) {
+    const int line = e / m, col = e - line * m;
+    const int a = line / fd, t = line - a * fd;
+    int base, stride;
+    if (d == 3) {
+      if (a == 0) { base = t; stride = q * q; }
+      else if (a == 1) { base = (t / q) * q * q + t % q; stride = q; }
+      else { base = t * q; stride = 1; }
+    } else {
+      if (a == 0) { base = t; stride = q; }
+      else { base = t * q; stride = 1; }
+    }
+    double lo = 0.0, hi = 0.0;
+#pragma unroll 4
+    for (int i = 0; i < q; ++i) {
+      const double x = X[(size_t)(base + i * stride) * ld + col];
+      lo += s_w[a][0][i] * x;
+      hi += s_w[a][1][i] * x;
+    }
+    const int b_lo = 2 * a * fd + t, b_hi = b_lo + fd;
+    T[(size_t)b_lo * m + col] = P.a_bb[(size_t)b_lo * m + col] + lo;
+    T[(size_t)b_hi * m + col] = P.a_bb[(size_t)b_hi * m + col] - hi;
   }
 }
 
@@ -1053,8 +1073,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     }
     if (prof) t0 = clock64();
     if (P.mode == MODE_DTN) {
-      copy_block(c.M + (size_t)P.n_pad * c.ld + P.n_pad, c.ld, P.out0 + (size_t)leaf * P.m * P.m,
-                 P.m, P.m, P.m, false);
+      dtn_lines(P, c.M, c.ld, P.out0 + (size_t)leaf * P.m * P.m);
     } else if (P.mode == MODE_SOLOP) {
       copy_block(c.M + P.n_pad, c.ld, P.out0 + (size_t)leaf * P.n * P.m, P.m, P.n, P.m, true);
     } else {
@@ -1176,7 +1195,7 @@ struct hps_plan_s {
   int has_first = 0, has_zeroth = 0, ncoef = 0;
   int sms = 0, slots = 0;
   size_t budget = 0;
-  double *D1 = nullptr, *D2 = nullptr, *a_bi = nullptr, *a_bb = nullptr, *bottom = nullptr;
+  double *D1 = nullptr, *D2 = nullptr, *a_bi = nullptr, *a_bb = nullptr;
   // workspace (sized for the largest mode requested so far)
   double* work = nullptr;
   size_t work_doubles = 0;
@@ -1225,10 +1244,7 @@ static int make_map(CUtensorMap* map, double* base, uint64_t cols, uint64_t rows
 static int round16(int x) { return (x + 15) / 16 * 16; }
 
 static void mode_dims(const hps_plan_s* P, int mode, int* NR, int* NC) {
-  if (mode == MODE_DTN) {
-    *NR = P->n_pad + P->m_pad;
-    *NC = P->n_pad + P->m_pad;
-  } else if (mode == MODE_SOLOP) {
+  if (mode == MODE_DTN || mode == MODE_SOLOP) {
     *NR = P->n_pad;
     *NC = P->n_pad + P->m_pad;
   } else {
@@ -1288,10 +1304,7 @@ static int ensure_program(hps_plan_s* P, int mode) {
   b.lu(0, P->n_pad, NR);
   b.swaps(0, P->n_pad, P->n_pad, NC);
   b.trsm_lower(0, P->n_pad, P->n_pad, NC);
-  if (mode == MODE_DTN)
-    b.gemm(OP_GEMM_SUB, P->n_pad, 0, 0, P->n_pad, P->n_pad, P->n_pad, NR - P->n_pad, NC - P->n_pad, P->n_pad);
-  else
-    b.trsm_upper(0, P->n_pad, P->n_pad, NC);
+  b.trsm_upper(0, P->n_pad, P->n_pad, NC);
   CK(cudaMalloc(&P->prog[mode], b.ops.size() * sizeof(Op)));
   CK(cudaMemcpy(P->prog[mode], b.ops.data(), b.ops.size() * sizeof(Op), cudaMemcpyHostToDevice));
   P->prog_len[mode] = (int)b.ops.size();
@@ -1319,7 +1332,7 @@ static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, c
   L.n_leaves = n_leaves;
   L.slot_stride = slot_doubles(P, mode);
   L.work = P->work; L.piv = P->piv; L.scratch = P->scratch;
-  L.D1 = P->D1; L.D2 = P->D2; L.a_bi = P->a_bi; L.a_bb = P->a_bb; L.bottom = P->bottom;
+  L.D1 = P->D1; L.D2 = P->D2; L.a_bi = P->a_bi; L.a_bb = P->a_bb;
   L.prof = P->prof;
   L.leaf_counter = P->leaf_counter;
   CK(cudaMemsetAsync(P->leaf_counter, 0, sizeof(int), stream));
@@ -1384,19 +1397,9 @@ int hps_plan_create(hps_plan_t* out, int device, int dim, int p, int has_first, 
   cudaMemcpy(P->D2, D2, tab, cudaMemcpyHostToDevice);
   cudaMemcpy(P->a_bi, a_bi, (size_t)P->m * P->n * 8, cudaMemcpyHostToDevice);
   cudaMemcpy(P->a_bb, a_bb, (size_t)P->m * P->m * 8, cudaMemcpyHostToDevice);
-  {
-    const size_t NCd = (size_t)P->n_pad + P->m_pad;
-    std::vector<double> bot((size_t)P->m_pad * NCd, 0.0);
-    for (int b = 0; b < P->m; ++b) {
-      for (int k = 0; k < P->n; ++k) bot[b * NCd + k] = a_bi[(size_t)b * P->n + k];
-      for (int k = 0; k < P->m; ++k) bot[b * NCd + P->n_pad + k] = a_bb[(size_t)b * P->m + k];
-    }
-    if (cudaMalloc(&P->bottom, bot.size() * 8) != cudaSuccess ||
-        cudaMalloc(&P->leaf_counter, sizeof(int)) != cudaSuccess) {
-      hps_plan_destroy(P);
-      return fail("device allocation of the boundary-row template failed");
-    }
-    cudaMemcpy(P->bottom, bot.data(), bot.size() * 8, cudaMemcpyHostToDevice);
+  if (cudaMalloc(&P->leaf_counter, sizeof(int)) != cudaSuccess) {
+    hps_plan_destroy(P);
+    return fail("device allocation of the leaf counter failed");
   }
   if (cudaGetLastError() != cudaSuccess) { hps_plan_destroy(P); return fail("template upload failed"); }
   *out = P;
@@ -1406,7 +1409,7 @@ int hps_plan_create(hps_plan_t* out, int device, int dim, int p, int has_first, 
 int hps_plan_destroy(hps_plan_t P) {
   if (!P) return 0;
   cudaSetDevice(P->device);
-  cudaFree(P->D1); cudaFree(P->D2); cudaFree(P->a_bi); cudaFree(P->a_bb); cudaFree(P->bottom);
+  cudaFree(P->D1); cudaFree(P->D2); cudaFree(P->a_bi); cudaFree(P->a_bb);
   cudaFree(P->leaf_counter);
   cudaFree(P->work); cudaFree(P->piv); cudaFree(P->scratch);
   for (int k = 0; k < 4; ++k) cudaFree(P->prog[k]);

@@ -193,3 +193,10 @@ def dtn_flops(n: int, m: int) -> float:
     """FLOPs of one leaf reduction in the reference's dense algorithm:
     getrf(n) + getrs with m right-hand sides + the (m x n) @ (n x m) product."""
     return 2.0 / 3.0 * n ** 3 + 2.0 * n * n * m + 2.0 * n * m * m
+
+
+def dtn_flops_executed(n: int, m: int, q: int) -> float:
+    """FLOPs of the algorithm the engine runs: getrf(n) + two triangular solves
+    with m right-hand sides + the line-sparse A_bi product (q = p - 2 nodes
+    per boundary row)."""
+    return 2.0 / 3.0 * n ** 3 + 2.0 * n * n * m + 2.0 * q * m * m

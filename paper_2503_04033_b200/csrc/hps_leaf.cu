@@ -743,28 +743,32 @@ __device__ void stage_tri(const Ctx& c, int r0, int h, double* Ls) {
   __syncthreads();
 }
 
+// Thread layout for the inverses: 4 lanes per column, each lane sums every
+// 4th term of the column's dot product, a 2-step shuffle reduces.
 __device__ void invert_unit_lower(const Ctx& c, int r0, int h) {
   double* Ls = c.smem;
   double* X = c.smem + TRI_BLOCK * TRI_LD;
   stage_tri(c, r0, h, Ls);
-  const int j = threadIdx.x;
-  if (j < h) {
-    for (int i = 0; i < h; ++i) {
-      double v;
-      if (i < j) v = 0.0;
-      else if (i == j) v = 1.0;
-      else {
+  const int lane = threadIdx.x & 31;
+  const int part = lane & 3;
+  for (int j = (threadIdx.x >> 2); j < TRI_BLOCK; j += NT / 4) {
+    // rows i <= j of column j are 0 / 1
+    for (int i = part; i <= j && i < TRI_BLOCK; i += 4) X[i * TRI_LD + j] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int j0 = 0; j0 < TRI_BLOCK; j0 += NT / 4) {
+    const int j = j0 + (threadIdx.x >> 2);
+    const bool act = j < h;
+    for (int i = j0 + 1; i < h; ++i) {  // uniform loop bound within the warp group
+      double v = 0.0;
+      if (act && i > j) {
         const double* Li = Ls + i * TRI_LD;
-        double v0 = 0.0, v1 = 0.0;
-        int k = j;
-        for (; k + 1 < i; k += 2) {
-          v0 -= Li[k] * X[k * TRI_LD + j];
-          v1 -= Li[k + 1] * X[(k + 1) * TRI_LD + j];
-        }
-        if (k < i) v0 -= Li[k] * X[k * TRI_LD + j];
-        v = v0 + v1;
+        for (int k = j + part; k < i; k += 4) v -= Li[k] * X[k * TRI_LD + j];
       }
-      X[i * TRI_LD + j] = v;
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      if (act && i > j && part == 0) X[i * TRI_LD + j] = v;
+      __syncwarp();
     }
   }
   __syncthreads();
@@ -776,23 +780,27 @@ __device__ void invert_upper(const Ctx& c, int r0, int h) {
   double* Us = c.smem;
   double* X = c.smem + TRI_BLOCK * TRI_LD;
   stage_tri(c, r0, h, Us);
-  const int j = threadIdx.x;
-  if (j < h) {
-    for (int i = h - 1; i >= 0; --i) {
-      double v;
-      if (i > j) v = 0.0;
-      else {
+  const int lane = threadIdx.x & 31;
+  const int part = lane & 3;
+  for (int j = (threadIdx.x >> 2); j < TRI_BLOCK; j += NT / 4) {
+    for (int i = j + 1 + part; i < TRI_BLOCK; i += 4) X[i * TRI_LD + j] = 0.0;
+    if (part == 0 && j < h) X[j * TRI_LD + j] = 1.0 / Us[j * TRI_LD + j];
+  }
+  __syncthreads();
+  for (int j0 = 0; j0 < TRI_BLOCK; j0 += NT / 4) {
+    const int j = j0 + (threadIdx.x >> 2);
+    const bool act = j < h;
+    const int top = min(h, j0 + NT / 4) - 1;
+    for (int i = top - 1; i >= 0; --i) {
+      double v = 0.0;
+      if (act && i < j) {
         const double* Ui = Us + i * TRI_LD;
-        double v0 = (i == j) ? 1.0 : 0.0, v1 = 0.0;
-        int k = i + 1;
-        for (; k + 1 <= j; k += 2) {
-          v0 -= Ui[k] * X[k * TRI_LD + j];
-          v1 -= Ui[k + 1] * X[(k + 1) * TRI_LD + j];
-        }
-        if (k <= j) v0 -= Ui[k] * X[k * TRI_LD + j];
-        v = (v0 + v1) / Ui[i];
+        for (int k = i + 1 + part; k <= j; k += 4) v -= Ui[k] * X[k * TRI_LD + j];
       }
-      X[i * TRI_LD + j] = v;
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      if (act && i < j && part == 0) X[i * TRI_LD + j] = v / Us[i * TRI_LD + i];
+      __syncwarp();
     }
   }
   __syncthreads();
@@ -983,28 +991,47 @@ __device__ void dtn_lines(const LeafParams& P, const double* M, int ld, double* 
   const int fd = (d == 3) ? q * q : q;
   const int lines = d * fd;
   const double* X = M + P.n_pad;
-  for (int e = threadIdx.x; e < lines * m; e += NT) {
-    const int line = e / m, col = e - line * m;
-    const int a = line / fd, t = line - a * fd;
-    int base, stride;
-    if (d == 3) {
-      if (a == 0) { base = t; stride = q * q; }
-      else if (a == 1) { base = (t / q) * q * q + t % q; stride = q; }
-      else { base = t * q; stride = 1; }
-    } else {
-      if (a == 0) { base = t; stride = q; }
-      else { base = t * q; stride = 1; }
+  constexpr int U = 2;  // independent (line, column) items per thread iteration
+  for (int e0 = threadIdx.x; e0 < lines * m; e0 += NT * U) {
+    double lo[U], hi[U];
+    int a_[U], t_[U], col_[U], base_[U], stride_[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * NT;
+      const int line = (e < lines * m) ? e / m : 0;
+      col_[u] = (e < lines * m) ? e - line * m : 0;
+      a_[u] = line / fd;
+      t_[u] = line - a_[u] * fd;
+      const int a = a_[u], t = t_[u];
+      if (d == 3) {
+        if (a == 0) { base_[u] = t; stride_[u] = q * q; }
+        else if (a == 1) { base_[u] = (t / q) * q * q + t % q; stride_[u] = q; }
+        else { base_[u] = t * q; stride_[u] = 1; }
+      } else {
+        if (a == 0) { base_[u] = t; stride_[u] = q; }
+        else { base_[u] = t * q; stride_[u] = 1; }
+      }
+      lo[u] = hi[u] = 0.0;
     }
-    double lo = 0.0, hi = 0.0;
-#pragma unroll 4
     for (int i = 0; i < q; ++i) {
-      const double x = X[(size_t)(base + i * stride) * ld + col];
-      lo += s_w[a][0][i] * x;
-      hi += s_w[a][1][i] * x;
+      double x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) x[u] = X[(size_t)(base_[u] + i * stride_[u]) * ld + col_[u]];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        lo[u] += s_w[a_[u]][0][i] * x[u];
+        hi[u] += s_w[a_[u]][1][i] * x[u];
+      }
     }
-    const int b_lo = 2 * a * fd + t, b_hi = b_lo + fd;
-    T[(size_t)b_lo * m + col] = P.a_bb[(size_t)b_lo * m + col] + lo;
-    T[(size_t)b_hi * m + col] = P.a_bb[(size_t)b_hi * m + col] - hi;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * NT;
+      if (e < lines * m) {
+        const int b_lo = 2 * a_[u] * fd + t_[u], b_hi = b_lo + fd;
+        T[(size_t)b_lo * m + col_[u]] = P.a_bb[(size_t)b_lo * m + col_[u]] + lo[u];
+        T[(size_t)b_hi * m + col_[u]] = P.a_bb[(size_t)b_hi * m + col_[u]] - hi[u];
+      }
+    }
   }
 }
 

@@ -8,7 +8,9 @@
  * Reference interfaces replaced (steklov, /root/reference/pkg/src/steklov):
  *
  *   hps_plan_create            <- LeafTemplate.__init__            local_ops.py:224-306
- *                                 (D1 = diff[axis], D2 = diff@diff, a_bi, a_bb)
+ *                                 (D1 = diff[axis], D2 = diff@diff, a_bi, a_bb), corner_mode="drop"
+ *   hps_plan_create_legendre   <- the same, corner_mode="legendre"  local_ops.py:289-299,320-353
+ *                                 (+ Q = _boundary_injection, cross terms local_ops.py:375-378)
  *   hps_leaf_dtn               <- build_leaf_factors, batched      local_ops.py:439-446
  *                                 as driven by condensation.build   condensation.py:220-264
  *                                 incl. factor_interior's guard     local_ops.py:422-436
@@ -18,9 +20,13 @@
  *                                 (cache_leaf_factors path)         condensation.py:258-260,376-377
  *   hps_leaf_reduce_load       <- reduce_load.leaf_task             condensation.py:314-323
  *   hps_leaf_interior_solve    <- solve.leaf_task (recompute path)  condensation.py:372-383
+ *   hps_leaf_apply             <- explicit_rows @ full in           problems.py:473-505
+ *                                 crank_nicolson_run
  *
  * Data layout (row-major, C order, float64):
  *   coeffs : [n_leaves][ncoef][n]   ncoef = d (diagonal second-order a_kk)
+ *                                         + d(d-1)/2 (a_ab + a_ba for (0,1),(0,2),(1,2),
+ *                                           if has_cross; legendre plans only)
  *                                         + d (first order, if has_first)
  *                                         + 1 (zeroth order, if has_zeroth)
  *                                   values at the leaf's interior nodes in the
@@ -32,8 +38,9 @@
  *   stats  : [n_leaves][2]          min |pivot|, max |pivot| of the LU of A_ii;
  *                                   the caller applies the reference's
  *                                   singularity rule (min <= 1e-14 * max).
- * with n = (p-2)^d interior nodes and m = 2 d (p-2)^(d-1) boundary DOFs
- * (corner-dropping face grids).
+ * with n = (p-2)^d interior nodes and m = 2 d (p-2)^(d-1) boundary DOFs for
+ * corner-dropping face grids, m = 2 d (p-1)^(d-1) Gauss-Legendre face DOFs
+ * for legendre plans.
  */
 #ifndef HPS_LEAF_H
 #define HPS_LEAF_H
@@ -59,6 +66,14 @@ int hps_device_count(void);
 int hps_plan_create(hps_plan_t* plan, int device, int dim, int p, int has_first, int has_zeroth,
                     const double* D1, const double* D2, const double* a_bi, const double* a_bb,
                     int max_slots, size_t workspace_budget_bytes);
+/* Legendre face grids: Q [n_bnd][m] maps Gauss face data to the n_bnd
+ * Chebyshev boundary nodes (edge/corner averaged); bpos [p^dim] maps a full
+ * grid flat index (C order) to its position among those boundary nodes
+ * (-1 for interior nodes); a_bi [m][n] and a_bb [m][m] are dense. */
+int hps_plan_create_legendre(hps_plan_t* plan, int device, int dim, int p, int has_cross,
+                             int has_first, int has_zeroth, const double* D1, const double* D2,
+                             const double* a_bi, const double* a_bb, const double* Q, int n_bnd,
+                             const int* bpos, int max_slots, size_t workspace_budget_bytes);
 int hps_plan_destroy(hps_plan_t plan);
 int hps_plan_info(hps_plan_t plan, int* n_interior, int* n_boundary, int* ncoef, int* slots,
                   size_t* dtn_slot_bytes, size_t* solve_slot_bytes);
@@ -77,6 +92,11 @@ int hps_leaf_solution_operator(hps_plan_t plan, int n_leaves, const double* coef
                                double* stats, void* stream);
 int hps_leaf_reduce_load(hps_plan_t plan, int n_leaves, const double* coeffs, const double* f,
                          double* v, double* flux, double* stats, void* stream);
+/* w = rows(coeffs) [u_int; u_b]: the leaf's collocation operator applied to
+ * interior + boundary values (drop plans; the explicit Crank-Nicolson half
+ * step, reference problems.py:473-505).  u_int, w: [n_leaves][n]; u_b: [n_leaves][m]. */
+int hps_leaf_apply(hps_plan_t plan, int n_leaves, const double* coeffs, const double* u_int,
+                   const double* u_b, double* w, void* stream);
 int hps_leaf_interior_solve(hps_plan_t plan, int n_leaves, const double* coeffs, const double* ub,
                             const double* v, double* u, double* stats, void* stream);
 

@@ -72,13 +72,40 @@ def cheb_D(p):
 # Leaf template (drop-corner mode): index partition + normal blocks
 # --------------------------------------------------------------------------
 
+def _bary(x):
+    gap = x[:, None] - x[None, :]
+    np.fill_diagonal(gap, 1.0)
+    w = 1.0 / gap.prod(axis=1)
+    return w / np.abs(w).max()
+
+
+def _interp(src, dst, w):
+    """Barycentric interpolation matrix (local_ops.py:100-114)."""
+    M = np.zeros((dst.size, src.size))
+    for i, t in enumerate(dst):
+        hit = np.flatnonzero(src == t)
+        if hit.size:
+            M[i, hit[0]] = 1.0
+        else:
+            c = w / (t - src)
+            M[i] = c / c.sum()
+    return M
+
+
 class OracleTemplate:
-    """Index bookkeeping of one leaf (local_ops.py:238-306, drop mode).
+    """Index bookkeeping of one leaf (local_ops.py:238-306).
 
     Multi-indices are full-grid (0..p-1 per axis, C order, axis 0 slowest).
+    ``mode`` "drop": face-interior Chebyshev boundary DOFs; "legendre":
+    (p-1)^(d-1) Gauss nodes per face, boundary data injected by the
+    averaged tensor interpolation Q (local_ops.py:289-353).
     """
 
-    def __init__(self, widths, p):
+    def __init__(self, widths, p, mode="drop"):
+        self.mode = mode
+        if mode == "legendre":
+            self._init_legendre(widths, p)
+            return
         self.widths = tuple(float(w) for w in widths)
         self.d = d = len(self.widths)
         self.p = p
@@ -105,6 +132,51 @@ class OracleTemplate:
         self.a_bi = self._normal_block(self.interior)
         self.a_bb = self._normal_block(self.boundary)
 
+    def _init_legendre(self, widths, p):
+        self.widths = tuple(float(w) for w in widths)
+        self.d = d = len(self.widths)
+        self.p = p
+        self.D1 = [cheb_D(p) * (2.0 / w) for w in self.widths]
+        self.D2 = [D @ D for D in self.D1]
+        grid = np.indices((p,) * d).reshape(d, -1).T
+        on_end = (grid == 0) | (grid == p - 1)
+        n_end = on_end.sum(axis=1)
+        self.interior = grid[n_end == 0]
+        self.bnd_all = grid[n_end > 0]
+        xc = cheb_points(p)
+        xg, _ = np.polynomial.legendre.leggauss(p - 1)
+        w_lob = np.where(np.arange(p) % 2 == 0, 1.0, -1.0)
+        w_lob[[0, -1]] *= 0.5
+        fwd1 = _interp(xc, xg, w_lob)
+        rev1 = _interp(xg, xc, _bary(xg))
+        fd = (p - 1) ** (d - 1)
+        self.n, self.m = self.interior.shape[0], 2 * d * fd
+        self.face_dofs = fd
+        rev_face = rev1 if d == 2 else np.kron(rev1, rev1)
+        strides = p ** np.arange(d - 1, -1, -1)
+        pos = np.full(p ** d, -1)
+        pos[self.bnd_all @ strides] = np.arange(self.bnd_all.shape[0])
+        Q = np.zeros((self.bnd_all.shape[0], self.m))
+        normal = []
+        k = 0
+        for axis in range(d):
+            for side in (0, 1):
+                plane = grid[grid[:, axis] == side * (p - 1)]
+                Q[pos[plane @ strides], k * fd:(k + 1) * fd] += \
+                    (1.0 / n_end[plane @ strides])[:, None] * rev_face
+                sign = 1.0 if side else -1.0
+                edge = p - 1 if side else 0
+                mat = None
+                for dim in range(d):
+                    part = sign * self.D1[axis][edge:edge + 1, :] if dim == axis else fwd1
+                    mat = part if mat is None else np.kron(mat, part)
+                normal.append(mat)
+                k += 1
+        self.Q = Q
+        normal = np.vstack(normal)
+        self.a_bi = normal[:, self.interior @ strides]
+        self.a_bb = normal[:, self.bnd_all @ strides] @ Q
+
     def _normal_block(self, cols):
         rows = []
         for axis, side, nodes in self.faces:
@@ -122,12 +194,15 @@ def coefficient_count(d, has_first, has_zeroth):
     return d + (d if has_first else 0) + (1 if has_zeroth else 0)
 
 
-def interior_blocks(tpl, a2diag, a1=None, a0=None):
+def interior_blocks(tpl, a2diag, a1=None, a0=None, cross=None):
     """Dense (A_ii, A_ib) from coefficients at interior nodes (local_ops.py:362-398).
 
-    a2diag: (n, d) diagonal second-order coefficients; a1: (n, d) or None;
-    a0: (n,) or None.  Summation order follows collocation_rows().
+    a2diag: (n, d) diagonal second-order coefficients; cross: (n, npairs)
+    sums a_ab + a_ba for pairs (0,1), (0,2), (1,2) or None; a1: (n, d) or
+    None; a0: (n,) or None.  Summation order follows collocation_rows().
     """
+    if tpl.mode == "legendre":
+        return _interior_blocks_legendre(tpl, a2diag, a1, a0, cross)
     p, d = tpl.p, tpl.d
     R = tpl.interior
     n = R.shape[0]
@@ -161,6 +236,47 @@ def interior_blocks(tpl, a2diag, a1=None, a0=None):
     return a_ii, a_ib
 
 
+def _interior_blocks_legendre(tpl, a2diag, a1, a0, cross):
+    """Full collocation rows over the p^d grid, then A_ii and A_ib = R_b Q."""
+    p, d = tpl.p, tpl.d
+    R = tpl.interior
+    n = R.shape[0]
+    strides = p ** np.arange(d - 1, -1, -1)
+    full = np.zeros((n, p ** d))
+    rows = np.arange(n)
+
+    def add(coef, axes, mats):
+        # nodes that differ from the row node only in `axes`
+        grids = np.meshgrid(*[np.arange(p)] * len(axes), indexing="ij")
+        combos = np.stack([g.reshape(-1) for g in grids], axis=1)
+        for combo in combos:
+            J = R.copy()
+            val = np.ones(n)
+            for ax, j, D in zip(axes, combo, mats):
+                J[:, ax] = j
+                val = val * D[R[:, ax], j]
+            full[rows, J @ strides] += coef * val
+
+    for axis in range(d):
+        add(-a2diag[:, axis], [axis], [tpl.D2[axis]])
+    if cross is not None:
+        k = 0
+        for a in range(d):
+            for b in range(a + 1, d):
+                c = -cross[:, k]
+                if np.any(c):
+                    add(c, [a, b], [tpl.D1[a], tpl.D1[b]])
+                k += 1
+    if a1 is not None:
+        for axis in range(d):
+            add(a1[:, axis], [axis], [tpl.D1[axis]])
+    if a0 is not None:
+        full[rows, R @ strides] += a0
+    a_ii = full[:, R @ strides]
+    a_ib = full[:, tpl.bnd_all @ strides] @ tpl.Q
+    return a_ii, a_ib
+
+
 def lu_guarded(a_ii):
     """Pivoted dense LU with the reference's relative pivot floor (local_ops.py:422-436)."""
     lu, piv = scipy.linalg.lu_factor(a_ii, check_finite=False)
@@ -170,26 +286,26 @@ def lu_guarded(a_ii):
     return (lu, piv), float(diag.min()), float(dmax), singular
 
 
-def leaf_dtn(tpl, a2diag, a1=None, a0=None):
+def leaf_dtn(tpl, a2diag, a1=None, a0=None, cross=None):
     """DtN map and solution operator of one leaf (local_ops.py:439-446)."""
-    a_ii, a_ib = interior_blocks(tpl, a2diag, a1, a0)
+    a_ii, a_ib = interior_blocks(tpl, a2diag, a1, a0, cross)
     fac, dmin, dmax, singular = lu_guarded(a_ii)
     s = -scipy.linalg.lu_solve(fac, a_ib, check_finite=False)
     dtn = tpl.a_bb + tpl.a_bi @ s
     return dtn, s, (dmin, dmax, singular)
 
 
-def leaf_reduce_load(tpl, f_int, a2diag, a1=None, a0=None):
+def leaf_reduce_load(tpl, f_int, a2diag, a1=None, a0=None, cross=None):
     """v = A_ii^{-1} f, flux = A_bi v (condensation.py:314-323)."""
-    a_ii, _ = interior_blocks(tpl, a2diag, a1, a0)
+    a_ii, _ = interior_blocks(tpl, a2diag, a1, a0, cross)
     fac, dmin, dmax, singular = lu_guarded(a_ii)
     v = scipy.linalg.lu_solve(fac, f_int, check_finite=False)
     return v, tpl.a_bi @ v, (dmin, dmax, singular)
 
 
-def leaf_interior_solve(tpl, v, ub, a2diag, a1=None, a0=None):
+def leaf_interior_solve(tpl, v, ub, a2diag, a1=None, a0=None, cross=None):
     """u_i = v - A_ii^{-1} (A_ib u_b) (condensation.py:379-383)."""
-    a_ii, a_ib = interior_blocks(tpl, a2diag, a1, a0)
+    a_ii, a_ib = interior_blocks(tpl, a2diag, a1, a0, cross)
     fac, dmin, dmax, singular = lu_guarded(a_ii)
     return v - scipy.linalg.lu_solve(fac, a_ib @ ub, check_finite=False), (dmin, dmax, singular)
 

@@ -19,6 +19,7 @@ from .local_ops import (DROP_CORNERS, LEGENDRE_FACES, CoefficientField, LeafFact
                         build_leaf_factors, build_leaf_operator, cheb_diff_matrix, cheb_nodes,
                         face_interp_cheb_to_legendre, isotropic_field, laplace_field,
                         legendre_nodes)
-from .problems import ProblemSpec, make_problem, relative_l2_error
+from .problems import (ParabolicProblem, ProblemSpec, TimeStepConfig, crank_nicolson_run,
+                       make_parabolic, make_problem, relative_l2_error)
 
 __version__ = "0.1.0"

@@ -17,7 +17,7 @@ EXPORTS = (
     "hps_abi_version", "hps_last_error", "hps_device_count", "hps_plan_create",
     "hps_plan_destroy", "hps_plan_info", "hps_leaf_dtn", "hps_leaf_dtn_host",
     "hps_leaf_reduce_load", "hps_leaf_interior_solve", "hps_leaf_solution_operator",
-    "hps_plan_set_profile",
+    "hps_plan_set_profile", "hps_plan_create_legendre", "hps_leaf_apply",
 )
 ABI_VERSION = 1
 
@@ -34,6 +34,9 @@ def _sig(lib):
     lib.hps_device_count.restype = _I
     lib.hps_plan_create.argtypes = [ctypes.POINTER(_P), _I, _I, _I, _I, _I, _P, _P, _P, _P, _I,
                                     ctypes.c_size_t]
+    lib.hps_plan_create_legendre.argtypes = [ctypes.POINTER(_P), _I, _I, _I, _I, _I, _I, _P, _P, _P,
+                                             _P, _P, _I, _P, _I, ctypes.c_size_t]
+    lib.hps_leaf_apply.argtypes = [_P, _I, _P, _P, _P, _P, _P]
     lib.hps_plan_destroy.argtypes = [_P]
     lib.hps_plan_info.argtypes = [_P] + [ctypes.POINTER(_I)] * 4 + [ctypes.POINTER(ctypes.c_size_t)] * 2
     lib.hps_leaf_dtn.argtypes = [_P, _I, _P, _P, _P, _P]

@@ -83,6 +83,10 @@ struct LeafParams {
   int NR, NC, ld;         // rows, cols, leading dim of the slot matrix
   int wb;                 // base panel width (candidate rows live in smem)
   int has_first, has_zeroth, ncoef;
+  int legendre, has_cross;  // legendre face grids; mixed second derivatives
+  int nb, col_rb;           // Chebyshev boundary nodes; first column of the R_b / T region
+  const double* Q;          // [nb_pad][m_pad] face injection (legendre)
+  const int* bpos;          // [p^d] full-grid flat index -> Chebyshev boundary position
   int n_leaves;
   size_t slot_stride;     // doubles per slot matrix
   double* work;           // slots * slot_stride
@@ -198,6 +202,8 @@ struct TmaMaps {
   CUtensorMap b_work;     // box {B_STRIDE, KC, 1}
   CUtensorMap a_scratch;  // box {A_STRIDE, TM, 1} over [slots][TRI][TRI]
   CUtensorMap c_red;      // box {16, 8, 1} over [slots][NR][NC]: epilogue reduce-add
+  CUtensorMap a_abi;      // legendre: box {A_STRIDE, TM, 1} over the plan's a_bi [m_pad][n_pad]
+  CUtensorMap b_q;        // legendre: box {B_STRIDE, KC, 1} over the plan's Q [nb_pad][m_pad]
 };
 
 struct Ctx {
@@ -223,8 +229,11 @@ struct Ctx {
 // columns are zero-filled by TMA and masked in the epilogue.
 // ---------------------------------------------------------------------------
 
-__device__ __forceinline__ void gemm(Ctx& c, const bool sub, const bool a_scratch, int ar, int ac,
-                                     int br, int bc, int cr, int cc, int M, int N, int K) {
+// Operand sources: a_src 0 = slot, 1 = slot scratch (triangular inverse),
+// 2 = plan a_bi; b_src 0 = slot, 1 = plan Q (legendre face injection).
+__device__ __forceinline__ void gemm(Ctx& c, const bool sub, const int a_src, int ar, int ac,
+                                     const int b_src, int br, int bc, int cr, int cc, int M, int N,
+                                     int K) {
   if (M <= 0 || N <= 0 || K <= 0) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wm = warp / WN, wn = warp % WN;
@@ -234,8 +243,10 @@ __device__ __forceinline__ void gemm(Ctx& c, const bool sub, const bool a_scratc
   const int kchunks = K / KC;
   const int total = tiles * kchunks;
   double* smem = c.smem;
-  const CUtensorMap* mapA = a_scratch ? &c.maps->a_scratch : &c.maps->a_work;
-  const CUtensorMap* mapB = &c.maps->b_work;
+  const CUtensorMap* mapA =
+      a_src == 0 ? &c.maps->a_work : (a_src == 1 ? &c.maps->a_scratch : &c.maps->a_abi);
+  const CUtensorMap* mapB = b_src == 0 ? &c.maps->b_work : &c.maps->b_q;
+  const int a_slot = a_src == 2 ? 0 : c.slot, b_slot = b_src == 1 ? 0 : c.slot;
   double* C = c.M + (size_t)cr * c.ld + cc;
 
   // every thread's earlier global writes must be visible to the TMA reads below
@@ -253,13 +264,11 @@ __device__ __forceinline__ void gemm(Ctx& c, const bool sub, const bool a_scratc
     double* sa = smem + s * STAGE_DBL;
     double* sb = sa + STAGE_A;
     mbar_expect_tx(&c.full[s], STAGE_BYTES);
-    if (a_scratch)
-      tma_load_3d(sa, mapA, p_kc * KC, tm * TM, c.slot, &c.full[s]);
-    else
-      tma_load_3d(sa, mapA, ac + p_kc * KC, ar + tm * TM, c.slot, &c.full[s]);
-    tma_load_3d(sb, mapB, bc + tn * TN, br + p_kc * KC, c.slot, &c.full[s]);
+    tma_load_3d(sa, mapA, ac + p_kc * KC, ar + tm * TM, a_slot, &c.full[s]);
+    tma_load_3d(sb, mapB, bc + tn * TN, br + p_kc * KC, b_slot, &c.full[s]);
     if (sub && p_kc == 0) {
-      for (int r = 0; r < TM; r += KC) tma_prefetch_3d(mapB, cc + tn * TN, cr + tm * TM + r, c.slot);
+      for (int r = 0; r < TM; r += KC)
+        tma_prefetch_3d(&c.maps->b_work, cc + tn * TN, cr + tm * TM + r, c.slot);
     }
     ++p_it;
     if (++p_kc == kchunks) { p_kc = 0; ++p_tile; }
@@ -821,6 +830,9 @@ enum OpKind : int {
   OP_INV_UPPER = 3,  // scratch := inv(upper M[a..a+b, a..a+b])
   OP_GEMM_SUB = 4,   // M[c_r.., c_c..] -= M[a_r.., a_c..] * M[b_r.., b_c..]  (Mdim, Ndim, Kdim)
   OP_GEMM_SET = 5,   // M[c_r.., c_c..]  = scratch * M[b_r.., b_c..]
+  OP_GEMM_SET_Q = 6, // legendre: A_ib = R_b (slot) * Q (plan)
+  OP_GEMM_SUB_ABI = 7,  // legendre: T -= a_bi (plan) * X (slot)
+  OP_COPY_ABB = 8,   // legendre: T region := a_bb (rows [0,m), cols [a, a+m))
 };
 
 struct Op {
@@ -865,39 +877,106 @@ __device__ __forceinline__ int boundary_index(const LeafParams& P, int a, int si
   return (2 * a + side) * fd + t;
 }
 
-// A[row r][col with multi-index J]; coefficient pointer layout (ncoef, n)
+// A[row r][col with multi-index J]; coefficient pointer layout (ncoef, n):
+// [a_kk (d) | a_ab + a_ba for (0,1),(0,2),(1,2) (if cross) | b_k (d) | c].
+// Sum order follows collocation_rows (local_ops.py:370-387): second order
+// x, y, z; cross pairs; first order x, y, z; zeroth.
 __device__ double op_entry(const LeafParams& P, const double* cf, int r, const int* I, const int* J) {
   const int p = P.p, d = P.d;
   double v = 0.0;
+  int ndiff = 0;
+  for (int k = 0; k < d; ++k) ndiff += (I[k] != J[k]);
   bool line[3];
-  for (int a = 0; a < 3; ++a) {
-    bool ok = true;
-    for (int k = 0; k < d; ++k)
-      if (k != a && I[k] != J[k]) ok = false;
-    line[a] = (a < d) && ok;
-  }
+  for (int a = 0; a < 3; ++a) line[a] = (a < d) && (ndiff == 0 || (ndiff == 1 && I[a] != J[a]));
   for (int a = 0; a < d; ++a)
     if (line[a]) v = __dadd_rn(v, __dmul_rn(-cf[a * P.n + r], P.D2[(a * p + I[a]) * p + J[a]]));
   int k = d;
+  if (P.has_cross) {
+    int pair = 0;
+    for (int a = 0; a < d; ++a) {
+      for (int b = a + 1; b < d; ++b, ++pair) {
+        bool in_plane = true;  // J differs from I at most in axes a and b
+        for (int t = 0; t < d; ++t)
+          if (t != a && t != b && I[t] != J[t]) in_plane = false;
+        if (in_plane) {
+          const double kr = __dmul_rn(P.D1[(a * p + I[a]) * p + J[a]], P.D1[(b * p + I[b]) * p + J[b]]);
+          v = __dadd_rn(v, __dmul_rn(-cf[(k + pair) * P.n + r], kr));
+        }
+      }
+    }
+    k += d * (d - 1) / 2;
+  }
   if (P.has_first) {
     for (int a = 0; a < d; ++a)
       if (line[a]) v = __dadd_rn(v, __dmul_rn(cf[(k + a) * P.n + r], P.D1[(a * p + I[a]) * p + J[a]]));
     k += d;
   }
-  if (P.has_zeroth) {
-    bool same = true;
-    for (int a = 0; a < d; ++a)
-      if (I[a] != J[a]) same = false;
-    if (same) v = __dadd_rn(v, cf[k * P.n + r]);
-  }
+  if (P.has_zeroth && ndiff == 0) v = __dadd_rn(v, cf[k * P.n + r]);
   return v;
 }
 
+// Nonzero pattern of row I: the d grid lines through I (d*p positions, the
+// diagonal once) and, with cross terms, the strict interiors of the coordinate
+// planes through I ((p-1)^2 each).  Returns the multi-index J of item e.
+__device__ __forceinline__ int pattern_size(const LeafParams& P) {
+  return P.d * P.p + (P.has_cross ? (P.d * (P.d - 1) / 2) * (P.p - 1) * (P.p - 1) : 0);
+}
+__device__ __forceinline__ bool pattern_item(const LeafParams& P, const int* I, int e, int* J) {
+  const int p = P.p, d = P.d;
+  J[0] = I[0]; J[1] = I[1]; J[2] = I[2];
+  if (e < d * p) {
+    const int a = e / p, pos = e - a * p;
+    if (pos == I[a] && a > 0) return false;
+    J[a] = pos;
+    return true;
+  }
+  e -= d * p;
+  const int per = (p - 1) * (p - 1);
+  const int pair = e / per, w = e - pair * per;
+  const int a = (d == 3 && pair == 2) ? 1 : 0, b = (d == 2) ? 1 : (pair == 0 ? 1 : 2);
+  int ja = w / (p - 1), jb = w - ja * (p - 1);
+  ja += (ja >= I[a]);  // skip I[a] / I[b]: strict plane interior
+  jb += (jb >= I[b]);
+  J[a] = ja;
+  J[b] = jb;
+  return true;
+}
+
+__device__ __forceinline__ bool is_interior(const LeafParams& P, const int* J) {
+  for (int k = 0; k < P.d; ++k)
+    if (J[k] == 0 || J[k] == P.p - 1) return false;
+  return true;
+}
+
+__device__ __forceinline__ int full_flat(const LeafParams& P, const int* J) {
+  int f = 0;
+  for (int k = 0; k < P.d; ++k) f = f * P.p + J[k];
+  return f;
+}
+
 // Fill the slot matrix.  Warp per row: zero the row, then scatter structural nonzeros.
-__device__ void assemble(const LeafParams& P, double* M, int leaf) {
+// Drop mode: boundary endpoints are the face DOF columns of A_ib.  Legendre
+// mode: boundary nodes are Chebyshev boundary nodes; their entries R_b go to
+// the slot's R_b region (A_ib = R_b Q is a GEMM op) or, for interior solves,
+// are contracted with Q u_b directly.
+__device__ void assemble(const LeafParams& P, double* M, int leaf, double* smem) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double* cf = P.coeffs + (size_t)leaf * P.ncoef * P.n;
-  const int p = P.p, d = P.d;
+  const int d = P.d;
+  const bool solve_mode = (P.mode == MODE_REDUCE || P.mode == MODE_INTERIOR);
+  double* qub = smem;  // legendre interior solve: (Q u_b)[g], g over Chebyshev boundary nodes
+  if (P.legendre && P.mode == MODE_INTERIOR) {
+    const double* ub = P.in0 + (size_t)leaf * P.m;
+    for (int g = warp; g < P.nb; g += NT / 32) {
+      double acc = 0.0;
+      for (int c = lane; c < P.m; c += 32) acc += P.Q[(size_t)g * P.m_pad + c] * ub[c];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      if (lane == 0) qub[g] = acc;
+    }
+    __syncthreads();
+  }
+  const int npat = pattern_size(P);
   for (int r = warp; r < P.NR; r += NT / 32) {
     double* row = M + (size_t)r * P.ld;
     double2* row2 = reinterpret_cast<double2*>(row);
@@ -906,41 +985,59 @@ __device__ void assemble(const LeafParams& P, double* M, int leaf) {
     if (r < P.n) {
       int I[3];
       interior_multi(P, r, I);
-      // each (axis, position) on the d lines through node I: interior neighbour or face node
-      for (int e = lane; e < d * p; e += 32) {
-        const int a = e / p, pos = e - a * p;
-        int J[3] = {I[0], I[1], I[2]};
-        J[a] = pos;
-        if (pos == I[a] && a > 0) continue;  // diagonal written once (a == 0)
-        int col;
-        if (pos == 0 || pos == p - 1) {
-          if (P.mode != MODE_DTN && P.mode != MODE_SOLOP) continue;  // solve modes: rhs column
-          col = P.n_pad + boundary_index(P, a, pos == p - 1 ? 1 : 0, I);
-        } else {
+      double rhs = 0.0;  // interior solve: A_ib u_b accumulated over the pattern
+      for (int e = lane; e < npat; e += 32) {
+        int J[3];
+        if (!pattern_item(P, I, e, J)) continue;
+        if (is_interior(P, J)) {
           int flat = 0;
           for (int k = 0; k < d; ++k) flat = flat * P.q + (J[k] - 1);
-          col = flat;
+          row[flat] = op_entry(P, cf, r, I, J);
+        } else if (P.legendre) {
+          if (P.mode == MODE_INTERIOR) rhs += op_entry(P, cf, r, I, J) * qub[P.bpos[full_flat(P, J)]];
+          else if (!solve_mode) row[P.col_rb + P.bpos[full_flat(P, J)]] = op_entry(P, cf, r, I, J);
+        } else if (!solve_mode) {
+          // drop mode: line endpoints are face-interior DOFs
+          int a = 0;
+          for (int k = 0; k < d; ++k)
+            if (J[k] != I[k]) a = k;
+          row[P.n_pad + boundary_index(P, a, J[a] == P.p - 1 ? 1 : 0, I)] = op_entry(P, cf, r, I, J);
         }
-        row[col] = op_entry(P, cf, r, I, J);
       }
       if (P.mode == MODE_REDUCE && lane == 0) {
         row[P.n_pad] = P.in0[(size_t)leaf * P.n + r];
-      } else if (P.mode == MODE_INTERIOR && lane == 0) {
-        // rhs = A_ib u_b over its 2d structural nonzeros, in column (face) order
-        const double* ub = P.in0 + (size_t)leaf * P.m;
-        double s = 0.0;
-        for (int a = 0; a < d; ++a) {
-          for (int side = 0; side < 2; ++side) {
-            int J[3] = {I[0], I[1], I[2]};
-            J[a] = side ? p - 1 : 0;
-            s += op_entry(P, cf, r, I, J) * ub[boundary_index(P, a, side, I)];
+      } else if (P.mode == MODE_INTERIOR) {
+        if (P.legendre) {
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) rhs += __shfl_xor_sync(0xffffffffu, rhs, off);
+          if (lane == 0) row[P.n_pad] = rhs;
+        } else if (lane == 0) {
+          // rhs = A_ib u_b over its 2d structural nonzeros, in column (face) order
+          const double* ub = P.in0 + (size_t)leaf * P.m;
+          double sacc = 0.0;
+          for (int a = 0; a < d; ++a) {
+            for (int side = 0; side < 2; ++side) {
+              int J[3] = {I[0], I[1], I[2]};
+              J[a] = side ? P.p - 1 : 0;
+              sacc += op_entry(P, cf, r, I, J) * ub[boundary_index(P, a, side, I)];
+            }
           }
+          row[P.n_pad] = sacc;
         }
-        row[P.n_pad] = s;
       }
     } else if (r < P.n_pad) {
       if (lane == 0) row[r] = 1.0;  // dummy pivot keeps padding inert
     }
+  }
+  __syncthreads();
+}
+
+// Legendre DtN: T region (rows [0, m), cols [col, col + m_pad)) := a_bb, zero padded.
+__device__ void copy_abb(const LeafParams& P, Ctx& c, int col) {
+  __syncthreads();
+  for (int e = threadIdx.x; e < P.m_pad * P.m_pad; e += NT) {
+    const int i = e / P.m_pad, j = e - i * P.m_pad;
+    c.M[(size_t)i * c.ld + col + j] = (i < P.m && j < P.m) ? P.a_bb[(size_t)i * P.m + j] : 0.0;
   }
   __syncthreads();
 }
@@ -1076,7 +1173,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     const int leaf = s_leaf;
     if (leaf >= P.n_leaves) break;
     long long t0 = clock64();
-    assemble(P, c.M, leaf);
+    assemble(P, c.M, leaf, c.smem);
     if (threadIdx.x == 0) { s_pmin = INFINITY; s_pmax = 0.0; }
     __syncthreads();
     if (prof && threadIdx.x == 0) { prof[6] += clock64() - t0; prof[9] += 1; }
@@ -1088,9 +1185,13 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
         case OP_SWAP: apply_swaps(c, op.a, op.b, op.c, op.d); break;
         case OP_INV_LOWER: invert_unit_lower(c, op.a, op.b); break;
         case OP_INV_UPPER: invert_upper(c, op.a, op.b); break;
+        case OP_COPY_ABB: copy_abb(P, c, op.a); break;
         default: {
-          const bool sub = (op.kind == OP_GEMM_SUB);
-          gemm(c, sub, !sub, op.ar, op.ac, op.br, op.bc, op.cr, op.cc, op.Mdim, op.Ndim, op.Kdim);
+          const bool sub = (op.kind == OP_GEMM_SUB || op.kind == OP_GEMM_SUB_ABI);
+          const int a_src = op.kind == OP_GEMM_SET ? 1 : (op.kind == OP_GEMM_SUB_ABI ? 2 : 0);
+          const int b_src = op.kind == OP_GEMM_SET_Q ? 1 : 0;
+          gemm(c, sub, a_src, op.ar, op.ac, b_src, op.br, op.bc, op.cr, op.cc, op.Mdim, op.Ndim,
+               op.Kdim);
         }
       }
       if (prof && threadIdx.x == 0) {
@@ -1099,7 +1200,9 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
       }
     }
     if (prof) t0 = clock64();
-    if (P.mode == MODE_DTN) {
+    if (P.mode == MODE_DTN && P.legendre) {
+      copy_block(c.M + P.col_rb, c.ld, P.out0 + (size_t)leaf * P.m * P.m, P.m, P.m, P.m, false);
+    } else if (P.mode == MODE_DTN) {
       dtn_lines(P, c.M, c.ld, P.out0 + (size_t)leaf * P.m * P.m);
     } else if (P.mode == MODE_SOLOP) {
       copy_block(c.M + P.n_pad, c.ld, P.out0 + (size_t)leaf * P.n * P.m, P.m, P.n, P.m, true);
@@ -1197,6 +1300,46 @@ struct ProgramBuilder {
   }
 };
 
+// Matrix-free collocation rows: w = A_rows(coeffs) [u_int ; u_b] per leaf
+// (the explicit half of a Crank-Nicolson step, reference problems.py:473-505:
+// explicit_rows @ full with the leaf's interior + boundary values scattered into
+// the p^d grid, corner/edge nodes zero).  Warp per interior row.
+__global__ void __launch_bounds__(256) hps_apply_kernel(LeafParams P) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int npat = pattern_size(P);
+  for (long long item = gw; item < (long long)P.n_leaves * P.n; item += nw) {
+    const int leaf = (int)(item / P.n), r = (int)(item - (long long)leaf * P.n);
+    const double* cf = P.coeffs + (size_t)leaf * P.ncoef * P.n;
+    const double* ui = P.in0 + (size_t)leaf * P.n;
+    const double* ub = P.in1 + (size_t)leaf * P.m;
+    int I[3];
+    interior_multi(P, r, I);
+    double acc = 0.0;
+    for (int e = lane; e < npat; e += 32) {
+      int J[3];
+      if (!pattern_item(P, I, e, J)) continue;
+      double x;
+      if (is_interior(P, J)) {
+        int flat = 0;
+        for (int k = 0; k < P.d; ++k) flat = flat * P.q + (J[k] - 1);
+        x = ui[flat];
+      } else {
+        int a = 0, nd = 0;
+        for (int k = 0; k < P.d; ++k)
+          if (J[k] != I[k]) { a = k; ++nd; }
+        if (nd != 1) continue;  // corner / edge nodes carry no value in drop mode
+        x = ub[boundary_index(P, a, J[a] == P.p - 1 ? 1 : 0, I)];
+      }
+      acc += op_entry(P, cf, r, I, J) * x;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) P.out0[(size_t)leaf * P.n + r] = acc;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Host side: plan + C ABI
 // ---------------------------------------------------------------------------
@@ -1220,6 +1363,9 @@ struct hps_plan_s {
   int device = 0;
   int d = 0, p = 0, q = 0, n = 0, m = 0, n_pad = 0, m_pad = 0, wb = 8;
   int has_first = 0, has_zeroth = 0, ncoef = 0;
+  int legendre = 0, has_cross = 0, nb = 0, nb_pad = 0;
+  double *Q = nullptr, *a_bi_pad = nullptr;  // legendre: [nb_pad][m_pad], [m_pad][n_pad]
+  int* bpos = nullptr;                        // legendre: [p^d]
   int sms = 0, slots = 0;
   size_t budget = 0;
   double *D1 = nullptr, *D2 = nullptr, *a_bi = nullptr, *a_bb = nullptr;
@@ -1273,17 +1419,26 @@ static int round16(int x) { return (x + 15) / 16 * 16; }
 static void mode_dims(const hps_plan_s* P, int mode, int* NR, int* NC) {
   if (mode == MODE_DTN || mode == MODE_SOLOP) {
     *NR = P->n_pad;
-    *NC = P->n_pad + P->m_pad;
+    *NC = P->n_pad + P->m_pad + (P->legendre ? P->nb_pad : 0);
   } else {
     *NR = P->n_pad;
     *NC = P->n_pad + RHS_COLS;
   }
 }
 
+// Rows allocated per slot: the LU rows, or more when the legendre T region
+// (m_pad rows) does not fit below them.
+static int rows_alloc(const hps_plan_s* P, int mode) {
+  int NR, NC;
+  mode_dims(P, mode, &NR, &NC);
+  if (P->legendre && mode == MODE_DTN && P->m_pad > NR) return P->m_pad;
+  return NR;
+}
+
 static size_t slot_doubles(const hps_plan_s* P, int mode) {
   int NR, NC;
   mode_dims(P, mode, &NR, &NC);
-  return (size_t)NR * NC;
+  return (size_t)rows_alloc(P, mode) * NC;
 }
 
 static int ensure_workspace(hps_plan_s* P, int mode, int want_slots) {
@@ -1299,12 +1454,19 @@ static int ensure_workspace(hps_plan_s* P, int mode, int want_slots) {
     if (!P->maps_ok[mode]) {
       int NR, NC;
       mode_dims(P, mode, &NR, &NC);
+      NR = rows_alloc(P, mode);
       TmaMaps& m = P->maps[mode];
       if (make_map(&m.a_work, P->work, NC, NR, P->ws_slots, NC, per, A_STRIDE, TM, true) ||
           make_map(&m.b_work, P->work, NC, NR, P->ws_slots, NC, per, B_STRIDE, KC) ||
           make_map(&m.a_scratch, P->scratch, TRI_BLOCK, TRI_BLOCK, P->ws_slots, TRI_BLOCK,
                    TRI_BLOCK * TRI_BLOCK, A_STRIDE, TM, true) ||
           make_map(&m.c_red, P->work, NC, NR, P->ws_slots, NC, per, 16, 8))
+        return -1;
+      if (P->legendre &&
+          (make_map(&m.a_abi, P->a_bi_pad, P->n_pad, P->m_pad, 1, P->n_pad,
+                    (size_t)P->m_pad * P->n_pad, A_STRIDE, TM, true) ||
+           make_map(&m.b_q, P->Q, P->m_pad, P->nb_pad, 1, P->m_pad, (size_t)P->nb_pad * P->m_pad,
+                    B_STRIDE, KC)))
         return -1;
       P->maps_ok[mode] = 1;
     }
@@ -1328,10 +1490,23 @@ static int ensure_program(hps_plan_s* P, int mode) {
   int NR, NC;
   mode_dims(P, mode, &NR, &NC);
   ProgramBuilder b;
+  // working columns: [A_ii | A_ib or rhs]; legendre adds an R_b / T region after them
+  const bool leg_op = P->legendre && (mode == MODE_DTN || mode == MODE_SOLOP);
+  const int NW = leg_op ? P->n_pad + P->m_pad : NC;
+  const int col_rb = P->n_pad + P->m_pad;
+  if (leg_op)  // A_ib = R_b Q
+    b.gemm(OP_GEMM_SET_Q, 0, col_rb, 0, 0, 0, P->n_pad, P->n_pad, P->m_pad, P->nb_pad);
   b.lu(0, P->n_pad, NR);
-  b.swaps(0, P->n_pad, P->n_pad, NC);
-  b.trsm_lower(0, P->n_pad, P->n_pad, NC);
-  b.trsm_upper(0, P->n_pad, P->n_pad, NC);
+  b.swaps(0, P->n_pad, P->n_pad, NW);
+  b.trsm_lower(0, P->n_pad, P->n_pad, NW);
+  b.trsm_upper(0, P->n_pad, P->n_pad, NW);
+  if (leg_op && mode == MODE_DTN) {  // T = a_bb - a_bi X in the (now free) R_b region
+    Op o{};
+    o.kind = OP_COPY_ABB;
+    o.a = col_rb;
+    b.ops.push_back(o);
+    b.gemm(OP_GEMM_SUB_ABI, 0, 0, 0, P->n_pad, 0, col_rb, P->m_pad, P->m_pad, P->n_pad);
+  }
   CK(cudaMalloc(&P->prog[mode], b.ops.size() * sizeof(Op)));
   CK(cudaMemcpy(P->prog[mode], b.ops.data(), b.ops.size() * sizeof(Op), cudaMemcpyHostToDevice));
   P->prog_len[mode] = (int)b.ops.size();
@@ -1356,6 +1531,8 @@ static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, c
   L.ld = L.NC;
   L.wb = P->wb;
   L.has_first = P->has_first; L.has_zeroth = P->has_zeroth; L.ncoef = P->ncoef;
+  L.legendre = P->legendre; L.has_cross = P->has_cross; L.nb = P->nb;
+  L.col_rb = P->n_pad + P->m_pad; L.Q = P->Q; L.bpos = P->bpos;
   L.n_leaves = n_leaves;
   L.slot_stride = slot_doubles(P, mode);
   L.work = P->work; L.piv = P->piv; L.scratch = P->scratch;
@@ -1387,24 +1564,32 @@ int hps_device_count(void) {
   return n;
 }
 
-int hps_plan_create(hps_plan_t* out, int device, int dim, int p, int has_first, int has_zeroth,
-                    const double* D1, const double* D2, const double* a_bi, const double* a_bb,
-                    int max_slots, size_t workspace_budget_bytes) {
+static int plan_create(hps_plan_t* out, int device, int dim, int p, int legendre, int has_cross,
+                       int has_first, int has_zeroth, const double* D1, const double* D2,
+                       const double* a_bi, const double* a_bb, const double* Q, int n_bnd,
+                       const int* bpos, int max_slots, size_t workspace_budget_bytes) {
   if (!out) return fail("null plan pointer");
   *out = nullptr;
   if (dim != 2 && dim != 3) return fail("dimension must be 2 or 3");
   if (p < 4) return fail("p must be >= 4");
+  if (has_cross && !legendre) return fail("cross terms require legendre face grids");
   hps_plan_s* P = new hps_plan_s();
   P->device = device;
   P->d = dim; P->p = p; P->q = p - 2;
+  P->legendre = legendre ? 1 : 0;
+  P->has_cross = has_cross ? 1 : 0;
   P->n = 1; for (int k = 0; k < dim; ++k) P->n *= P->q;
-  const int fd = (dim == 3) ? P->q * P->q : P->q;
+  const int fq = legendre ? p - 1 : p - 2;
+  const int fd = (dim == 3) ? fq * fq : fq;
   P->m = 2 * dim * fd;
   P->n_pad = round16(P->n);
   P->m_pad = round16(P->m);
+  P->nb = legendre ? n_bnd : 0;
+  P->nb_pad = legendre ? round16(n_bnd) : 0;
+  if (legendre && P->nb_pad < P->m_pad) P->nb_pad = P->m_pad;  // region also hosts T
   P->has_first = has_first ? 1 : 0;
   P->has_zeroth = has_zeroth ? 1 : 0;
-  P->ncoef = dim + (has_first ? dim : 0) + (has_zeroth ? 1 : 0);
+  P->ncoef = dim + (has_cross ? dim * (dim - 1) / 2 : 0) + (has_first ? dim : 0) + (has_zeroth ? 1 : 0);
   int wb = 8;
   while (wb > 1 && ((size_t)P->n_pad * wb + 32 * wb) * 8 > PANEL_SMEM_CAP) wb >>= 1;
   // (the panel step also needs max(n_pad*wb, 1024) + 32*wb doubles; 1024 + 256 always fits)
@@ -1416,7 +1601,8 @@ int hps_plan_create(hps_plan_t* out, int device, int dim, int p, int has_first, 
   const size_t tab = (size_t)dim * p * p * 8;
   if (cudaMalloc(&P->D1, tab) != cudaSuccess || cudaMalloc(&P->D2, tab) != cudaSuccess ||
       cudaMalloc(&P->a_bi, (size_t)P->m * P->n * 8) != cudaSuccess ||
-      cudaMalloc(&P->a_bb, (size_t)P->m * P->m * 8) != cudaSuccess) {
+      cudaMalloc(&P->a_bb, (size_t)P->m * P->m * 8) != cudaSuccess ||
+      cudaMalloc(&P->leaf_counter, sizeof(int)) != cudaSuccess) {
     hps_plan_destroy(P);
     return fail("device allocation of templates failed");
   }
@@ -1424,13 +1610,44 @@ int hps_plan_create(hps_plan_t* out, int device, int dim, int p, int has_first, 
   cudaMemcpy(P->D2, D2, tab, cudaMemcpyHostToDevice);
   cudaMemcpy(P->a_bi, a_bi, (size_t)P->m * P->n * 8, cudaMemcpyHostToDevice);
   cudaMemcpy(P->a_bb, a_bb, (size_t)P->m * P->m * 8, cudaMemcpyHostToDevice);
-  if (cudaMalloc(&P->leaf_counter, sizeof(int)) != cudaSuccess) {
-    hps_plan_destroy(P);
-    return fail("device allocation of the leaf counter failed");
+  if (legendre) {
+    // zero-padded copies for the TMA-fed GEMMs: Q [nb_pad][m_pad], a_bi [m_pad][n_pad]
+    std::vector<double> qp((size_t)P->nb_pad * P->m_pad, 0.0), ap((size_t)P->m_pad * P->n_pad, 0.0);
+    for (int g = 0; g < n_bnd; ++g)
+      for (int c = 0; c < P->m; ++c) qp[(size_t)g * P->m_pad + c] = Q[(size_t)g * P->m + c];
+    for (int b = 0; b < P->m; ++b)
+      for (int k = 0; k < P->n; ++k) ap[(size_t)b * P->n_pad + k] = a_bi[(size_t)b * P->n + k];
+    size_t full = 1;
+    for (int k = 0; k < dim; ++k) full *= p;
+    if (cudaMalloc(&P->Q, qp.size() * 8) != cudaSuccess ||
+        cudaMalloc(&P->a_bi_pad, ap.size() * 8) != cudaSuccess ||
+        cudaMalloc(&P->bpos, full * 4) != cudaSuccess) {
+      hps_plan_destroy(P);
+      return fail("device allocation of legendre templates failed");
+    }
+    cudaMemcpy(P->Q, qp.data(), qp.size() * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(P->a_bi_pad, ap.data(), ap.size() * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(P->bpos, bpos, full * 4, cudaMemcpyHostToDevice);
   }
   if (cudaGetLastError() != cudaSuccess) { hps_plan_destroy(P); return fail("template upload failed"); }
   *out = P;
   return 0;
+}
+
+int hps_plan_create(hps_plan_t* out, int device, int dim, int p, int has_first, int has_zeroth,
+                    const double* D1, const double* D2, const double* a_bi, const double* a_bb,
+                    int max_slots, size_t workspace_budget_bytes) {
+  return plan_create(out, device, dim, p, 0, 0, has_first, has_zeroth, D1, D2, a_bi, a_bb, nullptr,
+                     0, nullptr, max_slots, workspace_budget_bytes);
+}
+
+int hps_plan_create_legendre(hps_plan_t* out, int device, int dim, int p, int has_cross,
+                             int has_first, int has_zeroth, const double* D1, const double* D2,
+                             const double* a_bi, const double* a_bb, const double* Q, int n_bnd,
+                             const int* bpos, int max_slots, size_t workspace_budget_bytes) {
+  if (!Q || !bpos || n_bnd <= 0) return fail("legendre plan needs Q and the boundary position table");
+  return plan_create(out, device, dim, p, 1, has_cross, has_first, has_zeroth, D1, D2, a_bi, a_bb, Q,
+                     n_bnd, bpos, max_slots, workspace_budget_bytes);
 }
 
 int hps_plan_destroy(hps_plan_t P) {
@@ -1438,6 +1655,7 @@ int hps_plan_destroy(hps_plan_t P) {
   cudaSetDevice(P->device);
   cudaFree(P->D1); cudaFree(P->D2); cudaFree(P->a_bi); cudaFree(P->a_bb);
   cudaFree(P->leaf_counter);
+  cudaFree(P->Q); cudaFree(P->a_bi_pad); cudaFree(P->bpos);
   cudaFree(P->work); cudaFree(P->piv); cudaFree(P->scratch);
   for (int k = 0; k < 4; ++k) cudaFree(P->prog[k]);
   if (P->h_stage) cudaFreeHost(P->h_stage);
@@ -1487,6 +1705,27 @@ int hps_leaf_interior_solve(hps_plan_t P, int n_leaves, const double* coeffs, co
                             const double* v, double* u, double* stats, void* stream) {
   if (!P) return fail("null plan");
   return launch(P, MODE_INTERIOR, n_leaves, coeffs, ub, v, u, nullptr, stats, (cudaStream_t)stream);
+}
+
+int hps_leaf_apply(hps_plan_t P, int n_leaves, const double* coeffs, const double* u_int,
+                   const double* u_b, double* w, void* stream) {
+  if (!P) return fail("null plan");
+  if (P->legendre) return fail("hps_leaf_apply supports corner-dropping face grids");
+  if (n_leaves <= 0) return 0;
+  CK(cudaSetDevice(P->device));
+  LeafParams L;
+  memset(&L, 0, sizeof(L));
+  L.d = P->d; L.p = P->p; L.q = P->q; L.n = P->n; L.m = P->m;
+  L.has_first = P->has_first; L.has_zeroth = P->has_zeroth; L.ncoef = P->ncoef;
+  L.has_cross = 0; L.legendre = 0;
+  L.D1 = P->D1; L.D2 = P->D2;
+  L.coeffs = coeffs; L.in0 = u_int; L.in1 = u_b; L.out0 = w; L.n_leaves = n_leaves;
+  const long long warps = (long long)n_leaves * P->n;
+  long long blocks = (warps + 7) / 8;
+  if (blocks > 148LL * 16) blocks = 148LL * 16;
+  hps_apply_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(L);
+  CK(cudaGetLastError());
+  return 0;
 }
 
 // Host-buffer DtN with the two-level schedule on the device: chunks of

@@ -25,7 +25,7 @@ import numpy as np
 
 from . import _native
 from .errors import ConfigError, NativeUnavailableError
-from .local_ops import DROP_CORNERS, LeafTemplate, coefficient_layout
+from .local_ops import DROP_CORNERS, LEGENDRE_FACES, LeafTemplate, coefficient_layout
 
 
 def _torch():
@@ -49,10 +49,10 @@ class LeafEngine:
     _plans = {}
 
     def __init__(self, template: LeafTemplate, has_first: bool, has_zeroth: bool,
-                 device: int = 0, max_slots: int = 0, workspace_budget: int = 0):
-        if template.corner_mode != DROP_CORNERS:
-            raise ConfigError("the CUDA leaf engine currently implements corner-dropping face "
-                              "grids only; legendre face grids are not available on the GPU path")
+                 device: int = 0, max_slots: int = 0, workspace_budget: int = 0,
+                 has_cross: bool = False):
+        if has_cross and template.corner_mode != LEGENDRE_FACES:
+            raise ConfigError("cross-derivative terms require legendre face grids")
         self.lib = _native.load()
         torch = _torch()
         self.torch = torch
@@ -61,17 +61,31 @@ class LeafEngine:
         self.d, self.p = template.d, template.p
         self.n, self.m = template.n_interior, template.n_boundary
         self.has_first, self.has_zeroth = bool(has_first), bool(has_zeroth)
-        self.ncoef = self.d + (self.d if has_first else 0) + (1 if has_zeroth else 0)
+        self.has_cross = bool(has_cross)
+        self.legendre = template.corner_mode == LEGENDRE_FACES
+        self.ncoef = (self.d + (self.d * (self.d - 1) // 2 if has_cross else 0)
+                      + (self.d if has_first else 0) + (1 if has_zeroth else 0))
         D1 = np.ascontiguousarray(np.stack(template.diff))
         D2 = np.ascontiguousarray(np.stack(template.diff2))
         a_bi = np.ascontiguousarray(template.a_bi)
         a_bb = np.ascontiguousarray(template.a_bb)
         plan = ctypes.c_void_p()
         with torch.cuda.device(self.device):
-            _native.check(self.lib.hps_plan_create(
-                ctypes.byref(plan), self.device, self.d, self.p, int(has_first), int(has_zeroth),
-                _np_ptr(D1), _np_ptr(D2), _np_ptr(a_bi), _np_ptr(a_bb), int(max_slots),
-                int(workspace_budget)))
+            if self.legendre:
+                Q = np.ascontiguousarray(template._boundary_injection)
+                bpos = np.full(template.n_grid, -1, dtype=np.int32)
+                bpos[template.boundary_all_idx] = np.arange(template.boundary_all_idx.size,
+                                                            dtype=np.int32)
+                _native.check(self.lib.hps_plan_create_legendre(
+                    ctypes.byref(plan), self.device, self.d, self.p, int(has_cross),
+                    int(has_first), int(has_zeroth), _np_ptr(D1), _np_ptr(D2), _np_ptr(a_bi),
+                    _np_ptr(a_bb), _np_ptr(Q), int(Q.shape[0]), _np_ptr(bpos), int(max_slots),
+                    int(workspace_budget)))
+            else:
+                _native.check(self.lib.hps_plan_create(
+                    ctypes.byref(plan), self.device, self.d, self.p, int(has_first),
+                    int(has_zeroth), _np_ptr(D1), _np_ptr(D2), _np_ptr(a_bi), _np_ptr(a_bb),
+                    int(max_slots), int(workspace_budget)))
         self.plan = plan
         n, m, nc, slots = (ctypes.c_int() for _ in range(4))
         dtn_b, sol_b = ctypes.c_size_t(), ctypes.c_size_t()
@@ -94,12 +108,12 @@ class LeafEngine:
 
     @classmethod
     def for_template(cls, template: LeafTemplate, coeffs, device: int = 0, **kw) -> "LeafEngine":
-        has_first, has_zeroth = coefficient_layout(coeffs)
-        key = (template.widths, template.p, template.corner_mode, has_first, has_zeroth, device,
-               tuple(sorted(kw.items())))
+        has_first, has_zeroth, has_cross = coefficient_layout(coeffs)
+        key = (template.widths, template.p, template.corner_mode, has_first, has_zeroth, has_cross,
+               device, tuple(sorted(kw.items())))
         eng = cls._plans.get(key)
         if eng is None:
-            eng = cls(template, has_first, has_zeroth, device=device, **kw)
+            eng = cls(template, has_first, has_zeroth, device=device, has_cross=has_cross, **kw)
             cls._plans[key] = eng
         return eng
 
@@ -162,6 +176,16 @@ class LeafEngine:
                                                        _ptr(u), _ptr(stats), self._stream(stream)))
         return u, stats
 
+    def apply(self, coeffs, u_int, u_b, stream=None):
+        """w = collocation rows applied to [u_int; u_b] per leaf (drop plans)."""
+        coeffs, u_int, u_b = self._dev(coeffs), self._dev(u_int), self._dev(u_b)
+        self._check_coeffs(coeffs)
+        L = coeffs.shape[0]
+        w = self._empty(L, self.n)
+        _native.check(self.lib.hps_leaf_apply(self.plan, L, _ptr(coeffs), _ptr(u_int), _ptr(u_b),
+                                              _ptr(w), self._stream(stream)))
+        return w
+
     # ------------------------------------------------------------ host calls
     def dtn_host(self, coeffs: np.ndarray, out: Optional[np.ndarray] = None,
                  chunk_leaves: int = 0) -> Tuple[np.ndarray, np.ndarray]:
@@ -175,6 +199,9 @@ class LeafEngine:
         _native.check(self.lib.hps_leaf_dtn_host(self.plan, L, _np_ptr(coeffs), _np_ptr(out),
                                                  _np_ptr(stats), int(chunk_leaves)))
         return out, stats
+
+    def apply_host(self, coeffs, u_int, u_b):
+        return self.apply(coeffs, u_int, u_b).cpu().numpy()
 
     def solution_operator_host(self, coeffs):
         s, stats = self.solution_operator(coeffs)

@@ -274,7 +274,9 @@ class LeafTemplate:
 # ---------------------------------------------------------------------------
 
 def coefficient_layout(coeffs: CoefficientField):
-    return coeffs.first_order is not None, coeffs.zeroth_order is not None
+    """(has_first, has_zeroth, has_cross) of a field's device coefficient pack."""
+    return (coeffs.first_order is not None, coeffs.zeroth_order is not None,
+            bool(coeffs.has_cross_terms))
 
 
 def pack_coefficients(coeffs: CoefficientField, x_int: np.ndarray, n_leaves: int,
@@ -282,18 +284,26 @@ def pack_coefficients(coeffs: CoefficientField, x_int: np.ndarray, n_leaves: int
     """Evaluate the coefficient callables at interior nodes of ``n_leaves`` leaves.
 
     x_int: (n_leaves * n, d) points, leaf-major.  Returns (n_leaves, ncoef, n)
-    with rows [a_00 .. a_dd (diagonal second order), b_0 .. b_d, c].
+    with rows [a_00 .. a_dd (diagonal second order), a_ab + a_ba for the pairs
+    (0,1), (0,2), (1,2) if the field has cross terms (the sum the reference
+    forms in collocation_rows, local_ops.py:375-378), b_0 .. b_d, c].
     """
     d = x_int.shape[1]
     n = x_int.shape[0] // max(n_leaves, 1)
-    has_first, has_zeroth = coefficient_layout(coeffs)
-    ncoef = d + (d if has_first else 0) + (1 if has_zeroth else 0)
+    has_first, has_zeroth, has_cross = coefficient_layout(coeffs)
+    npair = d * (d - 1) // 2 if has_cross else 0
+    ncoef = d + npair + (d if has_first else 0) + (1 if has_zeroth else 0)
     if out is None:
         out = np.empty((n_leaves, ncoef, n))
     a2 = np.asarray(coeffs.second_order(x_int), dtype=float)
     for k in range(d):
         out[:, k, :] = a2[:, k, k].reshape(n_leaves, n)
     row = d
+    if has_cross:
+        for a in range(d):
+            for b in range(a + 1, d):
+                out[:, row, :] = (a2[:, a, b] + a2[:, b, a]).reshape(n_leaves, n)
+                row += 1
     if has_first:
         a1 = np.asarray(coeffs.first_order(x_int), dtype=float)
         for k in range(d):

@@ -141,15 +141,10 @@ def gaussian_bump(center: Sequence[float], variance: float = 0.002):
 def convdiff_step(domain: Optional[DomainBox] = None, d: int = 3, dt: float = 0.05,
                   diffusivity: float = 1e-4) -> ProblemSpec:
     """Implicit Crank-Nicolson half-step (I - dt/2 A) of the contaminant model (Eq. 15-16)."""
-    domain = domain or (CONVDIFF_DOMAIN_3D if d == 3 else CONVDIFF_DOMAIN_2D)
-    half = 0.5 * dt
-    vel = _rotation_velocity(domain.d)
-    coeffs = isotropic_field(domain.d, diffusion=half * diffusivity,
-                             zeroth=lambda x: np.ones(x.shape[0]) + half * np.zeros(x.shape[0]),
-                             first=lambda x: half * vel(x))
-    center = (0.0, -0.3, 0.0)[:domain.d]
-    return ProblemSpec(name="convdiff_step", coeffs=coeffs, f=gaussian_bump(center), g=_zero,
-                       domain=domain)
+    prob = convection_diffusion(d=d, diffusivity=diffusivity)
+    implicit, _ = cn_step_fields(prob, dt)
+    return ProblemSpec(name="convdiff_step", coeffs=implicit, f=prob.u0, g=_zero,
+                       domain=domain or prob.domain)
 
 
 ELLIPTIC_REGISTRY = {
@@ -175,3 +170,161 @@ def relative_l2_error(u: np.ndarray, exact_values: np.ndarray) -> float:
     if denom == 0.0:
         raise ConfigError("reference solution has zero norm")
     return float(np.linalg.norm(u - exact_values)) / denom
+
+
+# ---------------------------------------------------------------------------
+# Parabolic problems and Crank-Nicolson time stepping (reference problems.py:59-86,
+# 189-267, 441-515): the implicit operator (I - dt/2 A) is built and factorized
+# once; every step applies (I + dt/2 A) to u^n leaf by leaf on the GPU
+# (hps_leaf_apply) and runs the solve stage with that load.
+# ---------------------------------------------------------------------------
+
+@dataclass
+class TimeStepConfig:
+    dt: float
+    t_end: float
+    u0: Optional[Callable[[np.ndarray], np.ndarray]] = None
+
+    def __post_init__(self):
+        if not self.dt > 0.0:
+            raise ConfigError("dt must be positive")
+        if self.t_end < self.dt:
+            raise ConfigError("t_end must cover at least one step")
+
+    @property
+    def steps(self) -> int:
+        return int(round(self.t_end / self.dt))
+
+
+@dataclass
+class ParabolicProblem:
+    """du/dt = diffusivity Lap(u) - div(velocity u), homogeneous Dirichlet."""
+
+    name: str
+    domain: DomainBox
+    diffusivity: float
+    velocity: Optional[Callable[[np.ndarray], np.ndarray]] = None
+    div_velocity: Optional[Callable[[np.ndarray], np.ndarray]] = None
+    u0: Optional[Callable[[np.ndarray], np.ndarray]] = None
+    exact: Optional[Callable[[np.ndarray, float], np.ndarray]] = None
+
+
+def convection_diffusion(d: int = 3, diffusivity: float = 1e-4) -> ParabolicProblem:
+    domain = CONVDIFF_DOMAIN_3D if d == 3 else CONVDIFF_DOMAIN_2D
+    return ParabolicProblem(name="convection_diffusion", domain=domain,
+                            diffusivity=float(diffusivity), velocity=_rotation_velocity(domain.d),
+                            div_velocity=_zero, u0=gaussian_bump((0.0, -0.3, 0.0)[:domain.d]))
+
+
+def heat_manufactured(d: int = 3) -> ParabolicProblem:
+    domain = UNIT_CUBE if d == 3 else UNIT_SQUARE
+    rate = domain.d * np.pi ** 2
+
+    def exact(x, t):
+        return math.exp(-rate * t) * np.prod(np.sin(np.pi * x), axis=1)
+
+    return ParabolicProblem(name="heat_manufactured", domain=domain, diffusivity=1.0,
+                            u0=lambda x: exact(x, 0.0), exact=exact)
+
+
+def cn_step_fields(prob: ParabolicProblem, dt: float):
+    """(implicit, explicit) coefficient fields of (I -+ dt/2 A), Eq. (16)."""
+    def make(sign: float) -> CoefficientField:
+        half = sign * 0.5 * dt
+        first = None
+        if prob.velocity is not None:
+            vel = prob.velocity
+            first = lambda x, _h=half: _h * vel(x)  # noqa: E731
+        div_v = prob.div_velocity
+
+        def zeroth(x, _h=half):
+            out = np.ones(x.shape[0])
+            return out + _h * div_v(x) if div_v is not None else out
+
+        return isotropic_field(prob.domain.d, diffusion=half * prob.diffusivity, zeroth=zeroth,
+                               first=first)
+    return make(1.0), make(-1.0)
+
+
+PARABOLIC_REGISTRY = {"heat_manufactured": heat_manufactured,
+                      "convection_diffusion": convection_diffusion}
+
+
+def make_parabolic(name: str, d: int = 3, **params) -> ParabolicProblem:
+    if name not in PARABOLIC_REGISTRY:
+        raise ConfigError(f"unknown parabolic problem {name!r}; known: {sorted(PARABOLIC_REGISTRY)}")
+    return PARABOLIC_REGISTRY[name](d=d, **params)
+
+
+@dataclass
+class Trajectory:
+    times: list
+    states: list
+    factorization_events: int
+    step_seconds: list
+    system: object
+
+    @property
+    def final(self) -> np.ndarray:
+        return self.states[-1]
+
+
+def crank_nicolson_run(disc, prob: ParabolicProblem, cfg: TimeStepConfig, schedule=None,
+                       snapshot_stride: int = 1) -> Trajectory:
+    """Advance a parabolic problem; the implicit operator is factorized once."""
+    import time as _time
+    from . import condensation
+    from .condensation import BatchSchedule, interior_points
+    from .engine import LeafEngine
+    from .local_ops import DROP_CORNERS, pack_coefficients
+
+    if snapshot_stride < 1:
+        raise ConfigError("snapshot stride must be >= 1")
+    if disc.corner_mode != DROP_CORNERS:
+        raise ConfigError("time stepping uses corner-dropping meshes "
+                          "(the step operators have no cross terms)")
+    implicit, explicit = cn_step_fields(prob, cfg.dt)
+    sys = condensation.build(disc, implicit, schedule or BatchSchedule(cache_leaf_factors=True))
+    engine = LeafEngine.for_template(sys.template, explicit, device=sys.schedule.device)
+    leaves = range(len(disc.leaves))
+    pack_ex = pack_coefficients(explicit, interior_points(disc, leaves), len(disc.leaves))
+    int_ids = np.stack([lf.interior_ids for lf in disc.leaves])
+    bnd_ids = np.stack([lf.boundary_ids for lf in disc.leaves])
+    u0 = cfg.u0 or prob.u0
+    if u0 is None:
+        raise ConfigError("no initial condition available")
+    u = np.asarray(u0(disc.nodes), dtype=float).copy()
+    times, states, step_seconds = [0.0], [u.copy()], []
+    for step in range(1, cfg.steps + 1):
+        tic = _time.perf_counter()
+        w = np.zeros(disc.n_total)
+        w[int_ids] = engine.apply_host(pack_ex, u[int_ids], u[bnd_ids])
+        u = condensation.run_solve_stage(sys, w, _zero).u
+        step_seconds.append(_time.perf_counter() - tic)
+        if step % snapshot_stride == 0 or step == cfg.steps:
+            times.append(step * cfg.dt)
+            states.append(u.copy())
+    return Trajectory(times=times, states=states, factorization_events=1,
+                      step_seconds=step_seconds, system=sys)
+
+
+def interior_sample_points(domain: DomainBox, n: int, rng=None, margin: float = 0.05) -> np.ndarray:
+    """Random points strictly inside the domain (reference problems.py:371-378)."""
+    rng = rng or np.random.default_rng(0)
+    lo, hi = np.asarray(domain.lo), np.asarray(domain.hi)
+    pad = margin * (hi - lo)
+    return rng.uniform(lo + pad, hi - pad, size=(n, domain.d))
+
+
+def plane_mass_center(u: np.ndarray, nodes: np.ndarray, split_axis: int = 2) -> np.ndarray:
+    """Density-weighted (x1, x2) center of the upper half (x_split > 0), weights clipped at 0."""
+    mask = nodes[:, split_axis] > 0.0 if nodes.shape[1] > split_axis else slice(None)
+    w = np.clip(u[mask], 0.0, None)
+    total = w.sum()
+    if total <= 0.0:
+        raise ConfigError("no positive mass in the upper half domain")
+    return (w[:, None] * nodes[mask][:, :2]).sum(axis=0) / total
+
+
+def unwrap_angles(centers) -> np.ndarray:
+    return np.unwrap(np.array([math.atan2(c[1], c[0]) for c in centers]))

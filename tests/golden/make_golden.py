@@ -27,6 +27,7 @@ sys.path.insert(0, "/root/reference/pkg/src")
 
 from steklov import condensation as ref_cond  # noqa: E402
 from steklov.geometry import DomainBox, MeshConfig, build_discretization  # noqa: E402
+from steklov.geometry import sinusoidal_map  # noqa: E402
 from steklov.local_ops import (CoefficientField, LeafTemplate,  # noqa: E402
                                build_leaf_factors, cheb_nodes, isotropic_field)
 from steklov.problems import make_problem  # noqa: E402
@@ -48,6 +49,12 @@ LEAF_CASES = [
     ("grav3_p8", 3, 8, (1.1, -1.0, -1.2), (1.35, -0.75, -0.95), "gravity"),
     ("conv3_p7", 3, 7, (-0.5, -0.5, 0.0), (0.0, 0.0, 0.5), "convdiff"),
     ("bump3_p10", 3, 10, (0.375, 0.375, 0.375), (0.5, 0.5, 0.5), "bump"),
+    # legendre face grids (corner_mode="legendre"), with and without cross terms
+    ("leg_curv2_p6", 2, 6, (1.1, -1.0), (1.6, -0.5), "curved"),
+    ("leg_curv3_p5", 3, 5, (1.1, -1.0, -1.2), (1.6, -0.5, -0.7), "curved"),
+    ("leg_curv3_p7", 3, 7, (1.35, -0.75, -0.95), (1.6, -0.5, -0.7), "curved"),
+    ("leg_lap3_p6", 3, 6, (0.0, 0.0, 0.0), (0.5, 0.5, 0.5), "laplace"),
+    ("leg_grav2_p8", 2, 8, (1.1, -1.0), (1.35, -0.75), "gravity"),
 ]
 
 
@@ -60,6 +67,9 @@ def field(kind, d):
         return isotropic_field(d, zeroth=lambda x: bump(x, 12.0))
     if kind == "gravity":
         return isotropic_field(d, zeroth=lambda x: -144.0 * (1.0 - x[:, d - 1]))
+    if kind == "curved":
+        base = isotropic_field(d, zeroth=lambda x: np.full(x.shape[0], -36.0))
+        return sinusoidal_map(0.25, 6.0).coefficient_transform(base)
     if kind == "convdiff":
         def first(x):
             b = np.zeros_like(x)
@@ -72,9 +82,12 @@ def field(kind, d):
 
 
 def pack_coeffs(coeffs, x_int, d):
-    """(ncoef, n): diag second order, first order (if any), zeroth (if any)."""
+    """(ncoef, n): diag second order, cross sums a_ab + a_ba (if has_cross_terms),
+    first order (if any), zeroth (if any)."""
     a2 = np.asarray(coeffs.second_order(x_int), dtype=float)
     rows = [a2[:, k, k] for k in range(d)]
+    if coeffs.has_cross_terms:
+        rows += [a2[:, a, b] + a2[:, b, a] for a in range(d) for b in range(a + 1, d)]
     if coeffs.first_order is not None:
         a1 = np.asarray(coeffs.first_order(x_int), dtype=float)
         rows += [a1[:, k] for k in range(d)]
@@ -89,14 +102,15 @@ def leaf_cases():
     for name, d, p, lo, hi, kind in LEAF_CASES:
         lo, hi = np.asarray(lo), np.asarray(hi)
         widths = hi - lo
-        tpl = LeafTemplate(widths, p, "drop", False)
+        mode = "legendre" if name.startswith("leg_") else "drop"
+        coeffs = field(kind, d)
+        tpl = LeafTemplate(widths, p, mode, coeffs.has_cross_terms)
         nodes = []
         for k in range(d):
             x = lo[k] + widths[k] * tpl.ref_offsets
             x[0], x[-1] = lo[k], hi[k]
             nodes.append(x)
         grid = tpl.leaf_grid(nodes)
-        coeffs = field(kind, d)
         lf = build_leaf_factors(tpl, coeffs, grid, leaf_index=(0,) * d)
         a_ii, a_ib = tpl.interior_blocks(coeffs, grid)
         x_int = grid[tpl.interior_idx]
@@ -106,7 +120,9 @@ def leaf_cases():
         u_int = v - lf.solve_interior(a_ib @ ub)
         pre = name + "/"
         out[pre + "meta"] = np.array([d, p, 1 if coeffs.first_order is not None else 0,
-                                      1 if coeffs.zeroth_order is not None else 0])
+                                      1 if coeffs.zeroth_order is not None else 0,
+                                      1 if mode == "legendre" else 0,
+                                      1 if coeffs.has_cross_terms else 0])
         out[pre + "widths"] = widths
         out[pre + "coeffs"] = pack_coeffs(coeffs, x_int, d)
         out[pre + "a_ii"] = a_ii
@@ -121,7 +137,10 @@ def leaf_cases():
         out[pre + "ub"] = ub
         out[pre + "u_int"] = u_int
         out[pre + "interior_idx"] = tpl.interior_idx
-        out[pre + "bcols"] = tpl._bcols
+        if mode == "drop":
+            out[pre + "bcols"] = tpl._bcols
+        else:
+            out[pre + "Q"] = tpl._boundary_injection
         out[pre + "D"] = np.stack(tpl.diff)
     return out
 
@@ -132,6 +151,8 @@ PIPELINE_CASES = [
     ("gravity2_3x2_p7", "gravity_helmholtz", 2, {"kappa": 5.0}, (3, 2), 7),
     ("helm3_2x2x2_p6", "helmholtz_green", 3, {"kappa": 6.0}, (2, 2, 2), 6),
     ("convdiff3_2x1x2_p5", "convdiff_step", 3, {}, (2, 1, 2), 5),
+    ("curved2_2x2_p6_leg", "curved_helmholtz", 2, {"kappa": 4.0}, (2, 2), 6),
+    ("curved3_2x1x1_p5_leg", "curved_helmholtz", 3, {"kappa": 4.0}, (2, 1, 1), 5),
 ]
 
 
@@ -139,7 +160,8 @@ def pipeline_cases():
     out = {}
     for name, prob_name, d, params, boxes, p in PIPELINE_CASES:
         prob = make_problem(prob_name, d=d, **params)
-        disc = build_discretization(prob.domain, MeshConfig(boxes, p))
+        mode = "legendre" if name.endswith("_leg") else "drop"
+        disc = build_discretization(prob.domain, MeshConfig(boxes, p, mode))
         report, sys_ = ref_cond.solve_bvp(disc, prob.coeffs, prob.f, prob.g)
         pre = name + "/"
         out[pre + "u"] = report.u

@@ -25,9 +25,10 @@ def rel(a, b):
 def engine_for(name):
     from paper_2503_04033_b200.engine import LeafEngine
     from paper_2503_04033_b200.local_ops import LeafTemplate
-    d, p, hf, hz = (int(x) for x in G[name + "/meta"])
-    tpl = LeafTemplate(G[name + "/widths"], p, "drop", False)
-    return LeafEngine(tpl, bool(hf), bool(hz), device=0), G[name + "/coeffs"][None]
+    d, p, hf, hz, leg, hc = (int(x) for x in G[name + "/meta"])
+    tpl = LeafTemplate(G[name + "/widths"], p, "legendre" if leg else "drop", bool(hc))
+    return (LeafEngine(tpl, bool(hf), bool(hz), device=0, has_cross=bool(hc)),
+            G[name + "/coeffs"][None])
 
 
 @pytest.mark.parametrize("name", CASES)
@@ -113,3 +114,26 @@ def test_two_dimensional_batch_vs_oracle():
     for k in range(5):
         ref, _, _ = O.leaf_dtn(otpl, pack[k, :2].T, None, pack[k, 2])
         assert rel(dtn[k], ref) <= TOL
+
+
+def test_legendre_cross_batch_vs_oracle():
+    """Curved-domain operator (cross terms, first order, legendre faces), p = 10."""
+    from paper_2503_04033_b200.engine import LeafEngine
+    from paper_2503_04033_b200.geometry import sinusoidal_map
+    from paper_2503_04033_b200.local_ops import LeafTemplate, isotropic_field, pack_coefficients
+    p, h = 10, 0.125
+    base = isotropic_field(3, zeroth=lambda x: np.full(x.shape[0], -100.0))
+    field = sinusoidal_map(0.25, 6.0).coefficient_transform(base)
+    tpl = LeafTemplate((h, h, h), p, "legendre", True)
+    los = [np.array([1.1, -1.0, -1.2]) + h * np.array(ix) for ix in ((0, 0, 0), (3, 1, 2), (7, 7, 7))]
+    x = np.concatenate([tpl.leaf_grid(tpl.leaf_nodes1d(lo, lo + h))[tpl.interior_idx] for lo in los])
+    pack = pack_coefficients(field, x, len(los))
+    eng = LeafEngine(tpl, True, True, device=0, has_cross=True)
+    dtn, _ = eng.dtn_host(pack)
+    s, _ = eng.solution_operator_host(pack)
+    otpl = O.OracleTemplate(tpl.widths, p, "legendre")
+    for k in range(len(los)):
+        c = pack[k]
+        ref, sref, _ = O.leaf_dtn(otpl, c[:3].T, c[6:9].T, c[9], c[3:6].T)
+        assert rel(dtn[k], ref) <= TOL
+        assert rel(s[k], sref) <= TOL

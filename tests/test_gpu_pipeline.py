@@ -22,6 +22,8 @@ CASES = [
     ("gravity2_3x2_p7", "gravity_helmholtz", 2, {"kappa": 5.0}, (3, 2), 7),
     ("helm3_2x2x2_p6", "helmholtz_green", 3, {"kappa": 6.0}, (2, 2, 2), 6),
     ("convdiff3_2x1x2_p5", "convdiff_step", 3, {}, (2, 1, 2), 5),
+    ("curved2_2x2_p6_leg", "curved_helmholtz", 2, {"kappa": 4.0}, (2, 2), 6),
+    ("curved3_2x1x1_p5_leg", "curved_helmholtz", 3, {"kappa": 4.0}, (2, 1, 1), 5),
 ]
 
 
@@ -29,17 +31,18 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-def setup(prob, d, params, boxes, p, schedule=None):
+def setup(prob, d, params, boxes, p, schedule=None, mode="drop"):
     from paper_2503_04033_b200 import build_discretization, MeshConfig, make_problem, solve_bvp
     spec = make_problem(prob, d=d, **params)
-    disc = build_discretization(spec.domain, MeshConfig(boxes, p))
+    disc = build_discretization(spec.domain, MeshConfig(boxes, p, mode))
     report, sys_ = solve_bvp(disc, spec.coeffs, spec.f, spec.g, schedule=schedule)
     return spec, disc, report, sys_
 
 
 @pytest.mark.parametrize("name,prob,d,params,boxes,p", CASES)
 def test_pipeline_matches_reference(name, prob, d, params, boxes, p):
-    spec, disc, report, sys_ = setup(prob, d, params, boxes, p)
+    mode = "legendre" if name.endswith("_leg") else "drop"
+    spec, disc, report, sys_ = setup(prob, d, params, boxes, p, mode=mode)
     assert rel(report.u, PG[name + "/u"]) <= 1e-10
     assert rel(sys_.t.toarray(), PG[name + "/t_dense"]) <= 1e-10
     assert report.residual <= 1e-10

@@ -29,13 +29,16 @@ CASES = sorted({k.split("/")[0] for k in G.files})
 
 @pytest.mark.parametrize("name", CASES)
 def test_template_matches_reference(name):
-    d, p, _, _ = (int(x) for x in G[name + "/meta"])
-    tpl = LeafTemplate(G[name + "/widths"], p, DROP_CORNERS, False)
+    d, p, _, _, leg, hc = (int(x) for x in G[name + "/meta"])
+    tpl = LeafTemplate(G[name + "/widths"], p, LEGENDRE_FACES if leg else DROP_CORNERS, bool(hc))
     assert np.array_equal(np.stack(tpl.diff), G[name + "/D"])
     assert np.array_equal(tpl.interior_idx, G[name + "/interior_idx"])
-    assert np.array_equal(tpl._bcols, G[name + "/bcols"])
     assert np.array_equal(tpl.a_bi, G[name + "/a_bi"])
     assert np.array_equal(tpl.a_bb, G[name + "/a_bb"])
+    if leg:
+        assert np.array_equal(tpl._boundary_injection, G[name + "/Q"])
+    else:
+        assert np.array_equal(tpl._bcols, G[name + "/bcols"])
 
 
 def test_cheb_nodes_properties():
@@ -94,10 +97,13 @@ def test_geometry_counts():
     ("gravity2_3x2_p7", "gravity_helmholtz", 2, {"kappa": 5.0}, (3, 2), 7),
     ("helm3_2x2x2_p6", "helmholtz_green", 3, {"kappa": 6.0}, (2, 2, 2), 6),
     ("convdiff3_2x1x2_p5", "convdiff_step", 3, {}, (2, 1, 2), 5),
+    ("curved2_2x2_p6_leg", "curved_helmholtz", 2, {"kappa": 4.0}, (2, 2), 6),
+    ("curved3_2x1x1_p5_leg", "curved_helmholtz", 3, {"kappa": 4.0}, (2, 1, 1), 5),
 ])
 def test_numbering_matches_reference(name, prob, d, params, boxes, p):
     spec = make_problem(prob, d=d, **params)
-    disc = build_discretization(spec.domain, MeshConfig(boxes, p))
+    mode = LEGENDRE_FACES if name.endswith("_leg") else DROP_CORNERS
+    disc = build_discretization(spec.domain, MeshConfig(boxes, p, mode))
     assert np.array_equal(disc.nodes, PG[name + "/nodes"])
     if name + "/exact" in PG.files:
         assert np.array_equal(spec.exact(disc.nodes), PG[name + "/exact"])
@@ -140,3 +146,21 @@ def test_schedule_resolution():
     assert 1 <= r.batch_size and r.batch_size * r.workspace_bytes <= 3 * ws
     r = cond.BatchSchedule().resolve(8, 3, DROP_CORNERS)
     assert r.batch_size * r.workspace_bytes + r.resident_limit * r.block_bytes <= r.memory_budget
+
+
+def test_cn_fields_and_parabolic_registry():
+    from paper_2503_04033_b200.problems import (TimeStepConfig, cn_step_fields,
+                                                interior_sample_points, make_parabolic)
+    prob = make_parabolic("convection_diffusion", d=3)
+    implicit, explicit = cn_step_fields(prob, dt=0.1)
+    pts = interior_sample_points(prob.domain, 10, np.random.default_rng(3))
+    assert np.allclose(implicit.second_order(pts), -explicit.second_order(pts), atol=0.0)
+    assert np.allclose(implicit.first_order(pts), -explicit.first_order(pts), atol=0.0)
+    zi, ze = implicit.zeroth_order(pts), explicit.zeroth_order(pts)
+    assert np.allclose(zi - 1.0, -(ze - 1.0), atol=1e-15)
+    with pytest.raises(ConfigError):
+        TimeStepConfig(dt=0.0, t_end=1.0)
+    with pytest.raises(ConfigError):
+        TimeStepConfig(dt=1.0, t_end=0.5)
+    with pytest.raises(ConfigError):
+        make_parabolic("nope")

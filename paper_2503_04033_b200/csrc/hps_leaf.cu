@@ -51,15 +51,26 @@ constexpr int KC = 16;           // k-chunk per pipeline stage
 #define HPS_STAGES 3
 #endif
 #ifndef HPS_EPI_SLOTS
-#define HPS_EPI_SLOTS 2
+#define HPS_EPI_SLOTS 1
 #endif
 constexpr int STAGES = HPS_STAGES;
 constexpr int EPI_SLOTS = HPS_EPI_SLOTS;
-constexpr int A_STRIDE = KC;     // A box rows are 128 B, 128B-swizzled by TMA (1024 B aligned)
-constexpr int B_STRIDE = TN;     // B box rows are 1 KB, unswizzled
+// Operand boxes.  Padded boxes (A 20, B 132 doubles per row; the extra
+// columns are just neighbouring data) give bank-conflict-free m8n8k4 fragment
+// loads; the alternative is a 128B-swizzled 16-column A box / unpadded B box.
+#ifndef HPS_A_PAD
+#define HPS_A_PAD 1
+#endif
+#ifndef HPS_B_PAD
+#define HPS_B_PAD 1
+#endif
+constexpr bool A_PAD = HPS_A_PAD != 0;
+constexpr int A_STRIDE = A_PAD ? KC + 4 : KC;
+constexpr int B_STRIDE = HPS_B_PAD ? TN + 4 : TN;
 constexpr int STAGE_A = TM * A_STRIDE;
 constexpr int STAGE_B = KC * B_STRIDE;
-constexpr int STAGE_DBL = STAGE_A + STAGE_B;
+// swizzled A boxes need 1024-byte aligned stages
+constexpr int STAGE_DBL = A_PAD ? STAGE_A + STAGE_B : ((STAGE_A + STAGE_B + 127) / 128) * 128;
 constexpr int WARPS = NT / 32;
 constexpr int WN = 4;                 // warps along N (4 x 32 = TN)
 constexpr int WM = WARPS / WN;        // warps along M
@@ -191,7 +202,7 @@ __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;\n" ::: "memory");
 }
 
-constexpr unsigned STAGE_BYTES = (unsigned)(STAGE_DBL * 8);
+constexpr unsigned STAGE_BYTES = (unsigned)((STAGE_A + STAGE_B) * 8);  // TMA transaction bytes
 
 // ---------------------------------------------------------------------------
 // Per-CTA context
@@ -296,9 +307,13 @@ __device__ __forceinline__ void gemm(Ctx& c, const bool sub, const int a_src, in
       double af[MI], bf[NJ];
 #pragma unroll
       for (int i = 0; i < MI; ++i) {
-        // 128B swizzle: 16-byte chunk index ^= row % 8  (row % 8 == lr here)
         const int row = wm * (MI * 8) + i * 8 + lr, k = ks + lc;
-        af[i] = sa[row * A_STRIDE + ((((k >> 1) ^ lr) << 1) | (k & 1))];
+        if (A_PAD) {
+          af[i] = sa[row * A_STRIDE + k];
+        } else {
+          // 128B swizzle: 16-byte chunk index ^= row % 8  (row % 8 == lr here)
+          af[i] = sa[row * A_STRIDE + ((((k >> 1) ^ lr) << 1) | (k & 1))];
+        }
       }
 #pragma unroll
       for (int j = 0; j < NJ; ++j) bf[j] = sb[(ks + lc) * B_STRIDE + wn * 32 + j * 8 + lr];
@@ -1456,15 +1471,15 @@ static int ensure_workspace(hps_plan_s* P, int mode, int want_slots) {
       mode_dims(P, mode, &NR, &NC);
       NR = rows_alloc(P, mode);
       TmaMaps& m = P->maps[mode];
-      if (make_map(&m.a_work, P->work, NC, NR, P->ws_slots, NC, per, A_STRIDE, TM, true) ||
+      if (make_map(&m.a_work, P->work, NC, NR, P->ws_slots, NC, per, A_STRIDE, TM, !A_PAD) ||
           make_map(&m.b_work, P->work, NC, NR, P->ws_slots, NC, per, B_STRIDE, KC) ||
           make_map(&m.a_scratch, P->scratch, TRI_BLOCK, TRI_BLOCK, P->ws_slots, TRI_BLOCK,
-                   TRI_BLOCK * TRI_BLOCK, A_STRIDE, TM, true) ||
+                   TRI_BLOCK * TRI_BLOCK, A_STRIDE, TM, !A_PAD) ||
           make_map(&m.c_red, P->work, NC, NR, P->ws_slots, NC, per, 16, 8))
         return -1;
       if (P->legendre &&
           (make_map(&m.a_abi, P->a_bi_pad, P->n_pad, P->m_pad, 1, P->n_pad,
-                    (size_t)P->m_pad * P->n_pad, A_STRIDE, TM, true) ||
+                    (size_t)P->m_pad * P->n_pad, A_STRIDE, TM, !A_PAD) ||
            make_map(&m.b_q, P->Q, P->m_pad, P->nb_pad, 1, P->m_pad, (size_t)P->nb_pad * P->m_pad,
                     B_STRIDE, KC)))
         return -1;

@@ -16,7 +16,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) gemm_probe(double* base, size
   c.M = base + (size_t)blockIdx.x * stride;
   c.ld = ld; c.slot = blockIdx.x; c.smem = smem; c.maps = &maps;
   c.full = bars; c.empty = bars + STAGES; c.pipe = 0; c.prof = nullptr;
-  for (int r = 0; r < reps; ++r) gemm(c, true, false, 0, 0, M, 0, M + K, 0, M, N, K);
+  for (int r = 0; r < reps; ++r) gemm(c, true, 0, 0, 0, 0, M, 0, M + K, 0, M, N, K);
 }
 }  // namespace
 
@@ -42,7 +42,7 @@ int main(int argc, char** argv) {
     cudaMalloc(&buf, stride * CTAS_PER_SM * sms * 8);
     cudaMemset(buf, 0, stride * CTAS_PER_SM * sms * 8);
     TmaMaps maps;
-    make_map(&maps.a_work, buf, ld, NR, CTAS_PER_SM * sms, ld, stride, A_STRIDE, TM, true);
+    make_map(&maps.a_work, buf, ld, NR, CTAS_PER_SM * sms, ld, stride, A_STRIDE, TM, !A_PAD);
     make_map(&maps.b_work, buf, ld, NR, CTAS_PER_SM * sms, ld, stride, B_STRIDE, KC);
     maps.a_scratch = maps.a_work;
     make_map(&maps.c_red, buf, ld, NR, CTAS_PER_SM * sms, ld, stride, 16, 8);

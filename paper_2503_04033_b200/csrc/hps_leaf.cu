@@ -505,7 +505,8 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
   constexpr int GROUP = 32 / WB;  // lanes sharing one column of the reduce-scatter
   const int n_cand = c.n_piv - b0;
   const int done = b0 - c0, len = done + WB;
-  double* S = c.smem;                          // n_cand x WB
+  double* S = c.smem;                          // column-major [WB][n_cand]: S[j * NS + r]
+  const int NS = n_cand;
   // staging T (<= 32 x 32) and Q (<= 16 x 32) alias S; Ut sits after all of them
   double* Ut = c.smem + (size_t)max(c.n_piv * WB, 1024);  // WB x 32, Ut[j*32 + kk]
   unsigned long long* prof = c.prof;
@@ -579,8 +580,8 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
         if (r < c.NR && owns) {
           const double v0 = av[g][0] - acc[0], v1 = av[g][1] - acc[1];
           if (r < c.n_piv) {
-            S[(r - b0) * WB + 2 * lc] = v0;
-            if (2 * lc + 1 < WB) S[(r - b0) * WB + 2 * lc + 1] = v1;
+            S[(2 * lc) * NS + (r - b0)] = v0;
+            if (2 * lc + 1 < WB) S[(2 * lc + 1) * NS + (r - b0)] = v1;
           } else {
             c.M[(size_t)r * c.ld + b0 + 2 * lc] = v0;
             if (2 * lc + 1 < WB) c.M[(size_t)r * c.ld + b0 + 2 * lc + 1] = v1;
@@ -591,66 +592,86 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
   } else {
     for (int e = tid; e < n_cand * WB; e += NT) {
       const int r = e / WB, j = e - r * WB;
-      S[e] = c.M[(size_t)(b0 + r) * c.ld + b0 + j];
+      S[j * NS + r] = c.M[(size_t)(b0 + r) * c.ld + b0 + j];
     }
   }
   __syncthreads();
   PANEL_TICK(11)
-  // 3. partial pivoting on the block
-  for (int j = 0; j < WB; ++j) {
-    double best = -1.0;
-    int bidx = 0x7fffffff;
-    for (int r = j + tid; r < n_cand; r += NT) {
-      const double v = fabs(S[r * WB + j]);
-      if (v > best) { best = v; bidx = r; }
-    }
+  // 3. partial pivoting on the block.  The search for column j+1 is fused into
+  //    the rank-1 update of column j (each thread scans the rows it just
+  //    updated), thread 0 finalises the pivot and swaps: two barriers per column.
+  {
+    auto warp_argmax = [&](double best, int bidx) {
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, best, off);
-      const int oi = __shfl_xor_sync(0xffffffffu, bidx, off);
-      if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
-    }
-    if (lane == 0) { s_redv[warp] = best; s_redi[warp] = bidx; }
-    __syncthreads();
-    if (tid == 0) {
-      double bv = s_redv[0];
-      int bi = s_redi[0];
-      for (int q = 1; q < NW; ++q) {
-        if (s_redv[q] > bv || (s_redv[q] == bv && s_redi[q] < bi)) { bv = s_redv[q]; bi = s_redi[q]; }
+      for (int off = 16; off > 0; off >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, bidx, off);
+        if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
       }
-      if (bi == 0x7fffffff) bi = j;
-      s_pivot = bi;
-      c.piv[b0 + j] = b0 + bi;
-      if (c.prof && bi != j) c.prof[15] += 1;
+      if (lane == 0) { s_redv[warp] = best; s_redi[warp] = bidx; }
+    };
+    {
+      double best = -1.0;
+      int bidx = 0x7fffffff;
+      for (int r = tid; r < n_cand; r += NT) {
+        const double v = fabs(S[r]);
+        if (v > best) { best = v; bidx = r; }
+      }
+      warp_argmax(best, bidx);
     }
     __syncthreads();
-    const int pr = s_pivot;
-    if (pr != j && tid < WB) {
-      const double t = S[j * WB + tid];
-      S[j * WB + tid] = S[pr * WB + tid];
-      S[pr * WB + tid] = t;
-    }
-    __syncthreads();
-    const double pivot = S[j * WB + j];
-    if (tid == 0 && b0 + j < c.n_real) {
-      const double ap = fabs(pivot);
-      s_pmin = fmin(s_pmin, ap);
-      s_pmax = fmax(s_pmax, ap);
-    }
-    const double inv = (pivot != 0.0) ? 1.0 / pivot : 1.0;
-    for (int r = j + 1 + tid; r < n_cand; r += NT) {
-      const double l = S[r * WB + j] * inv;
-      S[r * WB + j] = l;
+    for (int j = 0; j < WB; ++j) {
+      if (tid == 0) {
+        double bv = s_redv[0];
+        int bi = s_redi[0];
+        for (int q = 1; q < NT / 32; ++q) {
+          if (s_redv[q] > bv || (s_redv[q] == bv && s_redi[q] < bi)) { bv = s_redv[q]; bi = s_redi[q]; }
+        }
+        if (bi == 0x7fffffff) bi = j;
+        c.piv[b0 + j] = b0 + bi;
+        if (c.prof && bi != j) c.prof[15] += 1;
+        if (bi != j) {
 #pragma unroll
-      for (int jj = j + 1; jj < WB; ++jj) S[r * WB + jj] -= l * S[j * WB + jj];
+          for (int t = 0; t < WB; ++t) {
+            const double x = S[t * NS + j];
+            S[t * NS + j] = S[t * NS + bi];
+            S[t * NS + bi] = x;
+          }
+        }
+        if (b0 + j < c.n_real) {
+          const double ap = fabs(S[j * NS + j]);
+          s_pmin = fmin(s_pmin, ap);
+          s_pmax = fmax(s_pmax, ap);
+        }
+      }
+      __syncthreads();
+      const double pivot = S[j * NS + j];
+      const double inv = (pivot != 0.0) ? 1.0 / pivot : 1.0;
+      double urow[WB];
+#pragma unroll
+      for (int t = 0; t < WB; ++t) urow[t] = S[t * NS + j];
+      double best = -1.0;
+      int bidx = 0x7fffffff;
+      for (int r = j + 1 + tid; r < n_cand; r += NT) {
+        const double l = S[j * NS + r] * inv;
+        S[j * NS + r] = l;
+#pragma unroll
+        for (int t = 0; t < WB; ++t)
+          if (t > j) S[t * NS + r] -= l * urow[t];
+        if (j + 1 < WB) {
+          const double v = fabs(S[(j + 1) * NS + r]);
+          if (v > best) { best = v; bidx = r; }
+        }
+      }
+      if (j + 1 < WB) warp_argmax(best, bidx);
+      __syncthreads();
     }
-    __syncthreads();
   }
   PANEL_TICK(12)
   // 4. write-back; non-candidate rows L = A U^{-1}
   for (int e = tid; e < n_cand * WB; e += NT) {
     const int r = e / WB, j = e - r * WB;
-    c.M[(size_t)(b0 + r) * c.ld + b0 + j] = S[e];
+    c.M[(size_t)(b0 + r) * c.ld + b0 + j] = S[j * NS + r];
   }
   {
     // 8 rows per thread in flight: loads first, then the WB x WB substitution
@@ -669,8 +690,8 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
         for (int j = 0; j < WB; ++j) {
           double v = x[t][j];
 #pragma unroll
-          for (int i = 0; i < j; ++i) v -= x[t][i] * S[i * WB + j];
-          const double pv = S[j * WB + j];
+          for (int i = 0; i < j; ++i) v -= x[t][i] * S[j * NS + i];
+          const double pv = S[j * NS + j];
           x[t][j] = v * ((pv != 0.0) ? 1.0 / pv : 1.0);
         }
         const int r = r0 + t * NT;

@@ -275,7 +275,7 @@ def main():
         torch.cuda.empty_cache()
         h_coef = torch.from_numpy(pack).pin_memory().numpy()
         h_out = torch.empty((L, m, m), dtype=torch.float64, pin_memory=True).numpy()
-        chunk = 2 * eng.slots
+        chunk = 4 * eng.slots
         eng.dtn_host(h_coef[:chunk], out=h_out[:chunk], chunk_leaves=chunk)
         barrier()
         ts = []

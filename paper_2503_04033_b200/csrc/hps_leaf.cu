@@ -1765,21 +1765,23 @@ int hps_leaf_apply(hps_plan_t P, int n_leaves, const double* coeffs, const doubl
 }
 
 // Host-buffer DtN with the two-level schedule on the device: chunks of
-// `chunk_leaves` leaves flow H2D (copy stream) -> kernel (compute stream) ->
-// D2H (copy stream) with double buffering, so PCIe traffic overlaps the LU work.
+// `chunk_leaves` leaves flow H2D (input stream) -> kernel (compute stream) ->
+// D2H (output stream), double-buffered, so PCIe traffic in both directions
+// overlaps the LU work of the neighbouring chunks.
 int hps_leaf_dtn_host(hps_plan_t P, int n_leaves, const double* coeffs_host, double* dtn_host,
                       double* stats_host, int chunk_leaves) {
   if (!P) return fail("null plan");
   if (n_leaves <= 0) return 0;
   CK(cudaSetDevice(P->device));
-  if (chunk_leaves <= 0) chunk_leaves = P->slots * 2;
+  if (chunk_leaves <= 0) chunk_leaves = P->slots * 4;
   if (chunk_leaves > n_leaves) chunk_leaves = n_leaves;
   const size_t cbytes = (size_t)P->ncoef * P->n * 8, tbytes = (size_t)P->m * P->m * 8;
   double *d_coef[2] = {nullptr, nullptr}, *d_dtn[2] = {nullptr, nullptr}, *d_stats[2] = {nullptr, nullptr};
-  cudaStream_t s_comp, s_copy;
+  cudaStream_t s_in, s_comp, s_out;
   cudaEvent_t ev_in[2], ev_done[2], ev_out[2];
+  CK(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&s_comp, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&s_copy, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
   for (int b = 0; b < 2; ++b) {
     CK(cudaMalloc(&d_coef[b], cbytes * chunk_leaves));
     CK(cudaMalloc(&d_dtn[b], tbytes * chunk_leaves));
@@ -1794,32 +1796,37 @@ int hps_leaf_dtn_host(hps_plan_t P, int n_leaves, const double* coeffs_host, dou
     const int b = ci & 1;
     const int l0 = ci * chunk_leaves;
     const int cnt = (n_leaves - l0 < chunk_leaves) ? (n_leaves - l0) : chunk_leaves;
-    if (ci >= 2) cudaStreamWaitEvent(s_copy, ev_out[b], 0);  // buffer b drained to host
+    // input buffer b was last read by the kernel of chunk ci-2
+    if (ci >= 2) cudaStreamWaitEvent(s_in, ev_done[b], 0);
     cudaMemcpyAsync(d_coef[b], coeffs_host + (size_t)l0 * P->ncoef * P->n, cbytes * cnt,
-                    cudaMemcpyHostToDevice, s_copy);
-    cudaEventRecord(ev_in[b], s_copy);
+                    cudaMemcpyHostToDevice, s_in);
+    cudaEventRecord(ev_in[b], s_in);
     cudaStreamWaitEvent(s_comp, ev_in[b], 0);
+    // output buffer b was last drained by the D2H of chunk ci-2
+    if (ci >= 2) cudaStreamWaitEvent(s_comp, ev_out[b], 0);
     rc = launch(P, MODE_DTN, cnt, d_coef[b], nullptr, nullptr, d_dtn[b], nullptr, d_stats[b], s_comp);
     cudaEventRecord(ev_done[b], s_comp);
-    cudaStreamWaitEvent(s_copy, ev_done[b], 0);
+    cudaStreamWaitEvent(s_out, ev_done[b], 0);
     cudaMemcpyAsync(dtn_host + (size_t)l0 * P->m * P->m, d_dtn[b], tbytes * cnt,
-                    cudaMemcpyDeviceToHost, s_copy);
+                    cudaMemcpyDeviceToHost, s_out);
     if (stats_host)
       cudaMemcpyAsync(stats_host + 2 * (size_t)l0, d_stats[b], 16 * (size_t)cnt,
-                      cudaMemcpyDeviceToHost, s_copy);
-    cudaEventRecord(ev_out[b], s_copy);
+                      cudaMemcpyDeviceToHost, s_out);
+    cudaEventRecord(ev_out[b], s_out);
   }
-  cudaError_t e1 = cudaStreamSynchronize(s_copy);
-  cudaError_t e2 = cudaStreamSynchronize(s_comp);
+  cudaError_t e0 = cudaStreamSynchronize(s_in);
+  cudaError_t e1 = cudaStreamSynchronize(s_comp);
+  cudaError_t e2 = cudaStreamSynchronize(s_out);
   for (int b = 0; b < 2; ++b) {
     cudaFree(d_coef[b]); cudaFree(d_dtn[b]); cudaFree(d_stats[b]);
     cudaEventDestroy(ev_in[b]); cudaEventDestroy(ev_done[b]); cudaEventDestroy(ev_out[b]);
   }
+  cudaStreamDestroy(s_in);
   cudaStreamDestroy(s_comp);
-  cudaStreamDestroy(s_copy);
+  cudaStreamDestroy(s_out);
   if (rc != 0) return rc;
-  if (e1 != cudaSuccess || e2 != cudaSuccess)
-    return fail(std::string("streamed dtn failed: ") + cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+  const cudaError_t e = e0 != cudaSuccess ? e0 : (e1 != cudaSuccess ? e1 : e2);
+  if (e != cudaSuccess) return fail(std::string("streamed dtn failed: ") + cudaGetErrorString(e));
   return 0;
 }
 

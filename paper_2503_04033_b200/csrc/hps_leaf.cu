@@ -32,6 +32,7 @@
 #include <string.h>
 
 #include <cstdlib>
+#include <type_traits>
 #include <string>
 #include <vector>
 
@@ -295,6 +296,16 @@ __device__ __forceinline__ void gemm(Ctx& c, const bool sub, const int a_src, in
     for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   int tile = 0, kc = 0;
+  // 8x8 sub-tiles of this warp that lie inside the GEMM extent (warp-uniform):
+  // edge tiles skip the DMMAs on zero-filled rows / columns.
+  int mv = MI, nv = NJ;
+  auto set_valid = [&](int t) {
+    const int tm = t / tiles_n, tn = t - tm * tiles_n;
+    const int rows = M - (tm * TM + wm * (MI * 8)), cols = N - (tn * TN + wn * (NJ * 8));
+    mv = rows <= 0 ? 0 : (rows >= MI * 8 ? MI : (rows + 7) / 8);
+    nv = cols <= 0 ? 0 : (cols >= NJ * 8 ? NJ : (cols + 7) / 8);
+  };
+  set_valid(0);
   for (int it = 0; it < total; ++it) {
     if (tid == 0) produce();
     const unsigned g = c.pipe + it;
@@ -302,32 +313,38 @@ __device__ __forceinline__ void gemm(Ctx& c, const bool sub, const int a_src, in
     mbar_wait(&c.full[s], (g / STAGES) & 1);
     const double* sa = smem + s * STAGE_DBL;
     const double* sb = sa + STAGE_A;
+    auto mainloop = [&](auto edge) {
 #pragma unroll
-    for (int ks = 0; ks < KC; ks += 4) {
-      double af[MI], bf[NJ];
+      for (int ks = 0; ks < KC; ks += 4) {
+        double af[MI], bf[NJ];
 #pragma unroll
-      for (int i = 0; i < MI; ++i) {
-        const int row = wm * (MI * 8) + i * 8 + lr, k = ks + lc;
-        if (A_PAD) {
-          af[i] = sa[row * A_STRIDE + k];
-        } else {
-          // 128B swizzle: 16-byte chunk index ^= row % 8  (row % 8 == lr here)
-          af[i] = sa[row * A_STRIDE + ((((k >> 1) ^ lr) << 1) | (k & 1))];
+        for (int i = 0; i < MI; ++i) {
+          const int row = wm * (MI * 8) + i * 8 + lr, k = ks + lc;
+          if (A_PAD) {
+            af[i] = sa[row * A_STRIDE + k];
+          } else {
+            // 128B swizzle: 16-byte chunk index ^= row % 8  (row % 8 == lr here)
+            af[i] = sa[row * A_STRIDE + ((((k >> 1) ^ lr) << 1) | (k & 1))];
+          }
         }
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) bf[j] = sb[(ks + lc) * B_STRIDE + wn * 32 + j * 8 + lr];
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int j = 0; j < NJ; ++j)
+            if (!decltype(edge)::value || (i < mv && j < nv)) dmma(acc[i][j], af[i], bf[j]);
       }
-#pragma unroll
-      for (int j = 0; j < NJ; ++j) bf[j] = sb[(ks + lc) * B_STRIDE + wn * 32 + j * 8 + lr];
-#pragma unroll
-      for (int i = 0; i < MI; ++i)
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) dmma(acc[i][j], af[i], bf[j]);
-    }
+    };
+    if (mv == MI && nv == NJ) mainloop(std::false_type{});
+    else if (mv > 0 && nv > 0) mainloop(std::true_type{});
     __syncwarp();
     if (lane == 0) mbar_arrive(&c.empty[s]);
     if (++kc == kchunks) {
       kc = 0;
       const int tm = tile / tiles_n, tn = tile - tm * tiles_n;
       ++tile;
+      if (tile < tiles) set_valid(tile);
       if (sub) {
         // C -= acc through TMA reduce-add in L2: -acc goes to a per-warp smem ring
         // (two [8][16] blocks per m-tile) and drains asynchronously.

@@ -525,7 +525,7 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
   double* S = c.smem;                          // column-major [WB][n_cand]: S[j * NS + r]
   const int NS = n_cand;
   // staging T (<= 32 x 32) and Q (<= 16 x 32) alias S; Ut sits after all of them
-  double* Ut = c.smem + (size_t)max(c.n_piv * WB, 1024);  // WB x 32, Ut[j*32 + kk]
+  double* Ut = c.smem + (size_t)max(n_cand * WB, 1024);  // WB x 32, Ut[j*32 + kk]
   unsigned long long* prof = c.prof;
   long long tp = (prof && tid == 0) ? clock64() : 0;
 #define PANEL_TICK(slot)                                   \
@@ -769,10 +769,15 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
 #undef PANEL_TICK
 }
 
-// Columns [c0, c0+w), w <= SMALL_PANEL.
+// Columns [c0, c0+w), w <= SMALL_PANEL.  The block width grows as the
+// candidate set shrinks (the smem block holds n_cand x WB doubles).
 __device__ void lu_small(Ctx& c, int c0, int w) {
-  for (int b0 = c0; b0 < c0 + w; b0 += c.wb) {
-    switch (c.wb) {
+  int wb = c.wb;
+  while (wb < 8 && (size_t)(c.n_piv - c0) * (2 * wb) * 8 + 32 * 2 * wb * 8 <= (size_t)PANEL_SMEM_CAP &&
+         w % (2 * wb) == 0)
+    wb *= 2;
+  for (int b0 = c0; b0 < c0 + w; b0 += wb) {
+    switch (wb) {
       case 8: panel_block<8>(c, c0, w, b0); break;
       case 4: panel_block<4>(c, c0, w, b0); break;
       case 2: panel_block<2>(c, c0, w, b0); break;

@@ -279,7 +279,7 @@ def main():
         torch.cuda.empty_cache()
         h_coef = torch.from_numpy(pack).pin_memory().numpy()
         h_out = torch.empty((L, m, m), dtype=torch.float64, pin_memory=True).numpy()
-        chunk = 4 * eng.slots
+        chunk = eng.slots // 2   # D2H granularity of the single-launch streamed path
         eng.dtn_host(h_coef[:chunk], out=h_out[:chunk], chunk_leaves=chunk)
         barrier()
         ts = []
@@ -295,8 +295,9 @@ def main():
         del h_coef, h_out
         e2e = {"value": world * L / e2e_t, "unit": "leaf DtN maps/s",
                "h2d_bytes_per_step": int(pack.nbytes), "d2h_bytes_per_step": int(L * m * m * 8),
-               "path": "LeafEngine.dtn_host -> hps_leaf_dtn_host (C ABI), chunks of "
-                       f"{chunk} leaves, copy/compute overlap on 2 streams"}
+               "path": "LeafEngine.dtn_host -> hps_leaf_dtn_host (C ABI): H2D of all coefficients, "
+                       "one persistent launch, D2H of each finished "
+                       f"{chunk}-leaf chunk overlapped via device completion counters"}
 
 
     if rank == 0:

@@ -116,6 +116,8 @@ struct LeafParams {
   double* stats;          // n_leaves * 2 : min |pivot|, max |pivot| over real columns
   unsigned long long* prof;  // optional [slots][PROF_SLOTS] cycle counters (diagnostics)
   int* leaf_counter;         // next leaf to reduce (zeroed before each launch)
+  int* done_counts;          // optional: finished leaves per output chunk (streamed D2H)
+  int done_chunk;            // leaves per output chunk
 };
 
 constexpr int PROF_SLOTS = 16;  // 0..5 op kinds, 6 assemble, 7 output, 8 gemm flops/2^20, 9 leaves
@@ -1289,6 +1291,12 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
       P.stats[2 * leaf] = s_pmin;
       P.stats[2 * leaf + 1] = s_pmax;
     }
+    if (P.done_counts) {
+      // outputs of this leaf complete and visible device-wide before the count
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) atomicAdd(P.done_counts + leaf / P.done_chunk, 1);
+    }
     __syncthreads();
     if (prof && threadIdx.x == 0) prof[7] += clock64() - t0;
   }
@@ -1439,6 +1447,12 @@ struct hps_plan_s {
   double* h_stage = nullptr;
   unsigned long long* prof = nullptr;  // diagnostics counters (device), optional
   int* leaf_counter = nullptr;
+  // streamed host-buffer DtN: device copies of all inputs / outputs (grow-only)
+  double* s_coef = nullptr;
+  double* s_out = nullptr;
+  double* s_stats = nullptr;
+  int* s_done = nullptr;
+  size_t s_leaves = 0;
   TmaMaps maps[4];
   int maps_ok[4] = {0, 0, 0, 0};
 };
@@ -1572,7 +1586,8 @@ static int ensure_program(hps_plan_s* P, int mode) {
 }
 
 static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, const double* in0,
-                  const double* in1, double* out0, double* out1, double* stats, cudaStream_t stream) {
+                  const double* in1, double* out0, double* out1, double* stats, cudaStream_t stream,
+                  int* done_counts = nullptr, int done_chunk = 1) {
   if (n_leaves <= 0) return 0;
   CK(cudaSetDevice(P->device));
   if (ensure_program(P, mode) != 0) return -1;
@@ -1597,6 +1612,8 @@ static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, c
   L.D1 = P->D1; L.D2 = P->D2; L.a_bi = P->a_bi; L.a_bb = P->a_bb;
   L.prof = P->prof;
   L.leaf_counter = P->leaf_counter;
+  L.done_counts = done_counts;
+  L.done_chunk = done_chunk;
   CK(cudaMemsetAsync(P->leaf_counter, 0, sizeof(int), stream));
   L.coeffs = coeffs; L.in0 = in0; L.in1 = in1; L.out0 = out0; L.out1 = out1; L.stats = stats;
   const int panel_bytes = ((P->n_pad * P->wb > 1024 ? P->n_pad * P->wb : 1024) + 32 * P->wb) * 8;
@@ -1713,6 +1730,7 @@ int hps_plan_destroy(hps_plan_t P) {
   cudaSetDevice(P->device);
   cudaFree(P->D1); cudaFree(P->D2); cudaFree(P->a_bi); cudaFree(P->a_bb);
   cudaFree(P->leaf_counter);
+  cudaFree(P->s_coef); cudaFree(P->s_out); cudaFree(P->s_stats); cudaFree(P->s_done);
   cudaFree(P->Q); cudaFree(P->a_bi_pad); cudaFree(P->bpos);
   cudaFree(P->work); cudaFree(P->piv); cudaFree(P->scratch);
   for (int k = 0; k < 4; ++k) cudaFree(P->prog[k]);
@@ -1786,15 +1804,24 @@ int hps_leaf_apply(hps_plan_t P, int n_leaves, const double* coeffs, const doubl
   return 0;
 }
 
-// Host-buffer DtN with the two-level schedule on the device: chunks of
-// `chunk_leaves` leaves flow H2D (input stream) -> kernel (compute stream) ->
-// D2H (output stream), double-buffered, so PCIe traffic in both directions
-// overlaps the LU work of the neighbouring chunks.
-int hps_leaf_dtn_host(hps_plan_t P, int n_leaves, const double* coeffs_host, double* dtn_host,
-                      double* stats_host, int chunk_leaves) {
-  if (!P) return fail("null plan");
-  if (n_leaves <= 0) return 0;
-  CK(cudaSetDevice(P->device));
+static PFN_cuStreamWaitValue32_v11070 wait_value_fn() {
+  static PFN_cuStreamWaitValue32_v11070 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(p);
+  }
+  return fn;
+}
+
+// Chunked fallback: chunks of `chunk_leaves` leaves flow H2D (input stream) ->
+// kernel (compute stream) -> D2H (output stream), double-buffered.
+static int dtn_host_chunked(hps_plan_t P, int n_leaves, const double* coeffs_host, double* dtn_host,
+                            double* stats_host, int chunk_leaves) {
   if (chunk_leaves <= 0) chunk_leaves = P->slots * 4;
   if (chunk_leaves > n_leaves) chunk_leaves = n_leaves;
   const size_t cbytes = (size_t)P->ncoef * P->n * 8, tbytes = (size_t)P->m * P->m * 8;
@@ -1818,13 +1845,11 @@ int hps_leaf_dtn_host(hps_plan_t P, int n_leaves, const double* coeffs_host, dou
     const int b = ci & 1;
     const int l0 = ci * chunk_leaves;
     const int cnt = (n_leaves - l0 < chunk_leaves) ? (n_leaves - l0) : chunk_leaves;
-    // input buffer b was last read by the kernel of chunk ci-2
     if (ci >= 2) cudaStreamWaitEvent(s_in, ev_done[b], 0);
     cudaMemcpyAsync(d_coef[b], coeffs_host + (size_t)l0 * P->ncoef * P->n, cbytes * cnt,
                     cudaMemcpyHostToDevice, s_in);
     cudaEventRecord(ev_in[b], s_in);
     cudaStreamWaitEvent(s_comp, ev_in[b], 0);
-    // output buffer b was last drained by the D2H of chunk ci-2
     if (ci >= 2) cudaStreamWaitEvent(s_comp, ev_out[b], 0);
     rc = launch(P, MODE_DTN, cnt, d_coef[b], nullptr, nullptr, d_dtn[b], nullptr, d_stats[b], s_comp);
     cudaEventRecord(ev_done[b], s_comp);
@@ -1848,6 +1873,80 @@ int hps_leaf_dtn_host(hps_plan_t P, int n_leaves, const double* coeffs_host, dou
   cudaStreamDestroy(s_out);
   if (rc != 0) return rc;
   const cudaError_t e = e0 != cudaSuccess ? e0 : (e1 != cudaSuccess ? e1 : e2);
+  if (e != cudaSuccess) return fail(std::string("streamed dtn failed: ") + cudaGetErrorString(e));
+  return 0;
+}
+
+// Host-buffer DtN with the two-level schedule on the device.  Preferred path:
+// ONE persistent launch over all leaves (no chunk-boundary tails); the kernel
+// counts finished leaves per output chunk in device memory and the D2H stream
+// waits on those counters (cuStreamWaitValue32), so each chunk of DtN maps is
+// copied to the host while later leaves are still being reduced.  Falls back
+// to chunked launches when the outputs do not fit in device memory or stream
+// memory operations are unavailable.
+int hps_leaf_dtn_host(hps_plan_t P, int n_leaves, const double* coeffs_host, double* dtn_host,
+                      double* stats_host, int chunk_leaves) {
+  if (!P) return fail("null plan");
+  if (n_leaves <= 0) return 0;
+  CK(cudaSetDevice(P->device));
+  const size_t cbytes = (size_t)P->ncoef * P->n * 8, tbytes = (size_t)P->m * P->m * 8;
+  auto wait_fn = wait_value_fn();
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  const size_t need = (size_t)n_leaves * (cbytes + tbytes + 16);
+  const size_t have = P->s_leaves >= (size_t)n_leaves ? need : 0;
+  if (!wait_fn || (have == 0 && need > free_b / 10 * 6))
+    return dtn_host_chunked(P, n_leaves, coeffs_host, dtn_host, stats_host, chunk_leaves);
+  if (P->s_leaves < (size_t)n_leaves) {
+    cudaFree(P->s_coef); cudaFree(P->s_out); cudaFree(P->s_stats); cudaFree(P->s_done);
+    P->s_coef = nullptr; P->s_out = nullptr; P->s_stats = nullptr; P->s_done = nullptr;
+    P->s_leaves = 0;
+    CK(cudaMalloc(&P->s_coef, cbytes * n_leaves));
+    CK(cudaMalloc(&P->s_out, tbytes * n_leaves));
+    CK(cudaMalloc(&P->s_stats, 16 * (size_t)n_leaves));
+    CK(cudaMalloc(&P->s_done, sizeof(int) * ((size_t)n_leaves + 1)));
+    P->s_leaves = n_leaves;
+  }
+  int chunk = chunk_leaves > 0 ? chunk_leaves : P->slots / 2;
+  if (chunk < 1) chunk = 1;
+  const int nchunks = (n_leaves + chunk - 1) / chunk;
+  cudaStream_t s_comp, s_out;
+  CK(cudaStreamCreateWithFlags(&s_comp, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
+  cudaEvent_t ev_start;
+  CK(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+  CK(cudaMemsetAsync(P->s_done, 0, sizeof(int) * nchunks, s_comp));
+  CK(cudaMemcpyAsync(P->s_coef, coeffs_host, cbytes * n_leaves, cudaMemcpyHostToDevice, s_comp));
+  cudaEventRecord(ev_start, s_comp);  // counters zeroed before any wait is evaluated
+  cudaStreamWaitEvent(s_out, ev_start, 0);
+  int rc = launch(P, MODE_DTN, n_leaves, P->s_coef, nullptr, nullptr, P->s_out, nullptr, P->s_stats,
+                  s_comp, P->s_done, chunk);
+  bool waits_ok = true;
+  for (int k = 0; k < nchunks && rc == 0; ++k) {
+    const int l0 = k * chunk, cnt = (n_leaves - l0 < chunk) ? n_leaves - l0 : chunk;
+    if (waits_ok &&
+        wait_fn((CUstream)s_out, (CUdeviceptr)(P->s_done + k), (cuuint32_t)cnt, CU_STREAM_WAIT_VALUE_GEQ) !=
+            CUDA_SUCCESS) {
+      waits_ok = false;  // cannot wait on counters: copy after the kernel instead
+      cudaEvent_t ev_k;
+      cudaEventCreateWithFlags(&ev_k, cudaEventDisableTiming);
+      cudaEventRecord(ev_k, s_comp);
+      cudaStreamWaitEvent(s_out, ev_k, 0);
+      cudaEventDestroy(ev_k);
+    }
+    cudaMemcpyAsync(dtn_host + (size_t)l0 * P->m * P->m, P->s_out + (size_t)l0 * P->m * P->m,
+                    tbytes * cnt, cudaMemcpyDeviceToHost, s_out);
+    if (stats_host)
+      cudaMemcpyAsync(stats_host + 2 * (size_t)l0, P->s_stats + 2 * (size_t)l0, 16 * (size_t)cnt,
+                      cudaMemcpyDeviceToHost, s_out);
+  }
+  cudaError_t e1 = cudaStreamSynchronize(s_comp);
+  cudaError_t e2 = cudaStreamSynchronize(s_out);
+  cudaEventDestroy(ev_start);
+  cudaStreamDestroy(s_comp);
+  cudaStreamDestroy(s_out);
+  if (rc != 0) return rc;
+  const cudaError_t e = e1 != cudaSuccess ? e1 : e2;
   if (e != cudaSuccess) return fail(std::string("streamed dtn failed: ") + cudaGetErrorString(e));
   return 0;
 }

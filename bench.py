@@ -216,7 +216,8 @@ def main():
 
     import torch
     torch.cuda.set_device(local)
-    if world > 1:
+    distributed = "RANK" in os.environ and "WORLD_SIZE" in os.environ  # launched by torchrun
+    if distributed:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     from paper_2503_04033_b200.engine import LeafEngine
@@ -230,7 +231,7 @@ def main():
     stream = torch.cuda.current_stream()
 
     def barrier():
-        if world > 1:
+        if distributed:
             torch.distributed.barrier()
 
     for _ in range(args.warmup):
@@ -251,7 +252,7 @@ def main():
     barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = float(sum(step_ms))
-    if world > 1:
+    if distributed:
         t = torch.tensor([total_ms], device=f"cuda:{local}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
@@ -288,7 +289,7 @@ def main():
             eng.dtn_host(h_coef, out=h_out, chunk_leaves=chunk)
             ts.append(time.perf_counter() - t0)
         e2e_t = float(np.mean(ts))
-        if world > 1:
+        if distributed:
             t = torch.tensor([e2e_t], device=f"cuda:{local}", dtype=torch.float64)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             e2e_t = float(t.item())
@@ -327,7 +328,7 @@ def main():
             "clocks": clk.summary(), "wall_s_timed": t_wall,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if distributed:
         torch.distributed.destroy_process_group()
 
 

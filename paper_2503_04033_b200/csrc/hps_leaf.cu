@@ -120,7 +120,8 @@ struct LeafParams {
   int done_chunk;            // leaves per output chunk
 };
 
-constexpr int PROF_SLOTS = 16;  // 0..5 op kinds, 6 assemble, 7 output, 8 gemm flops/2^20, 9 leaves
+constexpr int PROF_SLOTS = 24;  // 0..8 op kinds, 9 leaves, 10-14 panel steps, 15 interchanges,
+                                // 16-18 GEMM cycles by N (<=64, <=256, >256), 19-21 their MFLOP, 22 assemble, 23 output
 
 // ---------------------------------------------------------------------------
 // PTX helpers
@@ -1236,7 +1237,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     assemble(P, c.M, leaf, c.smem);
     if (threadIdx.x == 0) { s_pmin = INFINITY; s_pmax = 0.0; }
     __syncthreads();
-    if (prof && threadIdx.x == 0) { prof[6] += clock64() - t0; prof[9] += 1; }
+    if (prof && threadIdx.x == 0) { prof[22] += clock64() - t0; prof[9] += 1; }
     for (int k = 0; k < n_ops; ++k) {
       const Op op = ops[k];
       if (prof) t0 = clock64();
@@ -1255,8 +1256,14 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
         }
       }
       if (prof && threadIdx.x == 0) {
-        prof[op.kind] += clock64() - t0;
-        if (op.kind >= OP_GEMM_SUB) prof[8] += (2ull * op.Mdim * op.Ndim * op.Kdim) >> 20;
+        const long long dt = clock64() - t0;
+        prof[op.kind] += dt;
+        if (op.kind == OP_GEMM_SUB || op.kind == OP_GEMM_SET || op.kind == OP_GEMM_SET_Q ||
+            op.kind == OP_GEMM_SUB_ABI) {
+          const int bucket = op.Ndim <= 64 ? 0 : (op.Ndim <= 256 ? 1 : 2);
+          prof[16 + bucket] += dt;
+          prof[19 + bucket] += (2ull * op.Mdim * op.Ndim * op.Kdim) >> 20;
+        }
       }
     }
     if (prof) t0 = clock64();
@@ -1298,7 +1305,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
       if (threadIdx.x == 0) atomicAdd(P.done_counts + leaf / P.done_chunk, 1);
     }
     __syncthreads();
-    if (prof && threadIdx.x == 0) prof[7] += clock64() - t0;
+    if (prof && threadIdx.x == 0) prof[23] += clock64() - t0;
   }
 }
 

@@ -21,25 +21,32 @@ def run():
     else:
         eng.reduce_load(coeffs, f)
 run(); torch.cuda.synchronize()
-cnt = torch.zeros(eng.slots * 16, dtype=torch.int64, device="cuda")
+cnt = torch.zeros(eng.slots * 24, dtype=torch.int64, device="cuda")
 eng.lib.hps_plan_set_profile(eng.plan, ctypes.c_void_p(cnt.data_ptr()))
 e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
 e0.record(); run(); e1.record(); torch.cuda.synchronize()
 eng.lib.hps_plan_set_profile(eng.plan, ctypes.c_void_p(0))
 ms = e0.elapsed_time(e1)
-c = cnt.view(eng.slots, 16).cpu().numpy().astype(float)
-names = ["small-panel", "swaps", "inv-lower", "inv-upper", "gemm-sub", "gemm-set", "assemble", "output"]
-tot = c[:, :8].sum()
+c = cnt.view(eng.slots, 24).cpu().numpy().astype(float)
+names = ["small-panel", "swaps", "inv-lower", "inv-upper", "gemm-sub", "gemm-set", "gemm-set-Q", "gemm-sub-abi", "copy-abb"]
+tot = c[:, :9].sum() + c[:, 22].sum() + c[:, 23].sum()
 leaves = c[:, 9].sum()
 print(f"p={a.p} leaves={a.leaves} mode={a.mode} kernel {ms:.1f} ms, {a.leaves/ms*1e3:.1f} leaves/s, "
       f"{a.leaves*dtn_flops_executed(eng.n, eng.m, a.p-2)/ms/1e9:.2f} TFLOP/s executed, "
       f"{a.leaves*dtn_flops(eng.n, eng.m)/ms/1e9:.2f} reference-equivalent")
 clk = 1.965e9
-for i, nm in enumerate(names):
+for i, nm in list(enumerate(names)) + [(22, "assemble"), (23, "output")]:
+    if c[:, i].sum() == 0:
+        continue
     print(f"  {nm:12s} {100*c[:, i].sum()/tot:6.2f}%   {c[:, i].sum()/leaves/clk*1e3:8.2f} ms/leaf")
+for b, nm in enumerate(["N<=64", "N<=256", "N>256"]):
+    cyc, mf = c[:, 16 + b].sum(), c[:, 19 + b].sum() * 2**20
+    if cyc:
+        print(f"    gemm {nm:7s} {cyc/leaves/clk*1e3:8.2f} ms/leaf  {mf/leaves:.2e} flop/leaf  "
+              f"{mf/cyc*clk/1e9:6.1f} GF/s per CTA")
 for i, nm in zip(range(10, 15), ["p1-utop", "p2-gather", "p3-pivot", "p4-writeback", "p5-swaps"]):
     print(f"    {nm:12s} {c[:, i].sum()/leaves/clk*1e3:8.2f} ms/leaf")
 print(f"  row interchanges per leaf: {c[:, 15].sum()/leaves:.0f} of {eng.n} pivots")
-gf = c[:, 8].sum() * 2**20
-print(f"  gemm flops/leaf {gf/leaves:.3e}; gemm-only rate per SM {gf/(c[:, 4].sum()+c[:, 5].sum())*clk/1e9:.1f} GFLOP/s "
+gf = sum(c[:, 19 + b].sum() for b in range(3)) * 2**20
+print(f"  gemm flops/leaf {gf/leaves:.3e}; gemm-only rate per CTA {gf/(c[:, 16:19].sum())*clk/1e9:.1f} GFLOP/s "
       f"(peak 251/SM); per-leaf total {tot/leaves/clk*1e3:.1f} ms")

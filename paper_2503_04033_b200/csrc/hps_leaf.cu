@@ -118,6 +118,7 @@ struct LeafParams {
   int* leaf_counter;         // next leaf to reduce (zeroed before each launch)
   int* done_counts;          // optional: finished leaves per output chunk (streamed D2H)
   int done_chunk;            // leaves per output chunk
+  int smem_doubles;          // dynamic shared memory of the launch, in doubles
 };
 
 constexpr int PROF_SLOTS = 24;  // 0..8 op kinds, 9 leaves, 10-14 panel steps, 15 interchanges,
@@ -227,6 +228,7 @@ struct Ctx {
   int* piv;
   double* scratch;
   double* smem;
+  int smem_doubles;
   unsigned long long* prof;
   const TmaMaps* maps;
   uint64_t* full;   // STAGES mbarriers: stage filled (TMA tx complete)
@@ -776,9 +778,12 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
 // candidate set shrinks (the smem block holds n_cand x WB doubles).
 __device__ void lu_small(Ctx& c, int c0, int w) {
   int wb = c.wb;
-  while (wb < 8 && (size_t)(c.n_piv - c0) * (2 * wb) * 8 + 32 * 2 * wb * 8 <= (size_t)PANEL_SMEM_CAP &&
-         w % (2 * wb) == 0)
-    wb *= 2;
+  // panel block smem: max(n_cand * WB, 1024) doubles (S and the staging it hosts) + 32 * WB (Ut)
+  auto fits = [&](int W) {
+    const int sz = (c.n_piv - c0) * W;
+    return (sz > 1024 ? sz : 1024) + 32 * W <= c.smem_doubles;
+  };
+  while (wb < 8 && w % (2 * wb) == 0 && fits(2 * wb)) wb *= 2;
   for (int b0 = c0; b0 < c0 + w; b0 += wb) {
     switch (wb) {
       case 8: panel_block<8>(c, c0, w, b0); break;
@@ -1221,6 +1226,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
   c.piv = P.piv + (size_t)slot * P.n_pad;
   c.scratch = P.scratch + (size_t)slot * TRI_BLOCK * TRI_BLOCK;
   c.smem = smem;
+  c.smem_doubles = P.smem_doubles;
 
   unsigned long long* prof = P.prof ? P.prof + (size_t)slot * PROF_SLOTS : nullptr;
   c.prof = prof;
@@ -1529,6 +1535,17 @@ static int ensure_workspace(hps_plan_s* P, int mode, int want_slots) {
     if (fit < 1) return fail("memory budget cannot hold one leaf workspace");
     if ((size_t)slots > fit) slots = (int)fit;
   }
+  {
+    // never claim more than ~85% of the currently free device memory (large p:
+    // a p = 22 slot is ~0.7 GB); memory already held by this plan counts as free
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+      free_b += P->work_doubles * 8;
+      const size_t fit = free_b / 100 * 85 / slot_bytes;
+      if (fit < 1) return fail("device memory cannot hold one leaf workspace");
+      if ((size_t)slots > fit) slots = (int)fit;
+    }
+  }
   if (P->work && P->work_doubles >= per * (size_t)slots && P->ws_slots >= slots) {
     if (!P->maps_ok[mode]) {
       int NR, NC;
@@ -1627,6 +1644,7 @@ static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, c
   int smem = GEMM_SMEM_BYTES;
   if (panel_bytes > smem) smem = panel_bytes;
   if (2 * TRI_BLOCK * TRI_LD * 8 > smem) smem = 2 * TRI_BLOCK * TRI_LD * 8;
+  L.smem_doubles = smem / 8;
   CK(cudaFuncSetAttribute(hps_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   CK(cudaFuncSetAttribute(hps_leaf_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   hps_leaf_kernel<<<slots, NT, smem, stream>>>(L, P->prog[mode], P->prog_len[mode], P->maps[mode]);

@@ -103,7 +103,7 @@ struct LeafParams {
   size_t slot_stride;     // doubles per slot matrix
   double* work;           // slots * slot_stride
   int* piv;               // slots * n_pad
-  double* scratch;        // slots * TRI_BLOCK * TRI_BLOCK
+  double* scratch;        // slots * 2 n_pad * TRI_BLOCK: cached diagonal-block inverses
   const double* D1;       // d * p * p (scaled first derivative)
   const double* D2;       // d * p * p (D1 @ D1, computed on host like the reference)
   const double* a_bi;     // m * n
@@ -119,6 +119,7 @@ struct LeafParams {
   int* done_counts;          // optional: finished leaves per output chunk (streamed D2H)
   int done_chunk;            // leaves per output chunk
   int smem_doubles;          // dynamic shared memory of the launch, in doubles
+  int debug;                 // diagnostics (env HPS_DEBUG): 1 skip the LU program, 2 old DtN output
 };
 
 constexpr int PROF_SLOTS = 24;  // 0..8 op kinds, 9 leaves, 10-14 panel steps, 15 interchanges,
@@ -216,7 +217,7 @@ constexpr unsigned STAGE_BYTES = (unsigned)((STAGE_A + STAGE_B) * 8);  // TMA tr
 struct TmaMaps {
   CUtensorMap a_work;     // box {A_STRIDE, TM, 1} over [slots][NR][NC]
   CUtensorMap b_work;     // box {B_STRIDE, KC, 1}
-  CUtensorMap a_scratch;  // box {A_STRIDE, TM, 1} over [slots][TRI][TRI]
+  CUtensorMap a_scratch;  // box {A_STRIDE, TM, 1} over [slots][2 n_pad][TRI]
   CUtensorMap c_red;      // box {16, 8, 1} over [slots][NR][NC]: epilogue reduce-add
   CUtensorMap a_abi;      // legendre: box {A_STRIDE, TM, 1} over the plan's a_bi [m_pad][n_pad]
   CUtensorMap b_q;        // legendre: box {B_STRIDE, KC, 1} over the plan's Q [nb_pad][m_pad]
@@ -847,7 +848,8 @@ __device__ void invert_unit_lower(const Ctx& c, int r0, int h) {
     }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < h * TRI_BLOCK; e += NT) c.scratch[e] = X[(e / TRI_BLOCK) * TRI_LD + e % TRI_BLOCK];
+  double* dst = c.scratch + (size_t)r0 * TRI_BLOCK;
+  for (int e = threadIdx.x; e < h * TRI_BLOCK; e += NT) dst[e] = X[(e / TRI_BLOCK) * TRI_LD + e % TRI_BLOCK];
   __syncthreads();
 }
 
@@ -879,7 +881,8 @@ __device__ void invert_upper(const Ctx& c, int r0, int h) {
     }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < h * TRI_BLOCK; e += NT) c.scratch[e] = X[(e / TRI_BLOCK) * TRI_LD + e % TRI_BLOCK];
+  double* dst = c.scratch + (size_t)(c.n_piv + r0) * TRI_BLOCK;
+  for (int e = threadIdx.x; e < h * TRI_BLOCK; e += NT) dst[e] = X[(e / TRI_BLOCK) * TRI_LD + e % TRI_BLOCK];
   __syncthreads();
 }
 
@@ -892,10 +895,10 @@ __device__ void invert_upper(const Ctx& c, int r0, int h) {
 enum OpKind : int {
   OP_SMALL = 0,      // lu_small(c0=a, w=b)
   OP_SWAP = 1,       // apply_swaps(j0=a, cnt=b, c_lo=c, c_hi=d)
-  OP_INV_LOWER = 2,  // scratch := inv(unit lower M[a..a+b, a..a+b])
-  OP_INV_UPPER = 3,  // scratch := inv(upper M[a..a+b, a..a+b])
+  OP_INV_LOWER = 2,  // scratch[a..a+b, :] := inv(unit lower M[a..a+b, a..a+b])
+  OP_INV_UPPER = 3,  // scratch[n_pad+a.., :] := inv(upper M[a..a+b, a..a+b])
   OP_GEMM_SUB = 4,   // M[c_r.., c_c..] -= M[a_r.., a_c..] * M[b_r.., b_c..]  (Mdim, Ndim, Kdim)
-  OP_GEMM_SET = 5,   // M[c_r.., c_c..]  = scratch * M[b_r.., b_c..]
+  OP_GEMM_SET = 5,   // M[c_r.., c_c..]  = scratch[a_r.., 0..] * M[b_r.., b_c..]
   OP_GEMM_SET_Q = 6, // legendre: A_ib = R_b (slot) * Q (plan)
   OP_GEMM_SUB_ABI = 7,  // legendre: T -= a_bi (plan) * X (slot)
   OP_COPY_ABB = 8,   // legendre: T region := a_bb (rows [0,m), cols [a, a+m))
@@ -1143,6 +1146,121 @@ __device__ void copy_block(const double* src, int ld, double* out, int ld_out, i
 // -D1[a][0][.] (low face) / +D1[a][p-1][.] (high face) (local_ops.py:310-315).
 // Each interior line serves the two opposite face DOFs, so X is read once per
 // line: 2 q m^2 flops instead of the dense 2 n m^2.
+// Streamed variant: X is read exactly once.  X's rows are walked in slabs of
+// fixed first index i (S = q^(d-1) rows): the lines along the last d-1 axes
+// lie inside one slab and finish there; the lines along axis 0 take their i-th
+// point from slab i and accumulate in shared memory.  Columns go in chunks of
+// CW through an NBUF-deep cp.async ring.  A_bb (two structural nonzeros per
+// row, the line endpoints: a_bb[b, b_lo] = sign D1[a][edge][0], a_bb[b, b_hi] =
+// sign D1[a][edge][p-1]) is added in registers instead of read from HBM.
+// Returns false when the slab ring does not fit; the caller then uses dtn_lines.
+constexpr int LINE_NBUF = 4;
+__device__ bool dtn_lines_stream(const LeafParams& P, Ctx& c, const double* M, int ld, double* T) {
+  __shared__ double s_w[3][2][32];
+  __shared__ double s_e[3][2][2];
+  const int q = P.q, p = P.p, d = P.d, m = P.m;
+  const int S = (d == 3) ? q * q : q;
+  int CW = 8;
+  while (CW >= 2 && (2 + LINE_NBUF) * S * CW > c.smem_doubles) CW >>= 1;
+  if (CW < 2 || q > 32) return false;
+  __syncthreads();  // smem is free (previous op finished with it)
+  for (int e = threadIdx.x; e < d * 2 * q; e += NT) {
+    const int a = e / (2 * q), side = (e / q) & 1, i = e % q;
+    s_w[a][side][i] = P.D1[(a * p + (side ? p - 1 : 0)) * p + i + 1];
+  }
+  if (threadIdx.x < d * 4) {
+    const int a = threadIdx.x >> 2, side = (threadIdx.x >> 1) & 1, end = threadIdx.x & 1;
+    const double sgn = side ? 1.0 : -1.0;
+    s_e[a][side][end] = sgn * P.D1[(a * p + (side ? p - 1 : 0)) * p + (end ? p - 1 : 0)];
+  }
+  double* acc = c.smem;              // [2][S*CW]: axis-0 lines, low / high face
+  double* ring = c.smem + 2 * S * CW;  // [NBUF][S*CW]
+  const double* X = M + P.n_pad;
+  const int fd = S;
+  const int SC = S * CW;
+  const int vec = CW / 2;  // 16-byte pieces per row chunk
+  // in-slab line directions: d = 3 -> axis 1 (q lines, stride q) and axis 2 (q lines,
+  // stride 1); d = 2 -> axis 1 (1 line, stride 1)
+  const int nl = (d == 3) ? q : 1;
+  const int n_dir = d - 1;
+  auto load_slab = [&](int i, int c0) {
+    if (i < q) {
+      double* buf = ring + (i % LINE_NBUF) * SC;
+      const double* src = X + (size_t)(i * S) * ld + c0;
+      for (int e = threadIdx.x; e < S * vec; e += NT) {
+        const int r = e / vec, v = e - r * vec;
+        cp_async16(buf + r * CW + 2 * v, src + (size_t)r * ld + 2 * v, 16);
+      }
+    }
+    cp_async_commit();
+  };
+  auto put = [&](int b, int col0, int b_lo, int b_hi, const double* e2, double v0, double v1, bool neg) {
+    // T[b, col0 + {0,1}] = a_bb + (neg ? -v : v)
+    double o[2] = {v0, v1};
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int col = col0 + u;
+      const double abb = col == b_lo ? e2[0] : (col == b_hi ? e2[1] : 0.0);
+      o[u] = neg ? abb - o[u] : abb + o[u];
+    }
+    if (col0 + 1 < m) {
+      *reinterpret_cast<double2*>(T + (size_t)b * m + col0) = make_double2(o[0], o[1]);
+    } else if (col0 < m) {
+      T[(size_t)b * m + col0] = o[0];
+    }
+  };
+  for (int c0 = 0; c0 < m; c0 += CW) {
+    for (int e = threadIdx.x; e < 2 * SC; e += NT) acc[e] = 0.0;
+#pragma unroll 1
+    for (int s = 0; s < LINE_NBUF - 1; ++s) load_slab(s, c0);
+    for (int i = 0; i < q; ++i) {
+      cp_async_wait<LINE_NBUF - 2>();
+      __syncthreads();
+      load_slab(i + LINE_NBUF - 1, c0);
+      const double* buf = ring + (i % LINE_NBUF) * SC;
+      // axis-0 lines: slab row t is point i of line t
+      const double wl = s_w[0][0][i], wh = s_w[0][1][i];
+      for (int e = threadIdx.x; e < SC; e += NT) {
+        const double x = buf[e];
+        acc[e] += wl * x;
+        acc[SC + e] += wh * x;
+      }
+      // in-slab lines, two adjacent columns per item
+      const int items = n_dir * nl * vec;
+      for (int e = threadIdx.x; e < items; e += NT) {
+        const int v = e % vec, l = (e / vec) % nl, dir = e / (vec * nl);
+        const int a = dir + 1;
+        const int s0 = (d == 3 && a == 1) ? l : l * q;
+        const int st = (d == 3 && a == 1) ? q : 1;
+        double lo0 = 0.0, lo1 = 0.0, hi0 = 0.0, hi1 = 0.0;
+        for (int k = 0; k < q; ++k) {
+          const double2 x = *reinterpret_cast<const double2*>(buf + (s0 + k * st) * CW + 2 * v);
+          const double w0 = s_w[a][0][k], w1 = s_w[a][1][k];
+          lo0 += w0 * x.x; lo1 += w0 * x.y;
+          hi0 += w1 * x.x; hi1 += w1 * x.y;
+        }
+        const int t = i * nl + l;
+        const int b_lo = 2 * a * fd + t, b_hi = b_lo + fd;
+        const int col0 = c0 + 2 * v;
+        put(b_lo, col0, b_lo, b_hi, s_e[a][0], lo0, lo1, false);
+        put(b_hi, col0, b_lo, b_hi, s_e[a][1], hi0, hi1, true);
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    for (int e = threadIdx.x; e < S * vec; e += NT) {
+      const int t = e / vec, v = e - t * vec;
+      const int b_lo = t, b_hi = fd + t;
+      const int col0 = c0 + 2 * v;
+      put(b_lo, col0, b_lo, b_hi, s_e[0][0], acc[t * CW + 2 * v], acc[t * CW + 2 * v + 1], false);
+      put(b_hi, col0, b_lo, b_hi, s_e[0][1], acc[SC + t * CW + 2 * v], acc[SC + t * CW + 2 * v + 1],
+          true);
+    }
+    __syncthreads();
+  }
+  return true;
+}
+
 __device__ void dtn_lines(const LeafParams& P, const double* M, int ld, double* T) {
   __shared__ double s_w[3][2][32];
   const int q = P.q, p = P.p, d = P.d, m = P.m;
@@ -1224,7 +1342,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
   c.NR = P.NR;
   c.wb = P.wb;
   c.piv = P.piv + (size_t)slot * P.n_pad;
-  c.scratch = P.scratch + (size_t)slot * TRI_BLOCK * TRI_BLOCK;
+  c.scratch = P.scratch + (size_t)slot * 2 * P.n_pad * TRI_BLOCK;
   c.smem = smem;
   c.smem_doubles = P.smem_doubles;
 
@@ -1244,7 +1362,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     if (threadIdx.x == 0) { s_pmin = INFINITY; s_pmax = 0.0; }
     __syncthreads();
     if (prof && threadIdx.x == 0) { prof[22] += clock64() - t0; prof[9] += 1; }
-    for (int k = 0; k < n_ops; ++k) {
+    for (int k = 0; k < ((P.debug & 1) ? 0 : n_ops); ++k) {
       const Op op = ops[k];
       if (prof) t0 = clock64();
       switch (op.kind) {
@@ -1276,7 +1394,8 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     if (P.mode == MODE_DTN && P.legendre) {
       copy_block(c.M + P.col_rb, c.ld, P.out0 + (size_t)leaf * P.m * P.m, P.m, P.m, P.m, false);
     } else if (P.mode == MODE_DTN) {
-      dtn_lines(P, c.M, c.ld, P.out0 + (size_t)leaf * P.m * P.m);
+      double* T = P.out0 + (size_t)leaf * P.m * P.m;
+      if ((P.debug & 2) || !dtn_lines_stream(P, c, c.M, c.ld, T)) dtn_lines(P, c.M, c.ld, T);
     } else if (P.mode == MODE_SOLOP) {
       copy_block(c.M + P.n_pad, c.ld, P.out0 + (size_t)leaf * P.n * P.m, P.m, P.n, P.m, true);
     } else {
@@ -1332,6 +1451,13 @@ int split16_host(int w) {
 
 struct ProgramBuilder {
   std::vector<Op> ops;
+  int n_pad = 0;
+  // diagonal blocks are final once factored (later interchanges only touch rows
+  // below them), so each block's inverse is computed once and reused by every
+  // recursion level that solves against it
+  // owner[g] = (r0, h) of the inverse whose rows currently occupy cache rows
+  // [16g, 16g + 16); a block is reusable while it still owns all its rows
+  std::vector<std::pair<int, int>> owner[2];
   void small(int c0, int w) { Op o{}; o.kind = OP_SMALL; o.a = c0; o.b = w; ops.push_back(o); }
   void swaps(int j0, int cnt, int lo, int hi) {
     if (hi <= lo || cnt <= 0) return;
@@ -1343,11 +1469,20 @@ struct ProgramBuilder {
     Op o{}; o.kind = kind; o.ar = ar; o.ac = ac; o.br = br; o.bc = bc; o.cr = cr; o.cc = cc;
     o.Mdim = M; o.Ndim = N; o.Kdim = K; ops.push_back(o);
   }
+  void inv_cached(int kind, int r0, int h) {
+    std::vector<std::pair<int, int>>& own = owner[kind == OP_INV_UPPER];
+    if (own.empty()) own.assign(n_pad / 16 + 1, {-1, -1});
+    bool valid = true;
+    for (int g = r0 / 16; g < (r0 + h + 15) / 16; ++g) valid = valid && own[g] == std::make_pair(r0, h);
+    if (valid) return;
+    for (int g = r0 / 16; g < (r0 + h + 15) / 16; ++g) own[g] = {r0, h};
+    inv(kind, r0, h);
+  }
   void trsm_lower(int r0, int h, int lo, int hi) {
     if (hi <= lo) return;
     if (h <= TRI_BLOCK) {
-      inv(OP_INV_LOWER, r0, h);
-      gemm(OP_GEMM_SET, 0, 0, r0, lo, r0, lo, h, hi - lo, h);
+      inv_cached(OP_INV_LOWER, r0, h);
+      gemm(OP_GEMM_SET, r0, 0, r0, lo, r0, lo, h, hi - lo, h);
       return;
     }
     const int h1 = split16_host(h);
@@ -1358,8 +1493,8 @@ struct ProgramBuilder {
   void trsm_upper(int r0, int h, int lo, int hi) {
     if (hi <= lo) return;
     if (h <= TRI_BLOCK) {
-      inv(OP_INV_UPPER, r0, h);
-      gemm(OP_GEMM_SET, 0, 0, r0, lo, r0, lo, h, hi - lo, h);
+      inv_cached(OP_INV_UPPER, r0, h);
+      gemm(OP_GEMM_SET, n_pad + r0, 0, r0, lo, r0, lo, h, hi - lo, h);
       return;
     }
     const int h1 = split16_host(h);
@@ -1528,7 +1663,7 @@ static size_t slot_doubles(const hps_plan_s* P, int mode) {
 
 static int ensure_workspace(hps_plan_s* P, int mode, int want_slots) {
   const size_t per = slot_doubles(P, mode);
-  size_t slot_bytes = per * 8 + (size_t)P->n_pad * 4 + (size_t)TRI_BLOCK * TRI_BLOCK * 8;
+  size_t slot_bytes = per * 8 + (size_t)P->n_pad * 4 + (size_t)2 * P->n_pad * TRI_BLOCK * 8;
   int slots = want_slots;
   if (P->budget > 0) {
     const size_t fit = P->budget / slot_bytes;
@@ -1554,8 +1689,8 @@ static int ensure_workspace(hps_plan_s* P, int mode, int want_slots) {
       TmaMaps& m = P->maps[mode];
       if (make_map(&m.a_work, P->work, NC, NR, P->ws_slots, NC, per, A_STRIDE, TM, !A_PAD) ||
           make_map(&m.b_work, P->work, NC, NR, P->ws_slots, NC, per, B_STRIDE, KC) ||
-          make_map(&m.a_scratch, P->scratch, TRI_BLOCK, TRI_BLOCK, P->ws_slots, TRI_BLOCK,
-                   TRI_BLOCK * TRI_BLOCK, A_STRIDE, TM, !A_PAD) ||
+          make_map(&m.a_scratch, P->scratch, TRI_BLOCK, 2 * P->n_pad, P->ws_slots, TRI_BLOCK,
+                   (size_t)2 * P->n_pad * TRI_BLOCK, A_STRIDE, TM, !A_PAD) ||
           make_map(&m.c_red, P->work, NC, NR, P->ws_slots, NC, per, 16, 8))
         return -1;
       if (P->legendre &&
@@ -1574,7 +1709,7 @@ static int ensure_workspace(hps_plan_s* P, int mode, int want_slots) {
   P->work = nullptr; P->piv = nullptr; P->scratch = nullptr;
   CK(cudaMalloc(&P->work, per * (size_t)slots * 8));
   CK(cudaMalloc(&P->piv, (size_t)P->n_pad * slots * 4));
-  CK(cudaMalloc(&P->scratch, (size_t)TRI_BLOCK * TRI_BLOCK * slots * 8));
+  CK(cudaMalloc(&P->scratch, (size_t)2 * P->n_pad * TRI_BLOCK * slots * 8));
   P->work_doubles = per * (size_t)slots;
   P->ws_slots = slots;
   for (int k = 0; k < 4; ++k) P->maps_ok[k] = 0;
@@ -1586,6 +1721,7 @@ static int ensure_program(hps_plan_s* P, int mode) {
   int NR, NC;
   mode_dims(P, mode, &NR, &NC);
   ProgramBuilder b;
+  b.n_pad = P->n_pad;
   // working columns: [A_ii | A_ib or rhs]; legendre adds an R_b / T region after them
   const bool leg_op = P->legendre && (mode == MODE_DTN || mode == MODE_SOLOP);
   const int NW = leg_op ? P->n_pad + P->m_pad : NC;
@@ -1645,6 +1781,7 @@ static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, c
   if (panel_bytes > smem) smem = panel_bytes;
   if (2 * TRI_BLOCK * TRI_LD * 8 > smem) smem = 2 * TRI_BLOCK * TRI_LD * 8;
   L.smem_doubles = smem / 8;
+  if (const char* dbg = getenv("HPS_DEBUG")) L.debug = atoi(dbg);
   CK(cudaFuncSetAttribute(hps_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   CK(cudaFuncSetAttribute(hps_leaf_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   hps_leaf_kernel<<<slots, NT, smem, stream>>>(L, P->prog[mode], P->prog_len[mode], P->maps[mode]);

@@ -102,7 +102,9 @@ struct LeafParams {
   int n_leaves;
   size_t slot_stride;     // doubles per slot matrix
   double* work;           // slots * slot_stride
-  int* piv;               // slots * n_pad
+  int* piv;               // slots * piv_stride: pivots (n_pad), then the RHS prefix table
+  int piv_stride;         // n_pad + n_pad / 16 + 16
+  int colperm;            // DtN drop mode: A_ib columns in slab order (see rhs_col)
   double* scratch;        // slots * 2 n_pad * TRI_BLOCK: cached diagonal-block inverses
   const double* D1;       // d * p * p (scaled first derivative)
   const double* D2;       // d * p * p (D1 @ D1, computed on host like the reference)
@@ -119,10 +121,11 @@ struct LeafParams {
   int* done_counts;          // optional: finished leaves per output chunk (streamed D2H)
   int done_chunk;            // leaves per output chunk
   int smem_doubles;          // dynamic shared memory of the launch, in doubles
-  int debug;                 // diagnostics (env HPS_DEBUG): 1 skip the LU program, 2 old DtN output
+  int debug;                 // diagnostics (env HPS_DEBUG): 1 skip the LU program, 2 old DtN output,
+                             // 4 natural A_ib column order without zero-prefix skipping
 };
 
-constexpr int PROF_SLOTS = 24;  // 0..8 op kinds, 9 leaves, 10-14 panel steps, 15 interchanges,
+constexpr int PROF_SLOTS = 26;  // 0..8 op kinds, 9 leaves, 10-14 panel steps, 15 interchanges,
                                 // 16-18 GEMM cycles by N (<=64, <=256, >256), 19-21 their MFLOP, 22 assemble, 23 output
 
 // ---------------------------------------------------------------------------
@@ -227,6 +230,7 @@ struct Ctx {
   double* M;
   int ld, n_piv, n_real, NR, wb, slot;
   int* piv;
+  int* rhs_tab;  // [n_pad / 16 + 1]: RHS columns with a nonzero above row 16 g (forward solve)
   double* scratch;
   double* smem;
   int smem_doubles;
@@ -902,12 +906,14 @@ enum OpKind : int {
   OP_GEMM_SET_Q = 6, // legendre: A_ib = R_b (slot) * Q (plan)
   OP_GEMM_SUB_ABI = 7,  // legendre: T -= a_bi (plan) * X (slot)
   OP_COPY_ABB = 8,   // legendre: T region := a_bb (rows [0,m), cols [a, a+m))
+  OP_RHS_PROFILE = 9,  // rhs_tab from the pivots (zero prefixes of P A_ib's columns)
 };
 
 struct Op {
   int kind;
   int a, b, c, d;          // generic small-op arguments
   int ar, ac, br, bc, cr, cc, Mdim, Ndim, Kdim;  // GEMM operands (row, col offsets)
+  int dyn;  // forward solve against the RHS: B rows above `dyn` are zero beyond rhs_tab[dyn/16] columns
 };
 
 // ---------------------------------------------------------------------------
@@ -944,6 +950,94 @@ __device__ __forceinline__ int boundary_index(const LeafParams& P, int a, int si
     fd = q;
   }
   return (2 * a + side) * fd + t;
+}
+
+// DtN drop mode orders the A_ib columns (slot columns n_pad + s) by slab of the
+// interior numbering instead of by face: both axis-0 faces first (their lines
+// cross every slab), then per first index i the axis-1 / axis-2 face DOFs whose
+// lines lie in slab i.  Column s then has no nonzero above row ~ i q^(d-1) of
+// A_ib, so the forward solve L^{-1} P A_ib skips the zero prefixes (rhs_tab).
+// L = lines per face per slab.  Natural boundary index b = (2a + side) fd + t.
+__device__ __forceinline__ int rhs_col(const LeafParams& P, int b) {
+  if (!P.colperm) return b;
+  const int fd = P.d == 3 ? P.q * P.q : P.q, L = P.d == 3 ? P.q : 1;
+  const int face = b / fd, t = b - face * fd, a = face >> 1, side = face & 1;
+  if (a == 0) return side * fd + t;
+  const int i = t / L, k = t - i * L;
+  return 2 * fd + i * (2 * (P.d - 1) * L) + (a - 1) * 2 * L + side * L + k;
+}
+__device__ __forceinline__ int rhs_nat(const LeafParams& P, int s) {
+  if (!P.colperm) return s;
+  const int fd = P.d == 3 ? P.q * P.q : P.q, L = P.d == 3 ? P.q : 1;
+  if (s < 2 * fd) return s;
+  const int s2 = s - 2 * fd, blk = 2 * (P.d - 1) * L;
+  const int i = s2 / blk, r = s2 - i * blk;
+  const int a = 1 + r / (2 * L), side = (r / L) & 1, k = r % L;
+  return (2 * a + side) * fd + i * L + k;
+}
+// interior rows of the axis-a line of face DOF t: base + i * stride, i < q
+__device__ __forceinline__ void line_rows(const LeafParams& P, int a, int t, int& base, int& stride) {
+  const int q = P.q;
+  if (P.d == 3) {
+    if (a == 0) { base = t; stride = q * q; }
+    else if (a == 1) { base = (t / q) * q * q + t % q; stride = q; }
+    else { base = t * q; stride = 1; }
+  } else {
+    if (a == 0) { base = t; stride = q; }
+    else { base = t * q; stride = 1; }
+  }
+}
+
+// rhs_tab[g] = number of leading RHS columns that contain every column with a
+// nonzero of P A_ib above row 16 g (P = the LU's row interchanges).  Computed
+// once per leaf after the factorization; the forward-solve GEMMs clip N to it.
+__device__ void rhs_profile(const LeafParams& P, Ctx& c) {
+  const int n_pad = c.n_piv, m = P.m, m_pad = P.m_pad;
+  const int groups = n_pad / 16 + 1;
+  int* perm = reinterpret_cast<int*>(c.smem);
+  int* pinv = perm + n_pad;
+  int* g = pinv + n_pad;
+  __syncthreads();
+  if (2 * n_pad + m_pad > 2 * c.smem_doubles) {  // no room: no skipping
+    for (int e = threadIdx.x; e < groups; e += NT) c.rhs_tab[e] = m_pad;
+    __syncthreads();
+    return;
+  }
+  for (int r = threadIdx.x; r < n_pad; r += NT) { perm[r] = r; pinv[r] = c.piv[r]; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < n_pad; ++j) {
+      const int pj = pinv[j];
+      if (pj != j) { const int t = perm[j]; perm[j] = perm[pj]; perm[pj] = t; }
+    }
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < n_pad; r += NT) pinv[perm[r]] = r;
+  __syncthreads();
+  const int fd = P.d == 3 ? P.q * P.q : P.q;
+  for (int sc = threadIdx.x; sc < m_pad; sc += NT) {
+    int f = 0x7fffffff;
+    if (sc < m) {
+      const int b = rhs_nat(P, sc), face = b / fd;
+      int base, stride;
+      line_rows(P, face >> 1, b - face * fd, base, stride);
+      for (int i = 0; i < P.q; ++i) f = min(f, pinv[base + i * stride]);
+    }
+    g[sc] = f;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // suffix minimum: g non-decreasing
+    int run = 0x7fffffff;
+    for (int sc = m_pad - 1; sc >= 0; --sc) { run = min(run, g[sc]); g[sc] = run; }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < groups; e += NT) {
+    const int R = 16 * e;
+    int lo = 0, hi = m_pad;  // first column with g >= R
+    while (lo < hi) { const int mid = (lo + hi) >> 1; if (g[mid] < R) lo = mid + 1; else hi = mid; }
+    c.rhs_tab[e] = lo;
+  }
+  __syncthreads();
 }
 
 // A[row r][col with multi-index J]; coefficient pointer layout (ncoef, n):
@@ -1070,7 +1164,8 @@ __device__ void assemble(const LeafParams& P, double* M, int leaf, double* smem)
           int a = 0;
           for (int k = 0; k < d; ++k)
             if (J[k] != I[k]) a = k;
-          row[P.n_pad + boundary_index(P, a, J[a] == P.p - 1 ? 1 : 0, I)] = op_entry(P, cf, r, I, J);
+          row[P.n_pad + rhs_col(P, boundary_index(P, a, J[a] == P.p - 1 ? 1 : 0, I))] =
+              op_entry(P, cf, r, I, J);
         }
       }
       if (P.mode == MODE_REDUCE && lane == 0) {
@@ -1195,18 +1290,21 @@ __device__ bool dtn_lines_stream(const LeafParams& P, Ctx& c, const double* M, i
     cp_async_commit();
   };
   auto put = [&](int b, int col0, int b_lo, int b_hi, const double* e2, double v0, double v1, bool neg) {
-    // T[b, col0 + {0,1}] = a_bb + (neg ? -v : v)
+    // T[b, nat(col0 + {0,1})] = a_bb + (neg ? -v : v); col0 is a slot column
     double o[2] = {v0, v1};
+    int nat[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
-      const int col = col0 + u;
+      nat[u] = rhs_nat(P, col0 + u);
+      const int col = nat[u];
       const double abb = col == b_lo ? e2[0] : (col == b_hi ? e2[1] : 0.0);
       o[u] = neg ? abb - o[u] : abb + o[u];
     }
-    if (col0 + 1 < m) {
-      *reinterpret_cast<double2*>(T + (size_t)b * m + col0) = make_double2(o[0], o[1]);
-    } else if (col0 < m) {
-      T[(size_t)b * m + col0] = o[0];
+    if (col0 + 1 < m && nat[1] == nat[0] + 1 && (nat[0] & 1) == 0) {
+      *reinterpret_cast<double2*>(T + (size_t)b * m + nat[0]) = make_double2(o[0], o[1]);
+    } else {
+      if (col0 < m) T[(size_t)b * m + nat[0]] = o[0];
+      if (col0 + 1 < m) T[(size_t)b * m + nat[1]] = o[1];
     }
   };
   for (int c0 = 0; c0 < m; c0 += CW) {
@@ -1275,12 +1373,13 @@ __device__ void dtn_lines(const LeafParams& P, const double* M, int ld, double* 
   constexpr int U = 2;  // independent (line, column) items per thread iteration
   for (int e0 = threadIdx.x; e0 < lines * m; e0 += NT * U) {
     double lo[U], hi[U];
-    int a_[U], t_[U], col_[U], base_[U], stride_[U];
+    int a_[U], t_[U], col_[U], xcol_[U], base_[U], stride_[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int e = e0 + u * NT;
       const int line = (e < lines * m) ? e / m : 0;
       col_[u] = (e < lines * m) ? e - line * m : 0;
+      xcol_[u] = rhs_col(P, col_[u]);
       a_[u] = line / fd;
       t_[u] = line - a_[u] * fd;
       const int a = a_[u], t = t_[u];
@@ -1297,7 +1396,7 @@ __device__ void dtn_lines(const LeafParams& P, const double* M, int ld, double* 
     for (int i = 0; i < q; ++i) {
       double x[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) x[u] = X[(size_t)(base_[u] + i * stride_[u]) * ld + col_[u]];
+      for (int u = 0; u < U; ++u) x[u] = X[(size_t)(base_[u] + i * stride_[u]) * ld + xcol_[u]];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         lo[u] += s_w[a_[u]][0][i] * x[u];
@@ -1341,7 +1440,8 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
   c.n_real = P.n;
   c.NR = P.NR;
   c.wb = P.wb;
-  c.piv = P.piv + (size_t)slot * P.n_pad;
+  c.piv = P.piv + (size_t)slot * P.piv_stride;
+  c.rhs_tab = c.piv + P.n_pad;
   c.scratch = P.scratch + (size_t)slot * 2 * P.n_pad * TRI_BLOCK;
   c.smem = smem;
   c.smem_doubles = P.smem_doubles;
@@ -1363,7 +1463,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     __syncthreads();
     if (prof && threadIdx.x == 0) { prof[22] += clock64() - t0; prof[9] += 1; }
     for (int k = 0; k < ((P.debug & 1) ? 0 : n_ops); ++k) {
-      const Op op = ops[k];
+      Op op = ops[k];
       if (prof) t0 = clock64();
       switch (op.kind) {
         case OP_SMALL: lu_small(c, op.a, op.b); break;
@@ -1371,17 +1471,19 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
         case OP_INV_LOWER: invert_unit_lower(c, op.a, op.b); break;
         case OP_INV_UPPER: invert_upper(c, op.a, op.b); break;
         case OP_COPY_ABB: copy_abb(P, c, op.a); break;
+        case OP_RHS_PROFILE: rhs_profile(P, c); break;
         default: {
           const bool sub = (op.kind == OP_GEMM_SUB || op.kind == OP_GEMM_SUB_ABI);
           const int a_src = op.kind == OP_GEMM_SET ? 1 : (op.kind == OP_GEMM_SUB_ABI ? 2 : 0);
           const int b_src = op.kind == OP_GEMM_SET_Q ? 1 : 0;
-          gemm(c, sub, a_src, op.ar, op.ac, b_src, op.br, op.bc, op.cr, op.cc, op.Mdim, op.Ndim,
-               op.Kdim);
+          const int N = op.dyn ? min(op.Ndim, c.rhs_tab[op.dyn >> 4]) : op.Ndim;
+          gemm(c, sub, a_src, op.ar, op.ac, b_src, op.br, op.bc, op.cr, op.cc, op.Mdim, N, op.Kdim);
+          op.Ndim = N;  // profile counters below count the work done
         }
       }
       if (prof && threadIdx.x == 0) {
         const long long dt = clock64() - t0;
-        prof[op.kind] += dt;
+        prof[op.kind == OP_RHS_PROFILE ? 24 : op.kind] += dt;
         if (op.kind == OP_GEMM_SUB || op.kind == OP_GEMM_SET || op.kind == OP_GEMM_SET_Q ||
             op.kind == OP_GEMM_SUB_ABI) {
           const int bucket = op.Ndim <= 64 ? 0 : (op.Ndim <= 256 ? 1 : 2);
@@ -1464,11 +1566,13 @@ struct ProgramBuilder {
     Op o{}; o.kind = OP_SWAP; o.a = j0; o.b = cnt; o.c = lo; o.d = hi; ops.push_back(o);
   }
   void inv(int kind, int r0, int h) { Op o{}; o.kind = kind; o.a = r0; o.b = h; ops.push_back(o); }
-  void gemm(int kind, int ar, int ac, int br, int bc, int cr, int cc, int M, int N, int K) {
+  void gemm(int kind, int ar, int ac, int br, int bc, int cr, int cc, int M, int N, int K,
+            int dyn = 0) {
     if (M <= 0 || N <= 0 || K <= 0) return;
     Op o{}; o.kind = kind; o.ar = ar; o.ac = ac; o.br = br; o.bc = bc; o.cr = cr; o.cc = cc;
-    o.Mdim = M; o.Ndim = N; o.Kdim = K; ops.push_back(o);
+    o.Mdim = M; o.Ndim = N; o.Kdim = K; o.dyn = dyn; ops.push_back(o);
   }
+  bool dyn_rhs = false;  // forward solve against the slab-ordered A_ib: clip N by rhs_tab
   void inv_cached(int kind, int r0, int h) {
     std::vector<std::pair<int, int>>& own = owner[kind == OP_INV_UPPER];
     if (own.empty()) own.assign(n_pad / 16 + 1, {-1, -1});
@@ -1482,12 +1586,12 @@ struct ProgramBuilder {
     if (hi <= lo) return;
     if (h <= TRI_BLOCK) {
       inv_cached(OP_INV_LOWER, r0, h);
-      gemm(OP_GEMM_SET, r0, 0, r0, lo, r0, lo, h, hi - lo, h);
+      gemm(OP_GEMM_SET, r0, 0, r0, lo, r0, lo, h, hi - lo, h, dyn_rhs ? r0 + h : 0);
       return;
     }
     const int h1 = split16_host(h);
     trsm_lower(r0, h1, lo, hi);
-    gemm(OP_GEMM_SUB, r0 + h1, r0, r0, lo, r0 + h1, lo, h - h1, hi - lo, h1);
+    gemm(OP_GEMM_SUB, r0 + h1, r0, r0, lo, r0 + h1, lo, h - h1, hi - lo, h1, dyn_rhs ? r0 + h1 : 0);
     trsm_lower(r0 + h1, h - h1, lo, hi);
   }
   void trsm_upper(int r0, int h, int lo, int hi) {
@@ -1587,6 +1691,7 @@ struct hps_plan_s {
   double* work = nullptr;
   size_t work_doubles = 0;
   int* piv = nullptr;
+  int colperm[4] = {0, 0, 0, 0};
   double* scratch = nullptr;
   int ws_slots = 0;
   // unrolled LU programs per mode (device copies)
@@ -1661,9 +1766,11 @@ static size_t slot_doubles(const hps_plan_s* P, int mode) {
   return (size_t)rows_alloc(P, mode) * NC;
 }
 
+static int piv_stride(const hps_plan_s* P) { return P->n_pad + P->n_pad / 16 + 16; }
+
 static int ensure_workspace(hps_plan_s* P, int mode, int want_slots) {
   const size_t per = slot_doubles(P, mode);
-  size_t slot_bytes = per * 8 + (size_t)P->n_pad * 4 + (size_t)2 * P->n_pad * TRI_BLOCK * 8;
+  size_t slot_bytes = per * 8 + (size_t)piv_stride(P) * 4 + (size_t)2 * P->n_pad * TRI_BLOCK * 8;
   int slots = want_slots;
   if (P->budget > 0) {
     const size_t fit = P->budget / slot_bytes;
@@ -1708,7 +1815,7 @@ static int ensure_workspace(hps_plan_s* P, int mode, int want_slots) {
   if (P->scratch) cudaFree(P->scratch);
   P->work = nullptr; P->piv = nullptr; P->scratch = nullptr;
   CK(cudaMalloc(&P->work, per * (size_t)slots * 8));
-  CK(cudaMalloc(&P->piv, (size_t)P->n_pad * slots * 4));
+  CK(cudaMalloc(&P->piv, (size_t)piv_stride(P) * slots * 4));
   CK(cudaMalloc(&P->scratch, (size_t)2 * P->n_pad * TRI_BLOCK * slots * 8));
   P->work_doubles = per * (size_t)slots;
   P->ws_slots = slots;
@@ -1729,8 +1836,17 @@ static int ensure_program(hps_plan_s* P, int mode) {
   if (leg_op)  // A_ib = R_b Q
     b.gemm(OP_GEMM_SET_Q, 0, col_rb, 0, 0, 0, P->n_pad, P->n_pad, P->m_pad, P->nb_pad);
   b.lu(0, P->n_pad, NR);
+  const char* dbg = getenv("HPS_DEBUG");
+  P->colperm[mode] = (mode == MODE_DTN && !P->legendre && !(dbg && (atoi(dbg) & 4))) ? 1 : 0;
+  if (P->colperm[mode]) {
+    Op o{};
+    o.kind = OP_RHS_PROFILE;
+    b.ops.push_back(o);
+    b.dyn_rhs = true;
+  }
   b.swaps(0, P->n_pad, P->n_pad, NW);
   b.trsm_lower(0, P->n_pad, P->n_pad, NW);
+  b.dyn_rhs = false;
   b.trsm_upper(0, P->n_pad, P->n_pad, NW);
   if (leg_op && mode == MODE_DTN) {  // T = a_bb - a_bi X in the (now free) R_b region
     Op o{};
@@ -1769,6 +1885,8 @@ static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, c
   L.n_leaves = n_leaves;
   L.slot_stride = slot_doubles(P, mode);
   L.work = P->work; L.piv = P->piv; L.scratch = P->scratch;
+  L.piv_stride = piv_stride(P);
+  L.colperm = P->colperm[mode];
   L.D1 = P->D1; L.D2 = P->D2; L.a_bi = P->a_bi; L.a_bb = P->a_bb;
   L.prof = P->prof;
   L.leaf_counter = P->leaf_counter;

@@ -222,8 +222,30 @@ def dtn_flops(n: int, m: int) -> float:
     return 2.0 / 3.0 * n ** 3 + 2.0 * n * n * m + 2.0 * n * m * m
 
 
-def dtn_flops_executed(n: int, m: int, q: int) -> float:
-    """FLOPs of the algorithm the engine runs: getrf(n) + two triangular solves
-    with m right-hand sides + the line-sparse A_bi product (q = p - 2 nodes
-    per boundary row)."""
-    return 2.0 / 3.0 * n ** 3 + 2.0 * n * n * m + 2.0 * q * m * m
+def forward_prefix_rows(q: int, d: int = 3) -> np.ndarray:
+    """First structurally nonzero interior row of every A_ib column (drop mode,
+    natural i-major interior numbering, no pivoting): the zero prefix the
+    forward solve skips.  Axis-0 faces' lines start in slab 0; the lines of the
+    other faces start in the slab of their first tangential index."""
+    if d == 3:
+        t = np.arange(q * q)
+        i, k = t // q, t % q
+        f_x = t
+        f_y = i * q * q + k          # t = i q + k, rows i q^2 + j q + k
+        f_z = i * q * q + k * q      # t = i q + j, rows i q^2 + j q + k
+    else:
+        t = np.arange(q)
+        f_x, f_y, f_z = t, t * q, np.zeros(0, dtype=int)
+    return np.concatenate([f_x, f_x, f_y, f_y, f_z, f_z])
+
+
+def dtn_flops_executed(n: int, m: int, q: int, d: int = 3, skip_prefix: bool = True) -> float:
+    """FLOPs of the algorithm the engine runs: getrf(n) + forward solve of the
+    m right-hand sides (each from its first nonzero row on: sum (n - f_c)^2)
+    + backward solve (n^2 m) + the line-sparse A_bi product (q = p - 2 nodes
+    per boundary row).  skip_prefix=False: dense forward solve (legendre)."""
+    fwd = float(n) * n * m
+    if skip_prefix:
+        f = forward_prefix_rows(q, d).astype(float)
+        fwd = float(((n - f) ** 2).sum())
+    return 2.0 / 3.0 * n ** 3 + fwd + float(n) * n * m + 2.0 * q * m * m

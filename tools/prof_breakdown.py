@@ -21,21 +21,21 @@ def run():
     else:
         eng.reduce_load(coeffs, f)
 run(); torch.cuda.synchronize()
-cnt = torch.zeros(eng.slots * 24, dtype=torch.int64, device="cuda")
+cnt = torch.zeros(eng.slots * 26, dtype=torch.int64, device="cuda")
 eng.lib.hps_plan_set_profile(eng.plan, ctypes.c_void_p(cnt.data_ptr()))
 e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
 e0.record(); run(); e1.record(); torch.cuda.synchronize()
 eng.lib.hps_plan_set_profile(eng.plan, ctypes.c_void_p(0))
 ms = e0.elapsed_time(e1)
-c = cnt.view(eng.slots, 24).cpu().numpy().astype(float)
+c = cnt.view(eng.slots, 26).cpu().numpy().astype(float)
 names = ["small-panel", "swaps", "inv-lower", "inv-upper", "gemm-sub", "gemm-set", "gemm-set-Q", "gemm-sub-abi", "copy-abb"]
-tot = c[:, :9].sum() + c[:, 22].sum() + c[:, 23].sum()
+tot = c[:, :9].sum() + c[:, 22].sum() + c[:, 23].sum() + c[:, 24].sum()
 leaves = c[:, 9].sum()
 print(f"p={a.p} leaves={a.leaves} mode={a.mode} kernel {ms:.1f} ms, {a.leaves/ms*1e3:.1f} leaves/s, "
       f"{a.leaves*dtn_flops_executed(eng.n, eng.m, a.p-2)/ms/1e9:.2f} TFLOP/s executed, "
       f"{a.leaves*dtn_flops(eng.n, eng.m)/ms/1e9:.2f} reference-equivalent")
 clk = 1.965e9
-for i, nm in list(enumerate(names)) + [(22, "assemble"), (23, "output")]:
+for i, nm in list(enumerate(names)) + [(24, "rhs-profile"), (22, "assemble"), (23, "output")]:
     if c[:, i].sum() == 0:
         continue
     print(f"  {nm:12s} {100*c[:, i].sum()/tot:6.2f}%   {c[:, i].sum()/leaves/clk*1e3:8.2f} ms/leaf")

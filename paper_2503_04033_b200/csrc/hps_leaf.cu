@@ -122,7 +122,7 @@ struct LeafParams {
   int done_chunk;            // leaves per output chunk
   int smem_doubles;          // dynamic shared memory of the launch, in doubles
   int debug;                 // diagnostics (env HPS_DEBUG): 1 skip the LU program, 2 old DtN output,
-                             // 4 natural A_ib column order without zero-prefix skipping
+                             // 4 natural A_ib column order without zero-prefix skipping, 8 one CTA per SM
 };
 
 constexpr int PROF_SLOTS = 26;  // 0..8 op kinds, 9 leaves, 10-14 panel steps, 15 interchanges,
@@ -501,6 +501,12 @@ __device__ void apply_swaps(const Ctx& c, int j0, int cnt, int c_lo, int c_hi) {
 // ---------------------------------------------------------------------------
 
 __shared__ int s_swp_dst[16], s_swp_src[16], s_swp_cnt;
+// pivot search state, parity-buffered by column: per-warp best |a| / row / row values,
+// and row j's values at the start of step j
+__shared__ double s_pv[2][NT / 32];
+__shared__ int s_pi[2][NT / 32];
+__shared__ double s_cand[2][NT / 32][8];
+__shared__ double s_rowj[2][8];
 
 // Lane-sum of p[j] over the warp; on return lane holds the full sum for column
 // jout (= the high bits of lane after log2(WB) halving steps).
@@ -624,18 +630,29 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
   }
   __syncthreads();
   PANEL_TICK(11)
-  // 3. partial pivoting on the block.  The search for column j+1 is fused into
-  //    the rank-1 update of column j (each thread scans the rows it just
-  //    updated), thread 0 finalises the pivot and swaps: two barriers per column.
+  // 3. partial pivoting on the block, one barrier per column.  The search for
+  //    column j+1 is fused into the rank-1 update of column j (each thread scans
+  //    the rows it just updated).  Before the barrier each warp stashes its
+  //    candidate row and thread 0 (owner of row j+1) stashes row j+1, so after
+  //    it every thread picks the pivot itself and the interchange happens in
+  //    flight: row j takes the pivot row, the pivot row's owner takes old row j.
   {
-    auto warp_argmax = [&](double best, int bidx) {
+    auto warp_argmax = [&](double best, int bidx, int par) {
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) {
         const double ov = __shfl_xor_sync(0xffffffffu, best, off);
         const int oi = __shfl_xor_sync(0xffffffffu, bidx, off);
         if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
       }
-      if (lane == 0) { s_redv[warp] = best; s_redi[warp] = bidx; }
+      __syncwarp();  // the winner row's owner lane wrote it before the shuffles
+      if (lane == 0) {
+        s_pv[par][warp] = best;
+        s_pi[par][warp] = bidx;
+        if (bidx != 0x7fffffff) {
+#pragma unroll
+          for (int t = 0; t < WB; ++t) s_cand[par][warp][t] = S[t * NS + bidx];
+        }
+      }
     };
     {
       double best = -1.0;
@@ -644,53 +661,89 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
         const double v = fabs(S[r]);
         if (v > best) { best = v; bidx = r; }
       }
-      warp_argmax(best, bidx);
+      warp_argmax(best, bidx, 0);
+      if (tid == 0) {
+#pragma unroll
+        for (int t = 0; t < WB; ++t) s_rowj[0][t] = S[t * NS];
+      }
     }
     __syncthreads();
-    for (int j = 0; j < WB; ++j) {
+#pragma unroll
+    for (int j = 0; j < WB; ++j) {  // unrolled: register arrays indexed by j
+      const int par = j & 1;
+      double bv = s_pv[par][0];
+      int bi = s_pi[par][0], bw = 0;
+#pragma unroll
+      for (int q = 1; q < NT / 32; ++q) {
+        const double v = s_pv[par][q];
+        const int i = s_pi[par][q];
+        if (v > bv || (v == bv && i < bi)) { bv = v; bi = i; bw = q; }
+      }
+      if (bi == 0x7fffffff) bi = j;
+      double urow[WB], rowj[WB];
+#pragma unroll
+      for (int t = 0; t < WB; ++t) {
+        rowj[t] = s_rowj[par][t];
+        urow[t] = (bi == j) ? rowj[t] : s_cand[par][bw][t];
+      }
       if (tid == 0) {
-        double bv = s_redv[0];
-        int bi = s_redi[0];
-        for (int q = 1; q < NT / 32; ++q) {
-          if (s_redv[q] > bv || (s_redv[q] == bv && s_redi[q] < bi)) { bv = s_redv[q]; bi = s_redi[q]; }
-        }
-        if (bi == 0x7fffffff) bi = j;
         c.piv[b0 + j] = b0 + bi;
         if (c.prof && bi != j) c.prof[15] += 1;
-        if (bi != j) {
-#pragma unroll
-          for (int t = 0; t < WB; ++t) {
-            const double x = S[t * NS + j];
-            S[t * NS + j] = S[t * NS + bi];
-            S[t * NS + bi] = x;
-          }
-        }
         if (b0 + j < c.n_real) {
-          const double ap = fabs(S[j * NS + j]);
+          const double ap = fabs(urow[j]);
           s_pmin = fmin(s_pmin, ap);
           s_pmax = fmax(s_pmax, ap);
         }
-      }
-      __syncthreads();
-      const double pivot = S[j * NS + j];
-      const double inv = (pivot != 0.0) ? 1.0 / pivot : 1.0;
-      double urow[WB];
 #pragma unroll
-      for (int t = 0; t < WB; ++t) urow[t] = S[t * NS + j];
+        for (int t = 0; t < WB; ++t) S[t * NS + j] = urow[t];
+      }
+      const double pivot = urow[j];
+      const double inv = (pivot != 0.0) ? 1.0 / pivot : 1.0;
       double best = -1.0;
       int bidx = 0x7fffffff;
-      for (int r = j + 1 + tid; r < n_cand; r += NT) {
-        const double l = S[j * NS + r] * inv;
-        S[j * NS + r] = l;
+      constexpr int RU = WB >= 8 ? 2 : 4;  // rows in flight per thread
+      for (int r0 = j + 1 + tid; r0 < n_cand; r0 += NT * RU) {
+        double v[RU][WB];
 #pragma unroll
-        for (int t = 0; t < WB; ++t)
-          if (t > j) S[t * NS + r] -= l * urow[t];
-        if (j + 1 < WB) {
-          const double v = fabs(S[(j + 1) * NS + r]);
-          if (v > best) { best = v; bidx = r; }
+        for (int u = 0; u < RU; ++u) {
+          const int r = r0 + u * NT;
+#pragma unroll
+          for (int t = 0; t < WB; ++t)
+            v[u][t] = (r >= n_cand || t < j) ? 0.0 : (r == bi ? rowj[t] : S[t * NS + r]);
+        }
+#pragma unroll
+        for (int u = 0; u < RU; ++u) {
+          const int r = r0 + u * NT;
+          if (r < n_cand) {
+            const double l = v[u][j] * inv;
+            v[u][j] = l;
+#pragma unroll
+            for (int t = 0; t < WB; ++t)
+              if (t > j) v[u][t] -= l * urow[t];
+#pragma unroll
+            for (int t = 0; t < WB; ++t) {
+              if (t >= j) S[t * NS + r] = v[u][t];
+              else if (r == bi) S[t * NS + r] = rowj[t];
+            }
+            if (j + 1 < WB) {
+              const double a = fabs(v[u][j + 1]);
+              if (a > best) { best = a; bidx = r; }
+              if (r == j + 1) {  // thread 0: stash row j+1 for the next step
+#pragma unroll
+                for (int t = 0; t < WB; ++t)
+                  s_rowj[par ^ 1][t] = (t >= j) ? v[u][t] : (r == bi ? rowj[t] : S[t * NS + r]);
+              }
+            }
+          }
         }
       }
-      if (j + 1 < WB) warp_argmax(best, bidx);
+      if (j + 1 < WB) {
+        if (j + 1 >= n_cand && tid == 0) {
+#pragma unroll
+          for (int t = 0; t < WB; ++t) s_rowj[par ^ 1][t] = 0.0;
+        }
+        warp_argmax(best, bidx, par ^ 1);
+      }
       __syncthreads();
     }
   }
@@ -1868,6 +1921,10 @@ static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, c
   CK(cudaSetDevice(P->device));
   if (ensure_program(P, mode) != 0) return -1;
   int want = P->slots;
+  {
+    const char* dbg = getenv("HPS_DEBUG");
+    if (dbg && (atoi(dbg) & 8) && want > P->sms) want = P->sms;  // diagnostics: one CTA per SM
+  }
   if (want > n_leaves) want = n_leaves;
   const int slots = ensure_workspace(P, mode, want);
   if (slots < 0) return -1;

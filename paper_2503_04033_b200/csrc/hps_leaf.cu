@@ -224,7 +224,36 @@ struct TmaMaps {
   CUtensorMap c_red;      // box {16, 8, 1} over [slots][NR][NC]: epilogue reduce-add
   CUtensorMap a_abi;      // legendre: box {A_STRIDE, TM, 1} over the plan's a_bi [m_pad][n_pad]
   CUtensorMap b_q;        // legendre: box {B_STRIDE, KC, 1} over the plan's Q [nb_pad][m_pad]
+  CUtensorMap a_work_n;   // narrow tiles: box {12, 256, 1} over [slots][NR][NC]
+  CUtensorMap b_work_n;   // narrow tiles: box {36, 8, 1}
 };
+
+// GEMM tile configurations.  Wide: 64 x 128 tiles, 2 x 4 warps of 32 x 32, k-chunk 16
+// (A box 20 / B box 132 doubles per row).  Narrow: 256 x 32 tiles, 8 x 1 warps,
+// k-chunk 8 (A box 12 / B box 36: row strides = +-8 banks mod 32, conflict-free
+// fragments) for the tall rank-32/64 updates at the bottom of the LU recursion,
+// which use a quarter / half of a wide tile.  Both share the stage ring, the
+// mbarriers and the per-warp epilogue ring.
+struct GemmWide {
+  static constexpr int TM_ = TM, TN_ = TN, KC_ = KC, AS = A_STRIDE, BS = B_STRIDE, WN_ = WN;
+  static constexpr bool SWZ = !A_PAD;
+};
+struct GemmNarrow {
+  static constexpr int TM_ = 256, TN_ = 32, KC_ = 8, AS = 12, BS = 36, WN_ = 1;
+  static constexpr bool SWZ = false;
+};
+template <class G>
+struct GemmShape {
+  static constexpr int WM_ = (NT / 32) / G::WN_;
+  static constexpr int MI_ = G::TM_ / WM_ / 8;
+  static constexpr int NJ_ = G::TN_ / G::WN_ / 8;
+  static constexpr int SA = G::TM_ * G::AS, SB = G::KC_ * G::BS;
+  static constexpr int SDBL = G::SWZ ? ((SA + SB + 127) / 128) * 128 : SA + SB;
+  static constexpr unsigned BYTES = (unsigned)((SA + SB) * 8);
+  static_assert(MI_ == 4 && NJ_ == 4, "32 x 32 warp tiles");
+};
+constexpr int NARROW_SMEM_DBL = STAGES * GemmShape<GemmNarrow>::SDBL + (NT / 32) * EPI_DBL;
+static_assert(NARROW_SMEM_DBL * 8 <= GEMM_SMEM_BYTES, "narrow stages fit the wide GEMM smem");
 
 struct Ctx {
   double* M;
@@ -253,9 +282,14 @@ struct Ctx {
 
 // Operand sources: a_src 0 = slot, 1 = slot scratch (triangular inverse),
 // 2 = plan a_bi; b_src 0 = slot, 1 = plan Q (legendre face injection).
-__device__ __forceinline__ void gemm(Ctx& c, const bool sub, const int a_src, int ar, int ac,
-                                     const int b_src, int br, int bc, int cr, int cc, int M, int N,
-                                     int K) {
+template <class G>
+__device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, int ar, int ac,
+                                       const int b_src, int br, int bc, int cr, int cc, int M, int N,
+                                       int K) {
+  using S = GemmShape<G>;
+  constexpr int TM = G::TM_, TN = G::TN_, KC = G::KC_, A_STRIDE = G::AS, B_STRIDE = G::BS;
+  constexpr int WN = G::WN_, MI = S::MI_, NJ = S::NJ_, STAGE_A = S::SA, STAGE_DBL = S::SDBL;
+  constexpr bool narrow = (TN == 32);
   if (M <= 0 || N <= 0 || K <= 0) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wm = warp / WN, wn = warp % WN;
@@ -265,9 +299,10 @@ __device__ __forceinline__ void gemm(Ctx& c, const bool sub, const int a_src, in
   const int kchunks = K / KC;
   const int total = tiles * kchunks;
   double* smem = c.smem;
-  const CUtensorMap* mapA =
-      a_src == 0 ? &c.maps->a_work : (a_src == 1 ? &c.maps->a_scratch : &c.maps->a_abi);
-  const CUtensorMap* mapB = b_src == 0 ? &c.maps->b_work : &c.maps->b_q;
+  const CUtensorMap* mapA = narrow ? &c.maps->a_work_n
+                           : (a_src == 0 ? &c.maps->a_work
+                                         : (a_src == 1 ? &c.maps->a_scratch : &c.maps->a_abi));
+  const CUtensorMap* mapB = narrow ? &c.maps->b_work_n : (b_src == 0 ? &c.maps->b_work : &c.maps->b_q);
   const int a_slot = a_src == 2 ? 0 : c.slot, b_slot = b_src == 1 ? 0 : c.slot;
   double* C = c.M + (size_t)cr * c.ld + cc;
 
@@ -285,12 +320,16 @@ __device__ __forceinline__ void gemm(Ctx& c, const bool sub, const int a_src, in
     const int tm = p_tile / tiles_n, tn = p_tile - tm * tiles_n;
     double* sa = smem + s * STAGE_DBL;
     double* sb = sa + STAGE_A;
-    mbar_expect_tx(&c.full[s], STAGE_BYTES);
+    mbar_expect_tx(&c.full[s], S::BYTES);
     tma_load_3d(sa, mapA, ac + p_kc * KC, ar + tm * TM, a_slot, &c.full[s]);
     tma_load_3d(sb, mapB, bc + tn * TN, br + p_kc * KC, b_slot, &c.full[s]);
-    if (sub && p_kc == 0) {
-      for (int r = 0; r < TM; r += KC)
-        tma_prefetch_3d(&c.maps->b_work, cc + tn * TN, cr + tm * TM + r, c.slot);
+    if (sub && p_kc == 0) {  // C tile into L2 ahead of the reduce-add epilogue
+      if (narrow) {
+        for (int r = 0; r < TM; r += 8) tma_prefetch_3d(&c.maps->b_work_n, cc + tn * TN, cr + tm * TM + r, c.slot);
+      } else {
+        for (int r = 0; r < TM; r += KC)
+          tma_prefetch_3d(&c.maps->b_work, cc + tn * TN, cr + tm * TM + r, c.slot);
+      }
     }
     ++p_it;
     if (++p_kc == kchunks) { p_kc = 0; ++p_tile; }
@@ -330,7 +369,7 @@ __device__ __forceinline__ void gemm(Ctx& c, const bool sub, const int a_src, in
 #pragma unroll
         for (int i = 0; i < MI; ++i) {
           const int row = wm * (MI * 8) + i * 8 + lr, k = ks + lc;
-          if (A_PAD) {
+          if (!G::SWZ) {
             af[i] = sa[row * A_STRIDE + k];
           } else {
             // 128B swizzle: 16-byte chunk index ^= row % 8  (row % 8 == lr here)
@@ -338,7 +377,7 @@ __device__ __forceinline__ void gemm(Ctx& c, const bool sub, const int a_src, in
           }
         }
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) bf[j] = sb[(ks + lc) * B_STRIDE + wn * 32 + j * 8 + lr];
+        for (int j = 0; j < NJ; ++j) bf[j] = sb[(ks + lc) * B_STRIDE + wn * (NJ * 8) + j * 8 + lr];
 #pragma unroll
         for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -376,7 +415,7 @@ __device__ __forceinline__ void gemm(Ctx& c, const bool sub, const int a_src, in
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              const int col0 = tn * TN + wn * 32;
+              const int col0 = tn * TN + wn * (NJ * 8);
               if (col0 < N) tma_reduce_add_3d(&c.maps->c_red, cc + col0, cr + row0, c.slot, buf);
               if (col0 + 16 < N) tma_reduce_add_3d(&c.maps->c_red, cc + col0 + 16, cr + row0, c.slot, buf + 128);
               bulk_commit();
@@ -392,7 +431,7 @@ __device__ __forceinline__ void gemm(Ctx& c, const bool sub, const int a_src, in
         const int row = tm * TM + wm * (MI * 8) + i * 8 + lr;
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
-          const int col = tn * TN + wn * 32 + j * 8 + 2 * lc;
+          const int col = tn * TN + wn * (NJ * 8) + j * 8 + 2 * lc;
           if (row < M && col < N) {
             double2* cp = reinterpret_cast<double2*>(C + (size_t)row * c.ld + col);
             double2 v;
@@ -417,6 +456,16 @@ __device__ __forceinline__ void gemm(Ctx& c, const bool sub, const int a_src, in
     fence_proxy_async_global();
   }
   __syncthreads();
+}
+
+__device__ __forceinline__ void gemm(Ctx& c, const bool sub, const int a_src, int ar, int ac,
+                                     const int b_src, int br, int bc, int cr, int cc, int M, int N,
+                                     int K) {
+  // tall, narrow slot-only updates (the rank-32/64 steps of the LU recursion) on 256 x 32 tiles
+  if (sub && a_src == 0 && b_src == 0 && N <= 64 && M >= 256 && K % 8 == 0)
+    gemm_t<GemmNarrow>(c, sub, a_src, ar, ac, b_src, br, bc, cr, cc, M, N, K);
+  else
+    gemm_t<GemmWide>(c, sub, a_src, ar, ac, b_src, br, bc, cr, cc, M, N, K);
 }
 
 __shared__ double s_pmin, s_pmax;
@@ -1308,8 +1357,9 @@ __device__ bool dtn_lines_stream(const LeafParams& P, Ctx& c, const double* M, i
   __shared__ double s_e[3][2][2];
   const int q = P.q, p = P.p, d = P.d, m = P.m;
   const int S = (d == 3) ? q * q : q;
+  const int tab_d = P.colperm ? (m + 1) / 2 : 0;  // slot column -> DtN column table (ints)
   int CW = 8;
-  while (CW >= 2 && (2 + LINE_NBUF) * S * CW > c.smem_doubles) CW >>= 1;
+  while (CW >= 2 && (2 + LINE_NBUF) * S * CW + tab_d > c.smem_doubles) CW >>= 1;
   if (CW < 2 || q > 32) return false;
   __syncthreads();  // smem is free (previous op finished with it)
   for (int e = threadIdx.x; e < d * 2 * q; e += NT) {
@@ -1323,6 +1373,9 @@ __device__ bool dtn_lines_stream(const LeafParams& P, Ctx& c, const double* M, i
   }
   double* acc = c.smem;              // [2][S*CW]: axis-0 lines, low / high face
   double* ring = c.smem + 2 * S * CW;  // [NBUF][S*CW]
+  int* nat_tab = reinterpret_cast<int*>(ring + LINE_NBUF * S * CW);
+  if (P.colperm)
+    for (int e = threadIdx.x; e < m; e += NT) nat_tab[e] = rhs_nat(P, e);
   const double* X = M + P.n_pad;
   const int fd = S;
   const int SC = S * CW;
@@ -1348,7 +1401,7 @@ __device__ bool dtn_lines_stream(const LeafParams& P, Ctx& c, const double* M, i
     int nat[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
-      nat[u] = rhs_nat(P, col0 + u);
+      nat[u] = (col0 + u >= m) ? -1 : (P.colperm ? nat_tab[col0 + u] : col0 + u);
       const int col = nat[u];
       const double abb = col == b_lo ? e2[0] : (col == b_hi ? e2[1] : 0.0);
       o[u] = neg ? abb - o[u] : abb + o[u];
@@ -1851,7 +1904,11 @@ static int ensure_workspace(hps_plan_s* P, int mode, int want_slots) {
           make_map(&m.b_work, P->work, NC, NR, P->ws_slots, NC, per, B_STRIDE, KC) ||
           make_map(&m.a_scratch, P->scratch, TRI_BLOCK, 2 * P->n_pad, P->ws_slots, TRI_BLOCK,
                    (size_t)2 * P->n_pad * TRI_BLOCK, A_STRIDE, TM, !A_PAD) ||
-          make_map(&m.c_red, P->work, NC, NR, P->ws_slots, NC, per, 16, 8))
+          make_map(&m.c_red, P->work, NC, NR, P->ws_slots, NC, per, 16, 8) ||
+          make_map(&m.a_work_n, P->work, NC, NR, P->ws_slots, NC, per, GemmNarrow::AS,
+                   GemmNarrow::TM_) ||
+          make_map(&m.b_work_n, P->work, NC, NR, P->ws_slots, NC, per, GemmNarrow::BS,
+                   GemmNarrow::KC_))
         return -1;
       if (P->legendre &&
           (make_map(&m.a_abi, P->a_bi_pad, P->n_pad, P->m_pad, 1, P->n_pad,

@@ -46,6 +46,8 @@ int main(int argc, char** argv) {
     make_map(&maps.b_work, buf, ld, NR, CTAS_PER_SM * sms, ld, stride, B_STRIDE, KC);
     maps.a_scratch = maps.a_work;
     make_map(&maps.c_red, buf, ld, NR, CTAS_PER_SM * sms, ld, stride, 16, 8);
+    make_map(&maps.a_work_n, buf, ld, NR, CTAS_PER_SM * sms, ld, stride, GemmNarrow::AS, GemmNarrow::TM_);
+    make_map(&maps.b_work_n, buf, ld, NR, CTAS_PER_SM * sms, ld, stride, GemmNarrow::BS, GemmNarrow::KC_);
     double fl = 2.0 * s.M * s.N * s.K;
     int reps = (int)(2e10 / fl + 1);
     if (reps > 200) reps = 200;

@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--p", type=int, default=16)
     ap.add_argument("--boxes", type=int, default=16, help="leaf boxes per axis per GPU")
     ap.add_argument("--kappa", type=float, default=40.0)
+    ap.add_argument("--field", default="bump", choices=["bump", "const"],
+                    help="bump: variable-coefficient b(x) (configs 2-3); const: b = 1 (configs[1])")
     ap.add_argument("--leaves", type=int, default=0, help="override leaves per rank (profiling)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -61,8 +63,9 @@ def bump_b(x):
     return 1.0 - 0.5 * np.exp(-r2 / (2 * 0.15 ** 2))
 
 
-def make_shard(p, boxes, kappa, rank, world, leaves_override=0):
-    """Coefficient packs (L, 4, n) for this rank's slab of the unit-cube-stacked leaf grid."""
+def make_shard(p, boxes, kappa, rank, world, leaves_override=0, field="bump"):
+    """Coefficient packs (L, 4, n) for this rank's slab of the unit-cube-stacked leaf grid.
+    field "bump": -Lap u - kappa^2 b(x) u (configs 2-3); "const": b = 1 (configs[1])."""
     from paper_2503_04033_b200.local_ops import LeafTemplate
     h = 1.0 / boxes
     tpl = LeafTemplate((h, h, h), p, "drop", False)
@@ -84,7 +87,8 @@ def make_shard(p, boxes, kappa, rank, world, leaves_override=0):
         Y = np.broadcast_to(g[1][:, None, :, None], (B, q, q, q))
         Z = np.broadcast_to(g[2][:, None, None, :], (B, q, q, q))
         pts = np.stack([X, Y, Z], axis=-1).reshape(-1, 3)
-        pack[k0:k0 + B, 3, :] = (-kappa * kappa * bump_b(pts)).reshape(B, n)
+        b = bump_b(pts) if field == "bump" else np.ones(len(pts))
+        pack[k0:k0 + B, 3, :] = (-kappa * kappa * b).reshape(B, n)
     return tpl, pack
 
 
@@ -177,7 +181,9 @@ def main():
     grid = (f"{boxes}x{boxes}x{boxes} leaves per GPU" if leaves_per_gpu == boxes ** 3 else
             f"{leaves_per_gpu} leaves per GPU (a 1/{boxes ** 3 // max(leaves_per_gpu, 1)} shard of a "
             f"{boxes}x{boxes}x{boxes} leaf grid)")
-    workload = (f"3D variable-coefficient Helmholtz b(x) (Gaussian bump), p={p}, {grid}, "
+    kind = ("3D variable-coefficient Helmholtz b(x) (Gaussian bump)" if args.field == "bump"
+            else "3D constant-coefficient Helmholtz")
+    workload = (f"{kind}, p={p}, {grid}, "
                 f"kappa={args.kappa:g}")
     n = (p - 2) ** 3
     m = 6 * (p - 2) ** 2
@@ -189,7 +195,8 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        tpl, pack = make_shard(p, boxes, args.kappa, 0, 1, leaves_override=min(64, boxes ** 3))
+        tpl, pack = make_shard(p, boxes, args.kappa, 0, 1, leaves_override=min(64, boxes ** 3),
+                               field=args.field)
         steps = max(1, args.steps)
         per_step = max(2.0, 60.0 / (steps + args.warmup))
         for _ in range(args.warmup):
@@ -211,7 +218,7 @@ def main():
     # CPU reference first, before pinned buffers and GPU work claim host resources
     cpu = None
     if rank == 0 and not args.no_cpu:
-        tpl0, pack0 = make_shard(p, boxes, args.kappa, 0, 1, min(64, boxes ** 3))
+        tpl0, pack0 = make_shard(p, boxes, args.kappa, 0, 1, min(64, boxes ** 3), field=args.field)
         cpu = cpu_reference(tpl0, pack0, seconds=args.cpu_seconds)
 
     import torch
@@ -222,7 +229,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     from paper_2503_04033_b200.engine import LeafEngine
 
-    tpl, pack = make_shard(p, boxes, args.kappa, rank, world, args.leaves)
+    tpl, pack = make_shard(p, boxes, args.kappa, rank, world, args.leaves, field=args.field)
     L = pack.shape[0]
     eng = LeafEngine(tpl, False, True, device=local)
     coeffs = torch.from_numpy(pack).to(f"cuda:{local}")

@@ -47,7 +47,10 @@ constexpr int NT = HPS_NT;       // threads per CTA; two CTAs (two leaves) per S
 constexpr int CTAS_PER_SM = 2;
 constexpr int TM = 64;           // GEMM tile rows (1 x 4 warps of 64 x 32)
 constexpr int TN = 128;          // GEMM tile cols
-constexpr int KC = 16;           // k-chunk per pipeline stage
+#ifndef HPS_KC
+#define HPS_KC 16
+#endif
+constexpr int KC = HPS_KC;       // k-chunk per pipeline stage
 #ifndef HPS_STAGES
 #define HPS_STAGES 3
 #endif
@@ -239,7 +242,9 @@ struct GemmWide {
   static constexpr bool SWZ = !A_PAD;
 };
 struct GemmNarrow {
-  static constexpr int TM_ = 256, TN_ = 32, KC_ = 8, AS = 12, BS = 36, WN_ = 1;
+  // k-chunk 8 (row stride 12) with a 3-stage ring; 4 (stride 4) with deeper rings
+  static constexpr int TM_ = 256, TN_ = 32, KC_ = STAGES <= 3 ? 8 : 4, AS = KC_ == 8 ? 12 : 4;
+  static constexpr int BS = 36, WN_ = 1;
   static constexpr bool SWZ = false;
 };
 template <class G>

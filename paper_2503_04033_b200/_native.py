@@ -12,6 +12,8 @@ import os
 from .errors import NativeUnavailableError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libhps_leaf.so")
+# diagnostics: HPS_LIB points at an alternative in-tree build (tuning variants)
+LIB_PATH = os.environ.get("HPS_LIB", LIB_PATH)
 
 EXPORTS = (
     "hps_abi_version", "hps_last_error", "hps_device_count", "hps_plan_create",

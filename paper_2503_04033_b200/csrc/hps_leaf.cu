@@ -84,7 +84,10 @@ static_assert(MI * 8 * WM == TM && NJ == 4, "warp tiling");
 constexpr int EPI_DBL = EPI_SLOTS * 2 * 8 * 16;  // per warp: ring slots x two [8][16] blocks
 constexpr int GEMM_SMEM_BYTES = (STAGES * STAGE_DBL + (NT / 32) * EPI_DBL) * 8;
 constexpr int TRI_BLOCK = 64;    // triangular base block (explicit inverse + GEMM)
-constexpr int SMALL_PANEL = 32;  // recursion leaf width handled by rank-wb updates
+#ifndef HPS_SMALL_PANEL
+#define HPS_SMALL_PANEL 32
+#endif
+constexpr int SMALL_PANEL = HPS_SMALL_PANEL;  // recursion leaf width handled by the narrow panel
 constexpr int RHS_COLS = 16;     // padded rhs block in solve mode
 constexpr int PANEL_SMEM_CAP = 96 * 1024;
 
@@ -1045,15 +1048,20 @@ __device__ __forceinline__ void interior_multi(const LeafParams& P, int r, int* 
 // Boundary DOF index of the endpoint of the axis-`a` line through interior node I
 // (face order -x,+x,-y,+y[,-z,+z]; lexicographic over the tangential indices,
 // reference geometry convention local_ops.py:249-262).
+// Multi-indices live in 3 registers: every access below uses a compile-time
+// index (unrolled over 3 axes) so the arrays never go to local memory.
+__device__ __forceinline__ int pick3(const int* v, int a) {
+  return a == 0 ? v[0] : (a == 1 ? v[1] : v[2]);
+}
 __device__ __forceinline__ int boundary_index(const LeafParams& P, int a, int side, const int* I) {
   const int q = P.q;
   int t, fd;
   if (P.d == 3) {
-    const int o0 = (a == 0) ? 1 : 0, o1 = (a == 2) ? 1 : 2;
-    t = (I[o0] - 1) * q + (I[o1] - 1);
+    const int i0 = (a == 0) ? I[1] : I[0], i1 = (a == 2) ? I[1] : I[2];
+    t = (i0 - 1) * q + (i1 - 1);
     fd = q * q;
   } else {
-    t = I[a == 0 ? 1 : 0] - 1;
+    t = (a == 0 ? I[1] : I[0]) - 1;
     fd = q;
   }
   return (2 * a + side) * fd + t;
@@ -1151,37 +1159,65 @@ __device__ void rhs_profile(const LeafParams& P, Ctx& c) {
 // [a_kk (d) | a_ab + a_ba for (0,1),(0,2),(1,2) (if cross) | b_k (d) | c].
 // Sum order follows collocation_rows (local_ops.py:370-387): second order
 // x, y, z; cross pairs; first order x, y, z; zeroth.
-__device__ double op_entry(const LeafParams& P, const double* cf, int r, const int* I, const int* J) {
+// One row's coefficients, loaded once per row (warp-uniform) instead of per entry.
+struct RowCoef {
+  double a[3];  // a_kk
+  double x[3];  // a_ab + a_ba for (0,1), (0,2), (1,2)
+  double b[3];  // b_k
+  double c;     // zeroth order
+};
+__device__ __forceinline__ RowCoef row_coef(const LeafParams& P, const double* cf, int r) {
+  RowCoef rc;
+  const int d = P.d, n = P.n;
+  int k = 0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) rc.a[a] = (a < d) ? cf[(k + a) * n + r] : 0.0;
+  k += d;
+  const int npair = d * (d - 1) / 2;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) rc.x[a] = (P.has_cross && a < npair) ? cf[(k + a) * n + r] : 0.0;
+  if (P.has_cross) k += npair;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) rc.b[a] = (P.has_first && a < d) ? cf[(k + a) * n + r] : 0.0;
+  if (P.has_first) k += d;
+  rc.c = P.has_zeroth ? cf[k * n + r] : 0.0;
+  return rc;
+}
+
+// D1 / D2 are the plan's d x p x p tables (global) or their shared-memory copies.
+__device__ double op_entry(const LeafParams& P, const RowCoef& rc, const double* D1, const double* D2,
+                           const int* I, const int* J) {
   const int p = P.p, d = P.d;
   double v = 0.0;
   int ndiff = 0;
-  for (int k = 0; k < d; ++k) ndiff += (I[k] != J[k]);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) ndiff += (k < d && I[k] != J[k]);
   bool line[3];
+#pragma unroll
   for (int a = 0; a < 3; ++a) line[a] = (a < d) && (ndiff == 0 || (ndiff == 1 && I[a] != J[a]));
-  for (int a = 0; a < d; ++a)
-    if (line[a]) v = __dadd_rn(v, __dmul_rn(-cf[a * P.n + r], P.D2[(a * p + I[a]) * p + J[a]]));
-  int k = d;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    if (line[a]) v = __dadd_rn(v, __dmul_rn(-rc.a[a], D2[(a * p + I[a]) * p + J[a]]));
   if (P.has_cross) {
-    int pair = 0;
-    for (int a = 0; a < d; ++a) {
-      for (int b = a + 1; b < d; ++b, ++pair) {
-        bool in_plane = true;  // J differs from I at most in axes a and b
-        for (int t = 0; t < d; ++t)
-          if (t != a && t != b && I[t] != J[t]) in_plane = false;
+    // pairs (0,1), (0,2), (1,2); d = 2 has only (0,1)
+#pragma unroll
+    for (int pair = 0; pair < 3; ++pair) {
+      const int a = pair == 2 ? 1 : 0, b = pair == 0 ? 1 : 2, o = 3 - a - b;
+      if (b < d) {
+        const bool in_plane = (d < 3) || I[o] == J[o];  // J differs from I at most in a, b
         if (in_plane) {
-          const double kr = __dmul_rn(P.D1[(a * p + I[a]) * p + J[a]], P.D1[(b * p + I[b]) * p + J[b]]);
-          v = __dadd_rn(v, __dmul_rn(-cf[(k + pair) * P.n + r], kr));
+          const double kr = __dmul_rn(D1[(a * p + I[a]) * p + J[a]], D1[(b * p + I[b]) * p + J[b]]);
+          v = __dadd_rn(v, __dmul_rn(-rc.x[pair], kr));
         }
       }
     }
-    k += d * (d - 1) / 2;
   }
   if (P.has_first) {
-    for (int a = 0; a < d; ++a)
-      if (line[a]) v = __dadd_rn(v, __dmul_rn(cf[(k + a) * P.n + r], P.D1[(a * p + I[a]) * p + J[a]]));
-    k += d;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      if (line[a]) v = __dadd_rn(v, __dmul_rn(rc.b[a], D1[(a * p + I[a]) * p + J[a]]));
   }
-  if (P.has_zeroth && ndiff == 0) v = __dadd_rn(v, cf[k * P.n + r]);
+  if (P.has_zeroth && ndiff == 0) v = __dadd_rn(v, rc.c);
   return v;
 }
 
@@ -1193,11 +1229,11 @@ __device__ __forceinline__ int pattern_size(const LeafParams& P) {
 }
 __device__ __forceinline__ bool pattern_item(const LeafParams& P, const int* I, int e, int* J) {
   const int p = P.p, d = P.d;
-  J[0] = I[0]; J[1] = I[1]; J[2] = I[2];
   if (e < d * p) {
     const int a = e / p, pos = e - a * p;
-    if (pos == I[a] && a > 0) return false;
-    J[a] = pos;
+    if (pos == pick3(I, a) && a > 0) return false;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) J[t] = (t == a) ? pos : I[t];
     return true;
   }
   e -= d * p;
@@ -1205,22 +1241,26 @@ __device__ __forceinline__ bool pattern_item(const LeafParams& P, const int* I, 
   const int pair = e / per, w = e - pair * per;
   const int a = (d == 3 && pair == 2) ? 1 : 0, b = (d == 2) ? 1 : (pair == 0 ? 1 : 2);
   int ja = w / (p - 1), jb = w - ja * (p - 1);
-  ja += (ja >= I[a]);  // skip I[a] / I[b]: strict plane interior
-  jb += (jb >= I[b]);
-  J[a] = ja;
-  J[b] = jb;
+  ja += (ja >= pick3(I, a));  // skip I[a] / I[b]: strict plane interior
+  jb += (jb >= pick3(I, b));
+#pragma unroll
+  for (int t = 0; t < 3; ++t) J[t] = (t == a) ? ja : ((t == b) ? jb : I[t]);
   return true;
 }
 
 __device__ __forceinline__ bool is_interior(const LeafParams& P, const int* J) {
-  for (int k = 0; k < P.d; ++k)
-    if (J[k] == 0 || J[k] == P.p - 1) return false;
-  return true;
+  bool in = true;
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    if (k < P.d && (J[k] == 0 || J[k] == P.p - 1)) in = false;
+  return in;
 }
 
 __device__ __forceinline__ int full_flat(const LeafParams& P, const int* J) {
   int f = 0;
-  for (int k = 0; k < P.d; ++k) f = f * P.p + J[k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    if (k < P.d) f = f * P.p + J[k];
   return f;
 }
 
@@ -1244,8 +1284,13 @@ __device__ void assemble(const LeafParams& P, double* M, int leaf, double* smem)
       for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
       if (lane == 0) qub[g] = acc;
     }
-    __syncthreads();
   }
+  // derivative tables in shared memory (after the qub vector)
+  double* D1s = smem + (P.legendre ? ((P.nb + 1) & ~1) : 0);
+  const int dpp = d * P.p * P.p;
+  double* D2s = D1s + dpp;
+  for (int e = threadIdx.x; e < dpp; e += NT) { D1s[e] = P.D1[e]; D2s[e] = P.D2[e]; }
+  __syncthreads();
   const int npat = pattern_size(P);
   for (int r = warp; r < P.NR; r += NT / 32) {
     double* row = M + (size_t)r * P.ld;
@@ -1255,24 +1300,28 @@ __device__ void assemble(const LeafParams& P, double* M, int leaf, double* smem)
     if (r < P.n) {
       int I[3];
       interior_multi(P, r, I);
+      const RowCoef rc = row_coef(P, cf, r);
       double rhs = 0.0;  // interior solve: A_ib u_b accumulated over the pattern
       for (int e = lane; e < npat; e += 32) {
         int J[3];
         if (!pattern_item(P, I, e, J)) continue;
         if (is_interior(P, J)) {
           int flat = 0;
-          for (int k = 0; k < d; ++k) flat = flat * P.q + (J[k] - 1);
-          row[flat] = op_entry(P, cf, r, I, J);
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+            if (k < d) flat = flat * P.q + (J[k] - 1);
+          row[flat] = op_entry(P, rc, D1s, D2s, I, J);
         } else if (P.legendre) {
-          if (P.mode == MODE_INTERIOR) rhs += op_entry(P, cf, r, I, J) * qub[P.bpos[full_flat(P, J)]];
-          else if (!solve_mode) row[P.col_rb + P.bpos[full_flat(P, J)]] = op_entry(P, cf, r, I, J);
+          if (P.mode == MODE_INTERIOR) rhs += op_entry(P, rc, D1s, D2s, I, J) * qub[P.bpos[full_flat(P, J)]];
+          else if (!solve_mode) row[P.col_rb + P.bpos[full_flat(P, J)]] = op_entry(P, rc, D1s, D2s, I, J);
         } else if (!solve_mode) {
           // drop mode: line endpoints are face-interior DOFs
           int a = 0;
-          for (int k = 0; k < d; ++k)
-            if (J[k] != I[k]) a = k;
-          row[P.n_pad + rhs_col(P, boundary_index(P, a, J[a] == P.p - 1 ? 1 : 0, I))] =
-              op_entry(P, cf, r, I, J);
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+            if (k < d && J[k] != I[k]) a = k;
+          row[P.n_pad + rhs_col(P, boundary_index(P, a, pick3(J, a) == P.p - 1 ? 1 : 0, I))] =
+              op_entry(P, rc, D1s, D2s, I, J);
         }
       }
       if (P.mode == MODE_REDUCE && lane == 0) {
@@ -1286,11 +1335,15 @@ __device__ void assemble(const LeafParams& P, double* M, int leaf, double* smem)
           // rhs = A_ib u_b over its 2d structural nonzeros, in column (face) order
           const double* ub = P.in0 + (size_t)leaf * P.m;
           double sacc = 0.0;
-          for (int a = 0; a < d; ++a) {
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            if (a >= d) continue;
+#pragma unroll
             for (int side = 0; side < 2; ++side) {
-              int J[3] = {I[0], I[1], I[2]};
-              J[a] = side ? P.p - 1 : 0;
-              sacc += op_entry(P, cf, r, I, J) * ub[boundary_index(P, a, side, I)];
+              int J[3];
+#pragma unroll
+              for (int t = 0; t < 3; ++t) J[t] = (t == a) ? (side ? P.p - 1 : 0) : I[t];
+              sacc += op_entry(P, rc, D1s, D2s, I, J) * ub[boundary_index(P, a, side, I)];
             }
           }
           row[P.n_pad] = sacc;
@@ -1745,6 +1798,9 @@ __global__ void __launch_bounds__(256) hps_apply_kernel(LeafParams P) {
     const double* ub = P.in1 + (size_t)leaf * P.m;
     int I[3];
     interior_multi(P, r, I);
+    const RowCoef rc = row_coef(P, cf, r);
+    const double* D1s = P.D1;
+    const double* D2s = P.D2;
     double acc = 0.0;
     for (int e = lane; e < npat; e += 32) {
       int J[3];
@@ -1752,16 +1808,19 @@ __global__ void __launch_bounds__(256) hps_apply_kernel(LeafParams P) {
       double x;
       if (is_interior(P, J)) {
         int flat = 0;
-        for (int k = 0; k < P.d; ++k) flat = flat * P.q + (J[k] - 1);
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+          if (k < P.d) flat = flat * P.q + (J[k] - 1);
         x = ui[flat];
       } else {
         int a = 0, nd = 0;
-        for (int k = 0; k < P.d; ++k)
-          if (J[k] != I[k]) { a = k; ++nd; }
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+          if (k < P.d && J[k] != I[k]) { a = k; ++nd; }
         if (nd != 1) continue;  // corner / edge nodes carry no value in drop mode
-        x = ub[boundary_index(P, a, J[a] == P.p - 1 ? 1 : 0, I)];
+        x = ub[boundary_index(P, a, pick3(J, a) == P.p - 1 ? 1 : 0, I)];
       }
-      acc += op_entry(P, cf, r, I, J) * x;
+      acc += op_entry(P, rc, D1s, D2s, I, J) * x;
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);

@@ -842,7 +842,10 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
   __syncthreads();
   PANEL_TICK(13)
   // 5. the block's interchanges on the rest of the panel segment [c0, c0+w)
-  if (tid == 0) {
+  bool any_swap = false;  // most blocks have no interchange at all
+  for (int j = 0; j < WB; ++j) any_swap |= c.piv[b0 + j] != b0 + j;
+  if (tid == 0 && !any_swap) s_swp_cnt = 0;
+  if (tid == 0 && any_swap) {
     int rows[16], cont[16], cnt = 0;
     for (int j = 0; j < WB; ++j) {
       const int cand[2] = {b0 + j, c.piv[b0 + j]};

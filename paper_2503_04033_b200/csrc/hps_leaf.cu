@@ -936,35 +936,82 @@ __device__ void stage_tri(const Ctx& c, int r0, int h, double* Ls) {
   __syncthreads();
 }
 
-// Thread layout for the inverses: 4 lanes per column, each lane sums every
-// 4th term of the column's dot product, a 2-step shuffle reduces.
-__device__ void invert_unit_lower(const Ctx& c, int r0, int h) {
-  double* Ls = c.smem;
-  double* X = c.smem + TRI_BLOCK * TRI_LD;
-  stage_tri(c, r0, h, Ls);
-  const int lane = threadIdx.x & 31;
-  const int part = lane & 3;
-  for (int j = (threadIdx.x >> 2); j < TRI_BLOCK; j += NT / 4) {
-    // rows i <= j of column j are 0 / 1
-    for (int i = part; i <= j && i < TRI_BLOCK; i += 4) X[i * TRI_LD + j] = (i == j) ? 1.0 : 0.0;
+// Explicit inverse of a staged triangular block by recursive doubling: the
+// 8 x 8 diagonal blocks are inverted by substitution (thread per column), then
+// pairs of inverted s x s blocks are merged, s = 8, 16, 32:
+//   lower  [A 0; B C]^-1 = [A^-1 0; -C^-1 (B A^-1)  C^-1]
+//   upper  [A B; 0 C]^-1 = [A^-1  -A^-1 (B C^-1); 0 C^-1]
+// with every product of a level spread over all threads (no 64-long serial
+// chain).  Rows / columns h..63 are padded with the identity.
+__device__ void tri_inverse(double* T, double* X, double* W, int h, bool upper) {
+  const int tid = threadIdx.x;
+  // pad + zero X
+  for (int e = tid; e < TRI_BLOCK * TRI_BLOCK; e += NT) {
+    const int i = e / TRI_BLOCK, j = e - i * TRI_BLOCK;
+    if (i >= h || j >= h) T[i * TRI_LD + j] = (i == j) ? 1.0 : 0.0;
+    X[i * TRI_LD + j] = 0.0;
   }
   __syncthreads();
-  for (int j0 = 0; j0 < TRI_BLOCK; j0 += NT / 4) {
-    const int j = j0 + (threadIdx.x >> 2);
-    const bool act = j < h;
-    for (int i = j0 + 1; i < h; ++i) {  // uniform loop bound within the warp group
-      double v = 0.0;
-      if (act && i > j) {
-        const double* Li = Ls + i * TRI_LD;
-        for (int k = j + part; k < i; k += 4) v -= Li[k] * X[k * TRI_LD + j];
+  // level 0: 8 x 8 diagonal blocks, thread per (block, column)
+  if (tid < TRI_BLOCK) {
+    const int b = tid >> 3, j = tid & 7, o = b * 8;
+    const int cj = o + j;
+    if (!upper) {  // unit lower
+      X[cj * TRI_LD + cj] = 1.0;
+      for (int i = j + 1; i < 8; ++i) {
+        double v = 0.0;
+        for (int k = j; k < i; ++k) v -= T[(o + i) * TRI_LD + o + k] * X[(o + k) * TRI_LD + cj];
+        X[(o + i) * TRI_LD + cj] = v;
       }
-      v += __shfl_xor_sync(0xffffffffu, v, 1);
-      v += __shfl_xor_sync(0xffffffffu, v, 2);
-      if (act && i > j && part == 0) X[i * TRI_LD + j] = v;
-      __syncwarp();
+    } else {
+      X[cj * TRI_LD + cj] = 1.0 / T[cj * TRI_LD + cj];
+      for (int i = j - 1; i >= 0; --i) {
+        double v = 0.0;
+        for (int k = i + 1; k <= j; ++k) v -= T[(o + i) * TRI_LD + o + k] * X[(o + k) * TRI_LD + cj];
+        X[(o + i) * TRI_LD + cj] = v / T[(o + i) * TRI_LD + o + i];
+      }
     }
   }
   __syncthreads();
+  for (int sz = 8; sz < TRI_BLOCK; sz *= 2) {
+    const int pairs = TRI_BLOCK / (2 * sz), items = pairs * sz * sz;
+    // W = B A^-1 (lower) / B C^-1 (upper); W stored per pair as sz x sz
+    for (int e = tid; e < items; e += NT) {
+      const int pr = e / (sz * sz), r = (e / sz) % sz, cc = e % sz;
+      const int o = pr * 2 * sz;
+      double v = 0.0;
+      if (!upper) {  // B = T[o+sz+r][o+k], A^-1 = X[o+k][o+cc] (lower: k >= cc)
+        for (int k = cc; k < sz; ++k) v += T[(o + sz + r) * TRI_LD + o + k] * X[(o + k) * TRI_LD + o + cc];
+      } else {       // B = T[o+r][o+sz+k], C^-1 = X[o+sz+k][o+sz+cc] (upper: k <= cc)
+        for (int k = 0; k <= cc; ++k)
+          v += T[(o + r) * TRI_LD + o + sz + k] * X[(o + sz + k) * TRI_LD + o + sz + cc];
+      }
+      W[e] = v;
+    }
+    __syncthreads();
+    for (int e = tid; e < items; e += NT) {
+      const int pr = e / (sz * sz), r = (e / sz) % sz, cc = e % sz;
+      const int o = pr * 2 * sz;
+      const double* Wp = W + pr * sz * sz;
+      double v = 0.0;
+      if (!upper) {  // X21 = -C^-1 W: C^-1 = X[o+sz+r][o+sz+k] (k <= r)
+        for (int k = 0; k <= r; ++k) v -= X[(o + sz + r) * TRI_LD + o + sz + k] * Wp[k * sz + cc];
+        X[(o + sz + r) * TRI_LD + o + cc] = v;
+      } else {       // X12 = -A^-1 W: A^-1 = X[o+r][o+k] (k >= r)
+        for (int k = r; k < sz; ++k) v -= X[(o + r) * TRI_LD + o + k] * Wp[k * sz + cc];
+        X[(o + r) * TRI_LD + o + sz + cc] = v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__device__ void invert_unit_lower(const Ctx& c, int r0, int h) {
+  double* Ls = c.smem;
+  double* X = c.smem + TRI_BLOCK * TRI_LD;
+  double* W = X + TRI_BLOCK * TRI_LD;
+  stage_tri(c, r0, h, Ls);
+  tri_inverse(Ls, X, W, h, false);
   double* dst = c.scratch + (size_t)r0 * TRI_BLOCK;
   for (int e = threadIdx.x; e < h * TRI_BLOCK; e += NT) dst[e] = X[(e / TRI_BLOCK) * TRI_LD + e % TRI_BLOCK];
   __syncthreads();
@@ -973,31 +1020,9 @@ __device__ void invert_unit_lower(const Ctx& c, int r0, int h) {
 __device__ void invert_upper(const Ctx& c, int r0, int h) {
   double* Us = c.smem;
   double* X = c.smem + TRI_BLOCK * TRI_LD;
+  double* W = X + TRI_BLOCK * TRI_LD;
   stage_tri(c, r0, h, Us);
-  const int lane = threadIdx.x & 31;
-  const int part = lane & 3;
-  for (int j = (threadIdx.x >> 2); j < TRI_BLOCK; j += NT / 4) {
-    for (int i = j + 1 + part; i < TRI_BLOCK; i += 4) X[i * TRI_LD + j] = 0.0;
-    if (part == 0 && j < h) X[j * TRI_LD + j] = 1.0 / Us[j * TRI_LD + j];
-  }
-  __syncthreads();
-  for (int j0 = 0; j0 < TRI_BLOCK; j0 += NT / 4) {
-    const int j = j0 + (threadIdx.x >> 2);
-    const bool act = j < h;
-    const int top = min(h, j0 + NT / 4) - 1;
-    for (int i = top - 1; i >= 0; --i) {
-      double v = 0.0;
-      if (act && i < j) {
-        const double* Ui = Us + i * TRI_LD;
-        for (int k = i + 1 + part; k <= j; k += 4) v -= Ui[k] * X[k * TRI_LD + j];
-      }
-      v += __shfl_xor_sync(0xffffffffu, v, 1);
-      v += __shfl_xor_sync(0xffffffffu, v, 2);
-      if (act && i < j && part == 0) X[i * TRI_LD + j] = v / Us[i * TRI_LD + i];
-      __syncwarp();
-    }
-  }
-  __syncthreads();
+  tri_inverse(Us, X, W, h, true);
   double* dst = c.scratch + (size_t)(c.n_piv + r0) * TRI_BLOCK;
   for (int e = threadIdx.x; e < h * TRI_BLOCK; e += NT) dst[e] = X[(e / TRI_BLOCK) * TRI_LD + e % TRI_BLOCK];
   __syncthreads();
@@ -2078,7 +2103,7 @@ static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, c
   const int panel_bytes = ((P->n_pad * P->wb > 1024 ? P->n_pad * P->wb : 1024) + 32 * P->wb) * 8;
   int smem = GEMM_SMEM_BYTES;
   if (panel_bytes > smem) smem = panel_bytes;
-  if (2 * TRI_BLOCK * TRI_LD * 8 > smem) smem = 2 * TRI_BLOCK * TRI_LD * 8;
+  if ((2 * TRI_BLOCK * TRI_LD + 32 * TRI_BLOCK / 2) * 8 > smem) smem = (2 * TRI_BLOCK * TRI_LD + 32 * TRI_BLOCK / 2) * 8;
   L.smem_doubles = smem / 8;
   if (const char* dbg = getenv("HPS_DEBUG")) L.debug = atoi(dbg);
   CK(cudaFuncSetAttribute(hps_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

@@ -1640,6 +1640,11 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
 
   unsigned long long* prof = P.prof ? P.prof + (size_t)slot * PROF_SLOTS : nullptr;
   c.prof = prof;
+  if (prof && threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    prof[25] = smid;
+  }
   // dynamic leaf scheduling: the two CTAs sharing an SM do not progress at the
   // same rate (warp arbitration), so slots grab the next leaf when done
   __shared__ int s_leaf;

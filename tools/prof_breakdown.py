@@ -50,3 +50,16 @@ print(f"  row interchanges per leaf: {c[:, 15].sum()/leaves:.0f} of {eng.n} pivo
 gf = sum(c[:, 19 + b].sum() for b in range(3)) * 2**20
 print(f"  gemm flops/leaf {gf/leaves:.3e}; gemm-only rate per CTA {gf/(c[:, 16:19].sum())*clk/1e9:.1f} GFLOP/s "
       f"(peak 251/SM); per-leaf total {tot/leaves/clk*1e3:.1f} ms")
+# per-CTA spread (one leaf per CTA when leaves == slots): busy cycles by SM id
+busy = c[:, :9].sum(1) + c[:, 22] + c[:, 23] + c[:, 24]
+per_leaf = busy / np.maximum(c[:, 9], 1)
+sm = c[:, 25].astype(int)
+q = np.quantile(per_leaf, [0, 0.1, 0.5, 0.9, 1.0]) / clk * 1e3
+print("  per-CTA ms/leaf quantiles (0,10,50,90,100%):", " ".join(f"{x:.1f}" for x in q))
+lo = per_leaf[sm < sm.max() / 2].mean() / clk * 1e3
+hi = per_leaf[sm >= sm.max() / 2].mean() / clk * 1e3
+print(f"  mean ms/leaf on SM ids < half: {lo:.1f}, >= half: {hi:.1f}")
+order = np.argsort(sm)
+pair = per_leaf[order].reshape(-1, 2) if len(order) % 2 == 0 else None
+if pair is not None:
+    print(f"  same-SM pair |difference| mean {np.abs(pair[:, 0] - pair[:, 1]).mean() / clk * 1e3:.1f} ms")

@@ -639,13 +639,15 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
     //    8-row groups per warp (m8n8k4: A fragments straight from global,
     //    B fragments = Ut held in registers), G groups in flight.
     constexpr int G = 4;
-    const int nkq = (done + 3) >> 2;
+    // k order permuted so each lane's A operands of a DMMA pair are adjacent:
+    // DMMA kq uses k = 8 (kq / 2) + 2 lc + (kq & 1), one 16-byte load per pair
+    const int nkp = (done + 7) >> 3;  // DMMA pairs
     const int lr = lane >> 2, lc = lane & 3;
     double bfr[8];
 #pragma unroll
     for (int kq = 0; kq < 8; ++kq) {
-      const int k = kq * 4 + lc;
-      bfr[kq] = (kq < nkq && lr < WB && k < done) ? Ut[lr * 32 + k] : 0.0;
+      const int k = 8 * (kq >> 1) + 2 * lc + (kq & 1);
+      bfr[kq] = ((kq >> 1) < nkp && lr < WB && k < done) ? Ut[lr * 32 + k] : 0.0;
     }
     const bool owns = 2 * lc < WB;  // lane holds output columns 2lc, 2lc+1
     for (int g0 = b0 + warp * 8 * G; g0 < c.NR; g0 += NW * 8 * G) {
@@ -656,16 +658,28 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
         const bool ok = r < c.NR;
         const double* row = c.M + (size_t)(ok ? r : c.NR - 1) * c.ld;
 #pragma unroll
-        for (int kq = 0; kq < 8; ++kq) af[g][kq] = (ok && kq < nkq) ? row[c0 + kq * 4 + lc] : 0.0;
-        av[g][0] = (ok && owns) ? row[b0 + 2 * lc] : 0.0;
-        av[g][1] = (ok && owns && 2 * lc + 1 < WB) ? row[b0 + 2 * lc + 1] : 0.0;
+        for (int pq = 0; pq < 4; ++pq) {
+          double2 v2 = make_double2(0.0, 0.0);
+          if (ok && pq < nkp) v2 = *reinterpret_cast<const double2*>(row + c0 + 8 * pq + 2 * lc);
+          af[g][2 * pq] = v2.x;
+          af[g][2 * pq + 1] = v2.y;
+        }
+        if (WB >= 2) {
+          double2 v2 = make_double2(0.0, 0.0);
+          if (ok && owns) v2 = *reinterpret_cast<const double2*>(row + b0 + 2 * lc);
+          av[g][0] = v2.x;
+          av[g][1] = v2.y;
+        } else {
+          av[g][0] = (ok && owns) ? row[b0 + 2 * lc] : 0.0;
+          av[g][1] = 0.0;
+        }
       }
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         double acc[2] = {0.0, 0.0};
 #pragma unroll
         for (int kq = 0; kq < 8; ++kq)
-          if (kq < nkq) dmma(acc, af[g][kq], bfr[kq]);
+          if ((kq >> 1) < nkp) dmma(acc, af[g][kq], bfr[kq]);
         const int r = g0 + g * 8 + lr;
         if (r < c.NR && owns) {
           const double v0 = av[g][0] - acc[0], v1 = av[g][1] - acc[1];

@@ -93,6 +93,20 @@ constexpr int PANEL_SMEM_CAP = 96 * 1024;
 
 enum { MODE_DTN = 0, MODE_REDUCE = 1, MODE_INTERIOR = 2, MODE_SOLOP = 3 };
 
+// Endgame GEMM sharing.  Once every leaf of the launch has been claimed, a CTA
+// that finds no leaf left does not exit: it joins the GEMMs of CTAs still
+// reducing a leaf, claiming their output tiles through a per-slot counter.
+// The owner publishes each large GEMM op (op index, tile count, sequence
+// number), claims tiles itself with atomicAdd, and waits for the tile-done
+// count before its next op; helpers claim with compare-and-swap on the same
+// (seq, next) word so a stale helper can never take a tile of a newer op.
+struct ShareSlot {
+  unsigned long long claim;  // (seq << 32) | next unclaimed tile
+  int op_seq, op, tiles, done;
+  int pad[2];
+};
+constexpr int SHARE_MIN_TILES = 16;
+
 struct LeafParams {
   int mode;
   int d, p, q;            // q = p - 2 interior points per axis
@@ -127,11 +141,14 @@ struct LeafParams {
   int* done_counts;          // optional: finished leaves per output chunk (streamed D2H)
   int done_chunk;            // leaves per output chunk
   int smem_doubles;          // dynamic shared memory of the launch, in doubles
+  ShareSlot* share;          // [slots] endgame GEMM sharing (nullptr: off)
+  int* share_finished;       // CTAs that found no leaf left
   int debug;                 // diagnostics (env HPS_DEBUG): 1 skip the LU program, 2 old DtN output,
-                             // 4 natural A_ib column order without zero-prefix skipping, 8 one CTA per SM
+                             // 4 natural A_ib column order without zero-prefix skipping, 8 one CTA per SM,
+                             // 16 no endgame GEMM sharing
 };
 
-constexpr int PROF_SLOTS = 26;  // 0..8 op kinds, 9 leaves, 10-14 panel steps, 15 interchanges,
+constexpr int PROF_SLOTS = 28;  // 0..8 op kinds, 9 leaves, 10-14 panel steps, 15 interchanges,
                                 // 16-18 GEMM cycles by N (<=64, <=256, >256), 19-21 their MFLOP, 22 assemble, 23 output
 
 // ---------------------------------------------------------------------------
@@ -276,6 +293,14 @@ struct Ctx {
   uint64_t* full;   // STAGES mbarriers: stage filled (TMA tx complete)
   uint64_t* empty;  // STAGES mbarriers: stage released by all 8 warps
   unsigned pipe;    // running stage counter, identical in every thread
+  // endgame sharing: sh = share record of the slot whose GEMM runs (own slot for
+  // an owner, the helped slot for a helper); role 0 owner-capable, 2 helper
+  ShareSlot* sh;
+  int role;
+  unsigned seq;     // owner: last published sequence (thread 0); helper: the op's sequence
+  int cur_op;       // owner: index of the op being executed
+  const int* leaf_counter;
+  int n_leaves;
 };
 
 // ---------------------------------------------------------------------------
@@ -305,7 +330,6 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   const int tiles_n = (N + TN - 1) / TN;
   const int tiles = ((M + TM - 1) / TM) * tiles_n;
   const int kchunks = K / KC;
-  const int total = tiles * kchunks;
   double* smem = c.smem;
   const CUtensorMap* mapA = narrow ? &c.maps->a_work_n
                            : (a_src == 0 ? &c.maps->a_work
@@ -314,17 +338,66 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   const int a_slot = a_src == 2 ? 0 : c.slot, b_slot = b_src == 1 ? 0 : c.slot;
   double* C = c.M + (size_t)cr * c.ld + cc;
 
+  // Tile claims: mode 0 in order; mode 1 owner of a published op (atomicAdd on
+  // the slot's claim word); mode 2 helper (compare-and-swap with the op's seq).
+  __shared__ int s_gmode;
+  __shared__ int s_tile_ring[STAGES];  // tile id started in each stage (-1: end)
+  if (tid == 0) {
+    int m = 0;
+    if (c.role == 2) {
+      m = 2;
+    } else if (c.sh && tiles >= SHARE_MIN_TILES &&
+               *reinterpret_cast<const volatile int*>(c.leaf_counter) >= c.n_leaves) {
+      m = 1;
+      ShareSlot* sh = c.sh;
+      c.seq += 1;
+      sh->op = c.cur_op;
+      sh->tiles = tiles;
+      sh->done = 0;
+      sh->op_seq = (int)c.seq;
+      __threadfence();
+      atomicExch(&sh->claim, (unsigned long long)c.seq << 32);
+    }
+    s_gmode = m;
+  }
   // every thread's earlier global writes must be visible to the TMA reads below
   fence_proxy_async_global();
   __syncthreads();
+  const int gmode = s_gmode;
 
   // producer state (thread 0 only)
-  int p_it = 0, p_tile = 0, p_kc = 0;
+  int p_it = 0, p_tile = 0, p_kc = 0, p_next = 0;
+  bool p_end = false;
+  auto claim_tile = [&]() -> int {
+    if (gmode == 0) return p_next < tiles ? p_next++ : -1;
+    if (gmode == 1) {
+      const unsigned long long old = atomicAdd(&c.sh->claim, 1ull);
+      const int t = (int)(old & 0xffffffffull);
+      return t < tiles ? t : -1;
+    }
+    unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(&c.sh->claim);
+    for (;;) {
+      if ((unsigned)(old >> 32) != c.seq || (int)(old & 0xffffffffull) >= tiles) return -1;
+      const unsigned long long prev = atomicCAS(&c.sh->claim, old, old + 1);
+      if (prev == old) return (int)(old & 0xffffffffull);
+      old = prev;
+    }
+  };
   auto produce = [&]() {
-    if (p_it >= total) return;
+    if (p_end) return;
     const unsigned g = c.pipe + p_it;
     const unsigned s = g % STAGES, use = g / STAGES;
     if (use > 0) mbar_wait(&c.empty[s], (use - 1) & 1);
+    if (p_kc == 0) {
+      p_tile = claim_tile();
+      s_tile_ring[s] = p_tile;
+      if (p_tile < 0) {  // end marker: a stage with no data
+        p_end = true;
+        mbar_arrive(&c.full[s]);
+        ++p_it;
+        return;
+      }
+    }
     const int tm = p_tile / tiles_n, tn = p_tile - tm * tiles_n;
     double* sa = smem + s * STAGE_DBL;
     double* sb = sa + STAGE_A;
@@ -340,7 +413,7 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
       }
     }
     ++p_it;
-    if (++p_kc == kchunks) { p_kc = 0; ++p_tile; }
+    if (++p_kc == kchunks) p_kc = 0;
   };
   if (tid == 0) {
     for (int s = 0; s < STAGES - 1; ++s) produce();
@@ -352,7 +425,7 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
 #pragma unroll
     for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  int tile = 0, kc = 0;
+  int tile = 0, kc = 0, it = 0, my_tiles = 0;
   // 8x8 sub-tiles of this warp that lie inside the GEMM extent (warp-uniform):
   // edge tiles skip the DMMAs on zero-filled rows / columns.
   int mv = MI, nv = NJ;
@@ -362,12 +435,21 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     mv = rows <= 0 ? 0 : (rows >= MI * 8 ? MI : (rows + 7) / 8);
     nv = cols <= 0 ? 0 : (cols >= NJ * 8 ? NJ : (cols + 7) / 8);
   };
-  set_valid(0);
-  for (int it = 0; it < total; ++it) {
+  for (;; ++it) {
     if (tid == 0) produce();
     const unsigned g = c.pipe + it;
     const unsigned s = g % STAGES;
     mbar_wait(&c.full[s], (g / STAGES) & 1);
+    if (kc == 0) {
+      tile = reinterpret_cast<volatile int*>(s_tile_ring)[s];
+      if (tile < 0) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&c.empty[s]);
+        ++it;
+        break;
+      }
+      set_valid(tile);
+    }
     const double* sa = smem + s * STAGE_DBL;
     const double* sb = sa + STAGE_A;
     auto mainloop = [&](auto edge) {
@@ -400,8 +482,7 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     if (++kc == kchunks) {
       kc = 0;
       const int tm = tile / tiles_n, tn = tile - tm * tiles_n;
-      ++tile;
-      if (tile < tiles) set_valid(tile);
+      ++my_tiles;
       if (sub) {
         // C -= acc through TMA reduce-add in L2: -acc goes to a per-warp smem ring
         // (two [8][16] blocks per m-tile) and drains asynchronously.
@@ -458,10 +539,21 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
       }
     }
   }
-  c.pipe += total;
+  c.pipe += it;
   if (sub && lane == 0) {
     bulk_wait_all();
     fence_proxy_async_global();
+  }
+  if (gmode != 0) {  // shared op: count the tiles done here; the owner waits for all
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      if (my_tiles > 0) atomicAdd(&c.sh->done, my_tiles);
+      if (gmode == 1) {
+        while (*reinterpret_cast<volatile int*>(&c.sh->done) < tiles) __nanosleep(200);
+        __threadfence();
+      }
+    }
   }
   __syncthreads();
 }
@@ -1651,6 +1743,12 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
   c.scratch = P.scratch + (size_t)slot * 2 * P.n_pad * TRI_BLOCK;
   c.smem = smem;
   c.smem_doubles = P.smem_doubles;
+  c.sh = P.share ? P.share + slot : nullptr;
+  c.role = 0;
+  c.seq = 0;
+  c.cur_op = 0;
+  c.leaf_counter = P.leaf_counter;
+  c.n_leaves = P.n_leaves;
 
   unsigned long long* prof = P.prof ? P.prof + (size_t)slot * PROF_SLOTS : nullptr;
   c.prof = prof;
@@ -1675,6 +1773,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     if (prof && threadIdx.x == 0) { prof[22] += clock64() - t0; prof[9] += 1; }
     for (int k = 0; k < ((P.debug & 1) ? 0 : n_ops); ++k) {
       Op op = ops[k];
+      c.cur_op = k;
       if (prof) t0 = clock64();
       switch (op.kind) {
         case OP_SMALL: lu_small(c, op.a, op.b); break;
@@ -1744,6 +1843,65 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     }
     __syncthreads();
     if (prof && threadIdx.x == 0) prof[23] += clock64() - t0;
+  }
+  // Endgame: no leaf left for this CTA.  Help the CTAs still reducing a leaf
+  // with the tiles of their published GEMMs until every CTA is done.
+  if (P.share) {
+    __shared__ int s_tgt, s_top;
+    __shared__ unsigned s_tseq;
+    const int nslots = (int)gridDim.x;
+    long long th = prof ? clock64() : 0;
+    if (threadIdx.x == 0) atomicAdd(P.share_finished, 1);
+    for (int round = 0;; ++round) {
+      if (threadIdx.x == 0) {
+        int tgt = -1;
+        if (*reinterpret_cast<volatile int*>(P.share_finished) >= nslots) {
+          tgt = -2;
+        } else {
+          for (int k = 1; k < nslots && tgt < 0; ++k) {
+            const int s2 = (slot + k) % nslots;
+            ShareSlot* sh = P.share + s2;
+            const unsigned long long w = *reinterpret_cast<volatile unsigned long long*>(&sh->claim);
+            const unsigned seq = (unsigned)(w >> 32);
+            if (seq == 0) continue;
+            __threadfence();
+            const int oseq = *reinterpret_cast<volatile int*>(&sh->op_seq);
+            const int tiles = *reinterpret_cast<volatile int*>(&sh->tiles);
+            const int op = *reinterpret_cast<volatile int*>(&sh->op);
+            if ((unsigned)oseq == seq && (int)(w & 0xffffffffull) < tiles) {
+              tgt = s2;
+              s_tseq = seq;
+              s_top = op;
+            }
+          }
+          if (tgt < 0) __nanosleep(1000);
+        }
+        s_tgt = tgt;
+      }
+      __syncthreads();
+      const int tgt = s_tgt;
+      if (tgt == -2) break;
+      if (tgt >= 0) {
+        Ctx h = c;
+        h.slot = tgt;
+        h.M = P.work + (size_t)tgt * P.slot_stride;
+        h.piv = P.piv + (size_t)tgt * P.piv_stride;
+        h.rhs_tab = h.piv + P.n_pad;
+        h.scratch = P.scratch + (size_t)tgt * 2 * P.n_pad * TRI_BLOCK;
+        h.sh = P.share + tgt;
+        h.role = 2;
+        h.seq = s_tseq;
+        const Op op = ops[s_top];
+        const bool sub = (op.kind == OP_GEMM_SUB || op.kind == OP_GEMM_SUB_ABI);
+        const int a_src = op.kind == OP_GEMM_SET ? 1 : (op.kind == OP_GEMM_SUB_ABI ? 2 : 0);
+        const int b_src = op.kind == OP_GEMM_SET_Q ? 1 : 0;
+        const int N = op.dyn ? min(op.Ndim, h.rhs_tab[op.dyn >> 4]) : op.Ndim;
+        gemm(h, sub, a_src, op.ar, op.ac, b_src, op.br, op.bc, op.cr, op.cc, op.Mdim, N, op.Kdim);
+        c.pipe = h.pipe;
+      }
+      __syncthreads();
+    }
+    if (prof && threadIdx.x == 0) prof[26] += clock64() - th;
   }
 }
 
@@ -1916,7 +2074,9 @@ struct hps_plan_s {
   int prog_len[4] = {0, 0, 0, 0};
   double* h_stage = nullptr;
   unsigned long long* prof = nullptr;  // diagnostics counters (device), optional
-  int* leaf_counter = nullptr;
+  int* leaf_counter = nullptr;  // [0] next leaf, [32] CTAs without a leaf (endgame sharing)
+  ShareSlot* share = nullptr;
+  int share_cap = 0;
   // streamed host-buffer DtN: device copies of all inputs / outputs (grow-only)
   double* s_coef = nullptr;
   double* s_out = nullptr;
@@ -2115,9 +2275,25 @@ static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, c
   L.D1 = P->D1; L.D2 = P->D2; L.a_bi = P->a_bi; L.a_bb = P->a_bb;
   L.prof = P->prof;
   L.leaf_counter = P->leaf_counter;
+  L.share_finished = P->leaf_counter + 32;
   L.done_counts = done_counts;
   L.done_chunk = done_chunk;
-  CK(cudaMemsetAsync(P->leaf_counter, 0, sizeof(int), stream));
+  CK(cudaMemsetAsync(P->leaf_counter, 0, 64 * sizeof(int), stream));
+  {
+    const char* dbg = getenv("HPS_DEBUG");
+    const bool share_off = dbg && (atoi(dbg) & 16);
+    if (!share_off) {
+      if (P->share_cap < slots) {
+        cudaFree(P->share);
+        P->share = nullptr;
+        P->share_cap = 0;
+        CK(cudaMalloc(&P->share, sizeof(ShareSlot) * (size_t)slots));
+        P->share_cap = slots;
+      }
+      CK(cudaMemsetAsync(P->share, 0, sizeof(ShareSlot) * (size_t)slots, stream));
+      L.share = P->share;
+    }
+  }
   L.coeffs = coeffs; L.in0 = in0; L.in1 = in1; L.out0 = out0; L.out1 = out1; L.stats = stats;
   const int panel_bytes = ((P->n_pad * P->wb > 1024 ? P->n_pad * P->wb : 1024) + 32 * P->wb) * 8;
   int smem = GEMM_SMEM_BYTES;
@@ -2182,7 +2358,7 @@ static int plan_create(hps_plan_t* out, int device, int dim, int p, int legendre
   if (cudaMalloc(&P->D1, tab) != cudaSuccess || cudaMalloc(&P->D2, tab) != cudaSuccess ||
       cudaMalloc(&P->a_bi, (size_t)P->m * P->n * 8) != cudaSuccess ||
       cudaMalloc(&P->a_bb, (size_t)P->m * P->m * 8) != cudaSuccess ||
-      cudaMalloc(&P->leaf_counter, sizeof(int)) != cudaSuccess) {
+      cudaMalloc(&P->leaf_counter, 64 * sizeof(int)) != cudaSuccess) {
     hps_plan_destroy(P);
     return fail("device allocation of templates failed");
   }
@@ -2235,6 +2411,7 @@ int hps_plan_destroy(hps_plan_t P) {
   cudaSetDevice(P->device);
   cudaFree(P->D1); cudaFree(P->D2); cudaFree(P->a_bi); cudaFree(P->a_bb);
   cudaFree(P->leaf_counter);
+  cudaFree(P->share);
   cudaFree(P->s_coef); cudaFree(P->s_out); cudaFree(P->s_stats); cudaFree(P->s_done);
   cudaFree(P->Q); cudaFree(P->a_bi_pad); cudaFree(P->bpos);
   cudaFree(P->work); cudaFree(P->piv); cudaFree(P->scratch);

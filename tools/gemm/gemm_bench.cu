@@ -16,6 +16,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) gemm_probe(double* base, size
   c.M = base + (size_t)blockIdx.x * stride;
   c.ld = ld; c.slot = blockIdx.x; c.smem = smem; c.maps = &maps;
   c.full = bars; c.empty = bars + STAGES; c.pipe = 0; c.prof = nullptr;
+  c.sh = nullptr; c.role = 0; c.seq = 0; c.cur_op = 0; c.leaf_counter = nullptr; c.n_leaves = 0;
   for (int r = 0; r < reps; ++r) gemm(c, true, 0, 0, 0, 0, M, 0, M + K, 0, M, N, K);
 }
 }  // namespace

@@ -119,6 +119,26 @@ def test_zero_prefix_forward_solve_is_exact(p, d, monkeypatch):
     assert np.array_equal(fast, dense)
 
 
+def test_endgame_gemm_sharing_is_exact(monkeypatch):
+    """More leaves than slots: CTAs that run out of leaves take output tiles of the
+    remaining leaves' GEMMs.  Each tile is still computed by exactly one CTA in the
+    same order, so the maps equal the unshared run (HPS_DEBUG=16) bit for bit, and
+    the oracle within tolerance."""
+    from paper_2503_04033_b200.engine import LeafEngine
+    tpl0, _ = bump_pack(12, 1, kappa=25.0)
+    slots = LeafEngine(tpl0, False, True, device=0).slots
+    L = slots + 37
+    tpl, pack = bump_pack(12, L, kappa=25.0, seed=5)
+    shared, _ = LeafEngine(tpl, False, True, device=0).dtn_host(pack)
+    monkeypatch.setenv("HPS_DEBUG", "16")
+    alone, _ = LeafEngine(tpl, False, True, device=0).dtn_host(pack)
+    assert np.array_equal(shared, alone)
+    otpl = O.OracleTemplate(tpl.widths, 12)
+    for k in (0, L - 1):
+        ref, _, _ = O.leaf_dtn(otpl, pack[k, :3].T, None, pack[k, 3])
+        assert rel(shared[k], ref) <= TOL
+
+
 def test_two_dimensional_batch_vs_oracle():
     from paper_2503_04033_b200.engine import LeafEngine
     tpl, pack = bump_pack(9, 5, kappa=15.0, seed=4, d=2)

@@ -123,7 +123,7 @@ struct LeafParams {
   size_t slot_stride;     // doubles per slot matrix
   double* work;           // slots * slot_stride
   int* piv;               // slots * piv_stride: pivots (n_pad), then the RHS prefix table
-  int piv_stride;         // n_pad + n_pad / 16 + 16
+  int piv_stride;         // n_pad + (n_pad / 16 + 16) + m_pad: pivots, rhs_tab, rhs_g
   int colperm;            // DtN drop mode: A_ib columns in slab order (see rhs_col)
   double* scratch;        // slots * 2 n_pad * TRI_BLOCK: cached diagonal-block inverses
   const double* D1;       // d * p * p (scaled first derivative)
@@ -285,6 +285,7 @@ struct Ctx {
   int ld, n_piv, n_real, NR, wb, slot;
   int* piv;
   int* rhs_tab;  // [n_pad / 16 + 1]: RHS columns with a nonzero above row 16 g (forward solve)
+  int* rhs_g;    // [m_pad]: first row with a nonzero in RHS columns >= s (non-decreasing)
   double* scratch;
   double* smem;
   int smem_doubles;
@@ -318,7 +319,7 @@ struct Ctx {
 template <class G>
 __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, int ar, int ac,
                                        const int b_src, int br, int bc, int cr, int cc, int M, int N,
-                                       int K) {
+                                       int K, const bool kclip) {
   using S = GemmShape<G>;
   constexpr int TM = G::TM_, TN = G::TN_, KC = G::KC_, A_STRIDE = G::AS, B_STRIDE = G::BS;
   constexpr int WN = G::WN_, MI = S::MI_, NJ = S::NJ_, STAGE_A = S::SA, STAGE_DBL = S::SDBL;
@@ -342,6 +343,7 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   // the slot's claim word); mode 2 helper (compare-and-swap with the op's seq).
   __shared__ int s_gmode;
   __shared__ int s_tile_ring[STAGES];  // tile id started in each stage (-1: end)
+  __shared__ int s_kc0_ring[STAGES];   // its first k-chunk
   if (tid == 0) {
     int m = 0;
     if (c.role == 2) {
@@ -367,7 +369,7 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
 
   // producer state (thread 0 only)
   int p_it = 0, p_tile = 0, p_kc = 0, p_next = 0;
-  bool p_end = false;
+  bool p_end = false, p_in = false;
   auto claim_tile = [&]() -> int {
     if (gmode == 0) return p_next < tiles ? p_next++ : -1;
     if (gmode == 1) {
@@ -388,7 +390,8 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     const unsigned g = c.pipe + p_it;
     const unsigned s = g % STAGES, use = g / STAGES;
     if (use > 0) mbar_wait(&c.empty[s], (use - 1) & 1);
-    if (p_kc == 0) {
+    const bool first_chunk = !p_in;
+    if (!p_in) {
       p_tile = claim_tile();
       s_tile_ring[s] = p_tile;
       if (p_tile < 0) {  // end marker: a stage with no data
@@ -397,6 +400,14 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
         ++p_it;
         return;
       }
+      p_kc = 0;
+      if (kclip) {  // first B row with a nonzero in this tile's columns
+        const int g0 = c.rhs_g[(p_tile % tiles_n) * TN];
+        const int k0 = (g0 - br) / KC;
+        p_kc = k0 < 0 ? 0 : (k0 > kchunks - 1 ? kchunks - 1 : k0);
+      }
+      s_kc0_ring[s] = p_kc;
+      p_in = true;
     }
     const int tm = p_tile / tiles_n, tn = p_tile - tm * tiles_n;
     double* sa = smem + s * STAGE_DBL;
@@ -404,7 +415,7 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     mbar_expect_tx(&c.full[s], S::BYTES);
     tma_load_3d(sa, mapA, ac + p_kc * KC, ar + tm * TM, a_slot, &c.full[s]);
     tma_load_3d(sb, mapB, bc + tn * TN, br + p_kc * KC, b_slot, &c.full[s]);
-    if (sub && p_kc == 0) {  // C tile into L2 ahead of the reduce-add epilogue
+    if (sub && first_chunk) {  // C tile into L2 ahead of the reduce-add epilogue
       if (narrow) {
         for (int r = 0; r < TM; r += 8) tma_prefetch_3d(&c.maps->b_work_n, cc + tn * TN, cr + tm * TM + r, c.slot);
       } else {
@@ -413,7 +424,7 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
       }
     }
     ++p_it;
-    if (++p_kc == kchunks) p_kc = 0;
+    if (++p_kc == kchunks) p_in = false;
   };
   if (tid == 0) {
     for (int s = 0; s < STAGES - 1; ++s) produce();
@@ -426,6 +437,7 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   int tile = 0, kc = 0, it = 0, my_tiles = 0;
+  bool in_tile = false;
   // 8x8 sub-tiles of this warp that lie inside the GEMM extent (warp-uniform):
   // edge tiles skip the DMMAs on zero-filled rows / columns.
   int mv = MI, nv = NJ;
@@ -440,7 +452,7 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     const unsigned g = c.pipe + it;
     const unsigned s = g % STAGES;
     mbar_wait(&c.full[s], (g / STAGES) & 1);
-    if (kc == 0) {
+    if (!in_tile) {
       tile = reinterpret_cast<volatile int*>(s_tile_ring)[s];
       if (tile < 0) {
         __syncwarp();
@@ -448,6 +460,8 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
         ++it;
         break;
       }
+      kc = reinterpret_cast<volatile int*>(s_kc0_ring)[s];
+      in_tile = true;
       set_valid(tile);
     }
     const double* sa = smem + s * STAGE_DBL;
@@ -480,7 +494,7 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     __syncwarp();
     if (lane == 0) mbar_arrive(&c.empty[s]);
     if (++kc == kchunks) {
-      kc = 0;
+      in_tile = false;
       const int tm = tile / tiles_n, tn = tile - tm * tiles_n;
       ++my_tiles;
       if (sub) {
@@ -558,14 +572,17 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   __syncthreads();
 }
 
+// kclip: forward solve against the slab-ordered RHS (bc = first RHS column):
+// B rows above the first structural nonzero of a tile's columns are zero, so
+// each tile starts its k loop there (per-tile k offset from rhs_g).
 __device__ __forceinline__ void gemm(Ctx& c, const bool sub, const int a_src, int ar, int ac,
                                      const int b_src, int br, int bc, int cr, int cc, int M, int N,
-                                     int K) {
+                                     int K, const bool kclip = false) {
   // tall, narrow slot-only updates (the rank-32/64 steps of the LU recursion) on 256 x 32 tiles
   if (sub && a_src == 0 && b_src == 0 && N <= 64 && M >= 256 && K % 8 == 0)
-    gemm_t<GemmNarrow>(c, sub, a_src, ar, ac, b_src, br, bc, cr, cc, M, N, K);
+    gemm_t<GemmNarrow>(c, sub, a_src, ar, ac, b_src, br, bc, cr, cc, M, N, K, kclip);
   else
-    gemm_t<GemmWide>(c, sub, a_src, ar, ac, b_src, br, bc, cr, cc, M, N, K);
+    gemm_t<GemmWide>(c, sub, a_src, ar, ac, b_src, br, bc, cr, cc, M, N, K, kclip);
 }
 
 __shared__ double s_pmin, s_pmax;
@@ -1249,6 +1266,7 @@ __device__ void rhs_profile(const LeafParams& P, Ctx& c) {
   __syncthreads();
   if (2 * n_pad + m_pad > 2 * c.smem_doubles) {  // no room: no skipping
     for (int e = threadIdx.x; e < groups; e += NT) c.rhs_tab[e] = m_pad;
+    for (int e = threadIdx.x; e < m_pad; e += NT) c.rhs_g[e] = 0;
     __syncthreads();
     return;
   }
@@ -1280,6 +1298,7 @@ __device__ void rhs_profile(const LeafParams& P, Ctx& c) {
     for (int sc = m_pad - 1; sc >= 0; --sc) { run = min(run, g[sc]); g[sc] = run; }
   }
   __syncthreads();
+  for (int e = threadIdx.x; e < m_pad; e += NT) c.rhs_g[e] = g[e];
   for (int e = threadIdx.x; e < groups; e += NT) {
     const int R = 16 * e;
     int lo = 0, hi = m_pad;  // first column with g >= R
@@ -1740,6 +1759,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
   c.wb = P.wb;
   c.piv = P.piv + (size_t)slot * P.piv_stride;
   c.rhs_tab = c.piv + P.n_pad;
+  c.rhs_g = c.rhs_tab + P.n_pad / 16 + 16;
   c.scratch = P.scratch + (size_t)slot * 2 * P.n_pad * TRI_BLOCK;
   c.smem = smem;
   c.smem_doubles = P.smem_doubles;
@@ -1787,7 +1807,8 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
           const int a_src = op.kind == OP_GEMM_SET ? 1 : (op.kind == OP_GEMM_SUB_ABI ? 2 : 0);
           const int b_src = op.kind == OP_GEMM_SET_Q ? 1 : 0;
           const int N = op.dyn ? min(op.Ndim, c.rhs_tab[op.dyn >> 4]) : op.Ndim;
-          gemm(c, sub, a_src, op.ar, op.ac, b_src, op.br, op.bc, op.cr, op.cc, op.Mdim, N, op.Kdim);
+          gemm(c, sub, a_src, op.ar, op.ac, b_src, op.br, op.bc, op.cr, op.cc, op.Mdim, N, op.Kdim,
+               op.dyn != 0);
           op.Ndim = N;  // profile counters below count the work done
         }
       }
@@ -1887,6 +1908,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
         h.M = P.work + (size_t)tgt * P.slot_stride;
         h.piv = P.piv + (size_t)tgt * P.piv_stride;
         h.rhs_tab = h.piv + P.n_pad;
+        h.rhs_g = h.rhs_tab + P.n_pad / 16 + 16;
         h.scratch = P.scratch + (size_t)tgt * 2 * P.n_pad * TRI_BLOCK;
         h.sh = P.share + tgt;
         h.role = 2;
@@ -1896,7 +1918,8 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
         const int a_src = op.kind == OP_GEMM_SET ? 1 : (op.kind == OP_GEMM_SUB_ABI ? 2 : 0);
         const int b_src = op.kind == OP_GEMM_SET_Q ? 1 : 0;
         const int N = op.dyn ? min(op.Ndim, h.rhs_tab[op.dyn >> 4]) : op.Ndim;
-        gemm(h, sub, a_src, op.ar, op.ac, b_src, op.br, op.bc, op.cr, op.cc, op.Mdim, N, op.Kdim);
+        gemm(h, sub, a_src, op.ar, op.ac, b_src, op.br, op.bc, op.cr, op.cc, op.Mdim, N, op.Kdim,
+             op.dyn != 0);
         c.pipe = h.pipe;
       }
       __syncthreads();
@@ -2143,7 +2166,7 @@ static size_t slot_doubles(const hps_plan_s* P, int mode) {
   return (size_t)rows_alloc(P, mode) * NC;
 }
 
-static int piv_stride(const hps_plan_s* P) { return P->n_pad + P->n_pad / 16 + 16; }
+static int piv_stride(const hps_plan_s* P) { return P->n_pad + P->n_pad / 16 + 16 + P->m_pad; }
 
 static int ensure_workspace(hps_plan_s* P, int mode, int want_slots) {
   const size_t per = slot_doubles(P, mode);

@@ -31,6 +31,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 #include <string>
@@ -124,7 +125,10 @@ struct LeafParams {
   double* work;           // slots * slot_stride
   int* piv;               // slots * piv_stride: pivots (n_pad), then the RHS prefix table
   int piv_stride;         // n_pad + (n_pad / 16 + 16) + m_pad: pivots, rhs_tab, rhs_g
-  int colperm;            // DtN drop mode: A_ib columns in slab order (see rhs_col)
+  int colperm;            // DtN drop mode: ordered interior rows / A_ib columns (tables below)
+  const int* rowpos;      // [n]: slot row of natural interior node i
+  const int* colpos;      // [m]: slot column (after n_pad) of natural boundary DOF b
+  const int* colnat;      // [m]: natural boundary DOF in slot column s
   double* scratch;        // slots * 2 n_pad * TRI_BLOCK: cached diagonal-block inverses
   const double* D1;       // d * p * p (scaled first derivative)
   const double* D2;       // d * p * p (D1 @ D1, computed on host like the reference)
@@ -1218,29 +1222,13 @@ __device__ __forceinline__ int boundary_index(const LeafParams& P, int a, int si
   return (2 * a + side) * fd + t;
 }
 
-// DtN drop mode orders the A_ib columns (slot columns n_pad + s) by slab of the
-// interior numbering instead of by face: both axis-0 faces first (their lines
-// cross every slab), then per first index i the axis-1 / axis-2 face DOFs whose
-// lines lie in slab i.  Column s then has no nonzero above row ~ i q^(d-1) of
-// A_ib, so the forward solve L^{-1} P A_ib skips the zero prefixes (rhs_tab).
-// L = lines per face per slab.  Natural boundary index b = (2a + side) fd + t.
-__device__ __forceinline__ int rhs_col(const LeafParams& P, int b) {
-  if (!P.colperm) return b;
-  const int fd = P.d == 3 ? P.q * P.q : P.q, L = P.d == 3 ? P.q : 1;
-  const int face = b / fd, t = b - face * fd, a = face >> 1, side = face & 1;
-  if (a == 0) return side * fd + t;
-  const int i = t / L, k = t - i * L;
-  return 2 * fd + i * (2 * (P.d - 1) * L) + (a - 1) * 2 * L + side * L + k;
-}
-__device__ __forceinline__ int rhs_nat(const LeafParams& P, int s) {
-  if (!P.colperm) return s;
-  const int fd = P.d == 3 ? P.q * P.q : P.q, L = P.d == 3 ? P.q : 1;
-  if (s < 2 * fd) return s;
-  const int s2 = s - 2 * fd, blk = 2 * (P.d - 1) * L;
-  const int i = s2 / blk, r = s2 - i * blk;
-  const int a = 1 + r / (2 * L), side = (r / L) & 1, k = r % L;
-  return (2 * a + side) * fd + i * L + k;
-}
+// DtN drop mode: interior node i sits in slot row rowpos[i] and boundary DOF b
+// in A_ib slot column colpos[b] (host-built orderings, build_orderings): the
+// columns are sorted by the first slot row of their line, so the forward solve
+// L^{-1} P A_ib skips each column's zero prefix (rhs_tab / rhs_g).
+__device__ __forceinline__ int rhs_col(const LeafParams& P, int b) { return P.colperm ? P.colpos[b] : b; }
+__device__ __forceinline__ int rhs_nat(const LeafParams& P, int s) { return P.colperm ? P.colnat[s] : s; }
+__device__ __forceinline__ int slot_row(const LeafParams& P, int i) { return P.colperm ? P.rowpos[i] : i; }
 // interior rows of the axis-a line of face DOF t: base + i * stride, i < q
 __device__ __forceinline__ void line_rows(const LeafParams& P, int a, int t, int& base, int& stride) {
   const int q = P.q;
@@ -1288,7 +1276,7 @@ __device__ void rhs_profile(const LeafParams& P, Ctx& c) {
       const int b = rhs_nat(P, sc), face = b / fd;
       int base, stride;
       line_rows(P, face >> 1, b - face * fd, base, stride);
-      for (int i = 0; i < P.q; ++i) f = min(f, pinv[base + i * stride]);
+      for (int i = 0; i < P.q; ++i) f = min(f, pinv[slot_row(P, base + i * stride)]);
     }
     g[sc] = f;
   }
@@ -1445,11 +1433,22 @@ __device__ void assemble(const LeafParams& P, double* M, int leaf, double* smem)
   for (int e = threadIdx.x; e < dpp; e += NT) { D1s[e] = P.D1[e]; D2s[e] = P.D2[e]; }
   __syncthreads();
   const int npat = pattern_size(P);
+  // permuted rows (DtN drop orderings): zero the whole slot before any row is filled
+  const bool two_pass = P.colperm != 0;
+  if (two_pass) {
+    for (int r = warp; r < P.NR; r += NT / 32) {
+      double2* row2 = reinterpret_cast<double2*>(M + (size_t)r * P.ld);
+      for (int c2 = lane; c2 < P.NC / 2; c2 += 32) row2[c2] = make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+  }
   for (int r = warp; r < P.NR; r += NT / 32) {
-    double* row = M + (size_t)r * P.ld;
-    double2* row2 = reinterpret_cast<double2*>(row);
-    for (int c2 = lane; c2 < P.NC / 2; c2 += 32) row2[c2] = make_double2(0.0, 0.0);
-    __syncwarp();
+    double* row = M + (size_t)(r < P.n ? slot_row(P, r) : r) * P.ld;
+    if (!two_pass) {
+      double2* row2 = reinterpret_cast<double2*>(row);
+      for (int c2 = lane; c2 < P.NC / 2; c2 += 32) row2[c2] = make_double2(0.0, 0.0);
+      __syncwarp();
+    }
     if (r < P.n) {
       int I[3];
       interior_multi(P, r, I);
@@ -1463,7 +1462,7 @@ __device__ void assemble(const LeafParams& P, double* M, int leaf, double* smem)
 #pragma unroll
           for (int k = 0; k < 3; ++k)
             if (k < d) flat = flat * P.q + (J[k] - 1);
-          row[flat] = op_entry(P, rc, D1s, D2s, I, J);
+          row[slot_row(P, flat)] = op_entry(P, rc, D1s, D2s, I, J);
         } else if (P.legendre) {
           if (P.mode == MODE_INTERIOR) rhs += op_entry(P, rc, D1s, D2s, I, J) * qub[P.bpos[full_flat(P, J)]];
           else if (!solve_mode) row[P.col_rb + P.bpos[full_flat(P, J)]] = op_entry(P, rc, D1s, D2s, I, J);
@@ -1568,7 +1567,8 @@ __device__ bool dtn_lines_stream(const LeafParams& P, Ctx& c, const double* M, i
   __shared__ double s_e[3][2][2];
   const int q = P.q, p = P.p, d = P.d, m = P.m;
   const int S = (d == 3) ? q * q : q;
-  const int tab_d = P.colperm ? (m + 1) / 2 : 0;  // slot column -> DtN column table (ints)
+  // int tables in shared memory: slot column -> DtN column, interior node -> slot row
+  const int tab_d = P.colperm ? (m + 1) / 2 + (P.n + 1) / 2 : 0;
   int CW = 8;
   while (CW >= 2 && (2 + LINE_NBUF) * S * CW + tab_d > c.smem_doubles) CW >>= 1;
   if (CW < 2 || q > 32) return false;
@@ -1585,8 +1585,12 @@ __device__ bool dtn_lines_stream(const LeafParams& P, Ctx& c, const double* M, i
   double* acc = c.smem;              // [2][S*CW]: axis-0 lines, low / high face
   double* ring = c.smem + 2 * S * CW;  // [NBUF][S*CW]
   int* nat_tab = reinterpret_cast<int*>(ring + LINE_NBUF * S * CW);
-  if (P.colperm)
+  int* row_tab = nat_tab + m;
+  if (P.colperm) {
     for (int e = threadIdx.x; e < m; e += NT) nat_tab[e] = rhs_nat(P, e);
+    for (int e = threadIdx.x; e < P.n; e += NT) row_tab[e] = P.rowpos[e];
+  }
+  __syncthreads();
   const double* X = M + P.n_pad;
   const int fd = S;
   const int SC = S * CW;
@@ -1598,10 +1602,10 @@ __device__ bool dtn_lines_stream(const LeafParams& P, Ctx& c, const double* M, i
   auto load_slab = [&](int i, int c0) {
     if (i < q) {
       double* buf = ring + (i % LINE_NBUF) * SC;
-      const double* src = X + (size_t)(i * S) * ld + c0;
       for (int e = threadIdx.x; e < S * vec; e += NT) {
         const int r = e / vec, v = e - r * vec;
-        cp_async16(buf + r * CW + 2 * v, src + (size_t)r * ld + 2 * v, 16);
+        const double* src = X + (size_t)(P.colperm ? row_tab[i * S + r] : i * S + r) * ld + c0;
+        cp_async16(buf + r * CW + 2 * v, src + 2 * v, 16);
       }
     }
     cp_async_commit();
@@ -1713,7 +1717,7 @@ __device__ void dtn_lines(const LeafParams& P, const double* M, int ld, double* 
     for (int i = 0; i < q; ++i) {
       double x[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) x[u] = X[(size_t)(base_[u] + i * stride_[u]) * ld + xcol_[u]];
+      for (int u = 0; u < U; ++u) x[u] = X[(size_t)slot_row(P, base_[u] + i * stride_[u]) * ld + xcol_[u]];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         lo[u] += s_w[a_[u]][0][i] * x[u];
@@ -2098,6 +2102,9 @@ struct hps_plan_s {
   double* h_stage = nullptr;
   unsigned long long* prof = nullptr;  // diagnostics counters (device), optional
   int* leaf_counter = nullptr;  // [0] next leaf, [32] CTAs without a leaf (endgame sharing)
+  // DtN drop-mode orderings (device copies; host copies for the program builder)
+  int *rowpos = nullptr, *colpos = nullptr, *colnat = nullptr;
+  std::vector<int> h_fsort;  // first nonzero slot row of each slot column's line, non-decreasing
   ShareSlot* share = nullptr;
   int share_cap = 0;
   // streamed host-buffer DtN: device copies of all inputs / outputs (grow-only)
@@ -2295,6 +2302,9 @@ static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, c
   L.work = P->work; L.piv = P->piv; L.scratch = P->scratch;
   L.piv_stride = piv_stride(P);
   L.colperm = P->colperm[mode];
+  L.rowpos = P->rowpos;
+  L.colpos = P->colpos;
+  L.colnat = P->colnat;
   L.D1 = P->D1; L.D2 = P->D2; L.a_bi = P->a_bi; L.a_bb = P->a_bb;
   L.prof = P->prof;
   L.leaf_counter = P->leaf_counter;
@@ -2341,6 +2351,62 @@ int hps_device_count(void) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
   return n;
+}
+
+// Orderings for the DtN drop mode.  Interior nodes: growing cubes from a leaf
+// corner (key max_k I_k, then the natural index) — the lines of every face
+// family start late in this order, so the forward solve's zero prefixes are
+// long (sum (n - f)^2 = 0.463 n^2 m at p = 16 vs 0.545 for the natural order).
+// A_ib columns: sorted by the first slot row f of their line (stable), so the
+// columns with a nonzero above any row form a prefix.  HPS_DEBUG & 32 keeps
+// the natural interior order (columns still sorted).
+static int build_orderings(hps_plan_s* P) {
+  const int q = P->q, d = P->d, n = P->n, m = P->m;
+  const char* dbg = getenv("HPS_DEBUG");
+  const bool natural = dbg && (atoi(dbg) & 32);
+  std::vector<int> rowpos(n), colpos(m), colnat(m);
+  {
+    std::vector<long long> key(n);
+    for (int i = 0; i < n; ++i) {
+      int I[3] = {0, 0, 0}, t = i;
+      for (int k = d - 1; k >= 0; --k) { I[k] = t % q; t /= q; }
+      const int mx = std::max(I[0], std::max(I[1], d == 3 ? I[2] : 0));
+      key[i] = natural ? i : (long long)mx * n + i;
+    }
+    std::vector<int> idx(n);
+    for (int i = 0; i < n; ++i) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return key[a] < key[b]; });
+    for (int r = 0; r < n; ++r) rowpos[idx[r]] = r;
+  }
+  const int fd = (d == 3) ? q * q : q;
+  std::vector<int> f(m);
+  for (int b = 0; b < m; ++b) {
+    const int face = b / fd, t = b - face * fd, a = face >> 1;
+    int base, stride;
+    if (d == 3) {
+      if (a == 0) { base = t; stride = q * q; }
+      else if (a == 1) { base = (t / q) * q * q + t % q; stride = q; }
+      else { base = t * q; stride = 1; }
+    } else {
+      if (a == 0) { base = t; stride = q; }
+      else { base = t * q; stride = 1; }
+    }
+    int mn = n;
+    for (int k = 0; k < q; ++k) mn = std::min(mn, rowpos[base + k * stride]);
+    f[b] = mn;
+  }
+  for (int b = 0; b < m; ++b) colnat[b] = b;
+  std::stable_sort(colnat.begin(), colnat.end(), [&](int a, int b) { return f[a] < f[b]; });
+  P->h_fsort.assign(P->m_pad, 0x7fffffff);
+  for (int sc = 0; sc < m; ++sc) { colpos[colnat[sc]] = sc; P->h_fsort[sc] = f[colnat[sc]]; }
+  if (cudaMalloc(&P->rowpos, (size_t)n * 4) != cudaSuccess ||
+      cudaMalloc(&P->colpos, (size_t)m * 4) != cudaSuccess ||
+      cudaMalloc(&P->colnat, (size_t)m * 4) != cudaSuccess)
+    return fail("device allocation of orderings failed");
+  cudaMemcpy(P->rowpos, rowpos.data(), (size_t)n * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(P->colpos, colpos.data(), (size_t)m * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(P->colnat, colnat.data(), (size_t)m * 4, cudaMemcpyHostToDevice);
+  return 0;
 }
 
 static int plan_create(hps_plan_t* out, int device, int dim, int p, int legendre, int has_cross,
@@ -2408,6 +2474,7 @@ static int plan_create(hps_plan_t* out, int device, int dim, int p, int legendre
     cudaMemcpy(P->a_bi_pad, ap.data(), ap.size() * 8, cudaMemcpyHostToDevice);
     cudaMemcpy(P->bpos, bpos, full * 4, cudaMemcpyHostToDevice);
   }
+  if (!legendre && build_orderings(P) != 0) { hps_plan_destroy(P); return -1; }
   if (cudaGetLastError() != cudaSuccess) { hps_plan_destroy(P); return fail("template upload failed"); }
   *out = P;
   return 0;
@@ -2435,6 +2502,9 @@ int hps_plan_destroy(hps_plan_t P) {
   cudaFree(P->D1); cudaFree(P->D2); cudaFree(P->a_bi); cudaFree(P->a_bb);
   cudaFree(P->leaf_counter);
   cudaFree(P->share);
+  cudaFree(P->rowpos);
+  cudaFree(P->colpos);
+  cudaFree(P->colnat);
   cudaFree(P->s_coef); cudaFree(P->s_out); cudaFree(P->s_stats); cudaFree(P->s_done);
   cudaFree(P->Q); cudaFree(P->a_bi_pad); cudaFree(P->bpos);
   cudaFree(P->work); cudaFree(P->piv); cudaFree(P->scratch);

@@ -222,21 +222,38 @@ def dtn_flops(n: int, m: int) -> float:
     return 2.0 / 3.0 * n ** 3 + 2.0 * n * n * m + 2.0 * n * m * m
 
 
-def forward_prefix_rows(q: int, d: int = 3) -> np.ndarray:
-    """First structurally nonzero interior row of every A_ib column (drop mode,
-    natural i-major interior numbering, no pivoting): the zero prefix the
-    forward solve skips.  Axis-0 faces' lines start in slab 0; the lines of the
-    other faces start in the slab of their first tangential index."""
+def interior_order(q: int, d: int = 3, natural: bool = False) -> np.ndarray:
+    """Slot row of every natural interior node in the DtN drop mode (mirror of
+    build_orderings in hps_leaf.cu): growing cubes from a leaf corner, key
+    (max_k I_k, natural index)."""
+    n = q ** d
+    idx = np.arange(n)
+    if natural:
+        return idx
+    I = np.stack(np.unravel_index(idx, (q,) * d), axis=1)
+    key = I.max(axis=1).astype(np.int64) * n + idx
+    order = np.argsort(key, kind="stable")
+    rowpos = np.empty(n, dtype=np.int64)
+    rowpos[order] = np.arange(n)
+    return rowpos
+
+
+def forward_prefix_rows(q: int, d: int = 3, natural: bool = False) -> np.ndarray:
+    """First slot row of every boundary DOF's line (the zero prefix of its A_ib
+    column that the forward solve skips), natural face order."""
+    rowpos = interior_order(q, d, natural)
     if d == 3:
         t = np.arange(q * q)
-        i, k = t // q, t % q
-        f_x = t
-        f_y = i * q * q + k          # t = i q + k, rows i q^2 + j q + k
-        f_z = i * q * q + k * q      # t = i q + j, rows i q^2 + j q + k
+        bases = [(t, q * q), ((t // q) * q * q + t % q, q), (t * q, 1)]
     else:
         t = np.arange(q)
-        f_x, f_y, f_z = t, t * q, np.zeros(0, dtype=int)
-    return np.concatenate([f_x, f_x, f_y, f_y, f_z, f_z])
+        bases = [(t, q), (t * q, 1)]
+    f = []
+    for base, stride in bases:
+        rows = base[:, None] + stride * np.arange(q)[None, :]
+        fa = rowpos[rows].min(axis=1)
+        f += [fa, fa]
+    return np.concatenate(f)
 
 
 def dtn_flops_executed(n: int, m: int, q: int, d: int = 3, skip_prefix: bool = True) -> float:

@@ -124,11 +124,13 @@ struct LeafParams {
   size_t slot_stride;     // doubles per slot matrix
   double* work;           // slots * slot_stride
   int* piv;               // slots * piv_stride: pivots (n_pad), then the RHS prefix table
-  int piv_stride;         // n_pad + (n_pad / 16 + 16) + m_pad: pivots, rhs_tab, rhs_g
+  int piv_stride;         // n_pad + (n_pad / 16 + 16) + m_pad + RW: pivots, rhs_tab, rhs_g, wf
   int colperm;            // DtN drop mode: ordered interior rows / A_ib columns (tables below)
   const int* rowpos;      // [n]: slot row of natural interior node i
   const int* colpos;      // [m]: slot column (after n_pad) of natural boundary DOF b
   const int* colnat;      // [m]: natural boundary DOF in slot column s
+  const int* fsort;       // [m_pad]: first slot row of the line of slot column s (non-decreasing)
+  int wt, RW;             // W-trick DtN (T = A_bb - (A_bi U^-1)(L^-1 P A_ib)) and its row-block size
   double* scratch;        // slots * 2 n_pad * TRI_BLOCK: cached diagonal-block inverses
   const double* D1;       // d * p * p (scaled first derivative)
   const double* D2;       // d * p * p (D1 @ D1, computed on host like the reference)
@@ -251,6 +253,7 @@ struct TmaMaps {
   CUtensorMap c_red;      // box {16, 8, 1} over [slots][NR][NC]: epilogue reduce-add
   CUtensorMap a_abi;      // legendre: box {A_STRIDE, TM, 1} over the plan's a_bi [m_pad][n_pad]
   CUtensorMap b_q;        // legendre: box {B_STRIDE, KC, 1} over the plan's Q [nb_pad][m_pad]
+  CUtensorMap b_scratch;  // box {B_STRIDE, KC, 1} over [slots][2 n_pad][TRI]: inverse as B operand
   CUtensorMap a_work_n;   // narrow tiles: box {12, 256, 1} over [slots][NR][NC]
   CUtensorMap b_work_n;   // narrow tiles: box {36, 8, 1}
 };
@@ -290,6 +293,7 @@ struct Ctx {
   int* piv;
   int* rhs_tab;  // [n_pad / 16 + 1]: RHS columns with a nonzero above row 16 g (forward solve)
   int* rhs_g;    // [m_pad]: first row with a nonzero in RHS columns >= s (non-decreasing)
+  int* wf;       // [RW]: first nonzero column of each row of the current W block
   double* scratch;
   double* smem;
   int smem_doubles;
@@ -323,7 +327,7 @@ struct Ctx {
 template <class G>
 __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, int ar, int ac,
                                        const int b_src, int br, int bc, int cr, int cc, int M, int N,
-                                       int K, const bool kclip) {
+                                       int K, const int kmode) {
   using S = GemmShape<G>;
   constexpr int TM = G::TM_, TN = G::TN_, KC = G::KC_, A_STRIDE = G::AS, B_STRIDE = G::BS;
   constexpr int WN = G::WN_, MI = S::MI_, NJ = S::NJ_, STAGE_A = S::SA, STAGE_DBL = S::SDBL;
@@ -339,7 +343,8 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   const CUtensorMap* mapA = narrow ? &c.maps->a_work_n
                            : (a_src == 0 ? &c.maps->a_work
                                          : (a_src == 1 ? &c.maps->a_scratch : &c.maps->a_abi));
-  const CUtensorMap* mapB = narrow ? &c.maps->b_work_n : (b_src == 0 ? &c.maps->b_work : &c.maps->b_q);
+  const CUtensorMap* mapB = narrow ? &c.maps->b_work_n
+                           : (b_src == 0 ? &c.maps->b_work : (b_src == 1 ? &c.maps->b_q : &c.maps->b_scratch));
   const int a_slot = a_src == 2 ? 0 : c.slot, b_slot = b_src == 1 ? 0 : c.slot;
   double* C = c.M + (size_t)cr * c.ld + cc;
 
@@ -405,10 +410,12 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
         return;
       }
       p_kc = 0;
-      if (kclip) {  // first B row with a nonzero in this tile's columns
-        const int g0 = c.rhs_g[(p_tile % tiles_n) * TN];
-        const int k0 = (g0 - br) / KC;
-        p_kc = k0 < 0 ? 0 : (k0 > kchunks - 1 ? kchunks - 1 : k0);
+      if (kmode) {  // first k with a nonzero in this tile's B columns / A rows
+        int kk = 0;
+        if (kmode & 1) kk = max(kk, c.rhs_g[(p_tile % tiles_n) * TN] - br);
+        if (kmode & 2) kk = max(kk, c.wf[ar + (p_tile / tiles_n) * TM - c.n_piv] - ac);
+        const int k0 = kk / KC;
+        p_kc = k0 > kchunks - 1 ? kchunks - 1 : k0;
       }
       s_kc0_ring[s] = p_kc;
       p_in = true;
@@ -576,17 +583,19 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   __syncthreads();
 }
 
-// kclip: forward solve against the slab-ordered RHS (bc = first RHS column):
-// B rows above the first structural nonzero of a tile's columns are zero, so
-// each tile starts its k loop there (per-tile k offset from rhs_g).
+// kmode: per-tile k offsets where an operand has structural zero prefixes —
+// bit 1: B = the sorted RHS (bc = first RHS column), rows above the first
+// nonzero of the tile's columns are zero (rhs_g); bit 2: A = W-block rows
+// (ar >= n_pad), columns left of the tile's first nonzero are zero (wf).
+// The k origin is br (A column ac + k pairs with B row br + k).
 __device__ __forceinline__ void gemm(Ctx& c, const bool sub, const int a_src, int ar, int ac,
                                      const int b_src, int br, int bc, int cr, int cc, int M, int N,
-                                     int K, const bool kclip = false) {
+                                     int K, const int kmode = 0) {
   // tall, narrow slot-only updates (the rank-32/64 steps of the LU recursion) on 256 x 32 tiles
   if (sub && a_src == 0 && b_src == 0 && N <= 64 && M >= 256 && K % 8 == 0)
-    gemm_t<GemmNarrow>(c, sub, a_src, ar, ac, b_src, br, bc, cr, cc, M, N, K, kclip);
+    gemm_t<GemmNarrow>(c, sub, a_src, ar, ac, b_src, br, bc, cr, cc, M, N, K, kmode);
   else
-    gemm_t<GemmWide>(c, sub, a_src, ar, ac, b_src, br, bc, cr, cc, M, N, K, kclip);
+    gemm_t<GemmWide>(c, sub, a_src, ar, ac, b_src, br, bc, cr, cc, M, N, K, kmode);
 }
 
 __shared__ double s_pmin, s_pmax;
@@ -1172,6 +1181,9 @@ enum OpKind : int {
   OP_GEMM_SUB_ABI = 7,  // legendre: T -= a_bi (plan) * X (slot)
   OP_COPY_ABB = 8,   // legendre: T region := a_bb (rows [0,m), cols [a, a+m))
   OP_RHS_PROFILE = 9,  // rhs_tab from the pivots (zero prefixes of P A_ib's columns)
+  OP_WBLOCK_INIT = 10, // W-trick: rows [n_pad, n_pad+RW) := A_bi / A_bb rows of sorted DOFs [a, a+b)
+  OP_WBLOCK_OUT = 11,  // W-trick: T rows of sorted DOFs [a, a+b) -> DtN output (natural order)
+  OP_GEMM_SET_R = 12,  // M[c_r.., c_c..] = M[a_r.., a_c..] * scratch[b_r.., 0..]  (right inverse)
 };
 
 struct Op {
@@ -1179,6 +1191,7 @@ struct Op {
   int a, b, c, d;          // generic small-op arguments
   int ar, ac, br, bc, cr, cc, Mdim, Ndim, Kdim;  // GEMM operands (row, col offsets)
   int dyn;  // forward solve against the RHS: B rows above `dyn` are zero beyond rhs_tab[dyn/16] columns
+  int kmode;  // per-tile k offset: 1 from the tile's RHS columns (rhs_g), 2 from its W rows (wf)
 };
 
 // ---------------------------------------------------------------------------
@@ -1736,6 +1749,69 @@ __device__ void dtn_lines(const LeafParams& P, const double* M, int ld, double* 
   }
 }
 
+// W-trick DtN (drop mode).  T = A_bb - W Y with W = A_bi U^-1 (m x n) and
+// Y = L^-1 P A_ib (n x m): both triangular solves start at the first nonzero of
+// each line (W row b is zero left of f_b in the slot's interior order, Y
+// column c above the pivoted f_c), and so does the k range of W Y.  W is
+// formed in blocks of RW sorted boundary DOFs in the slot rows below A_ii;
+// the same rows hold the block's T rows in the A_ib columns.
+//   wblock_init: rows [n_pad, n_pad + RW) := [A_bi rows | A_bb rows] of the
+//   sorted DOFs s0 .. s0+R (zero elsewhere from column zc on); wf = their f.
+__device__ void wblock_init(const LeafParams& P, Ctx& c, int s0, int R, int zc) {
+  const int q = P.q, p = P.p, d = P.d, m = P.m;
+  const int fd = (d == 3) ? q * q : q;
+  __syncthreads();
+  for (int r = threadIdx.x >> 5; r < P.RW; r += NT / 32) {
+    double* row = c.M + (size_t)(c.n_piv + r) * c.ld;
+    for (int col = zc + (threadIdx.x & 31) * 2; col < P.NC; col += 64)
+      *reinterpret_cast<double2*>(row + col) = make_double2(0.0, 0.0);
+  }
+  for (int r = threadIdx.x; r < P.RW; r += NT) c.wf[r] = (r < R) ? P.fsort[s0 + r] : 0x7fffffff;
+  __syncthreads();
+  // warp per DOF: lanes over the q line nodes (+ 2 endpoints)
+  for (int r = threadIdx.x >> 5; r < R; r += NT / 32) {
+    const int lane = threadIdx.x & 31;
+    const int b = P.colnat[s0 + r];
+    const int face = b / fd, t = b - face * fd, a = face >> 1, side = face & 1;
+    int base, stride;
+    line_rows(P, a, t, base, stride);
+    const double sgn = side ? 1.0 : -1.0;
+    const double* Drow = P.D1 + (size_t)(a * p + (side ? p - 1 : 0)) * p;
+    double* row = c.M + (size_t)(c.n_piv + r) * c.ld;
+    for (int k = lane; k < q; k += 32) row[P.rowpos[base + k * stride]] = sgn * Drow[k + 1];
+    if (lane == 0) {
+      const int b_lo = (2 * a) * fd + t, b_hi = b_lo + fd;
+      row[c.n_piv + P.colpos[b_lo]] = sgn * Drow[0];
+      row[c.n_piv + P.colpos[b_hi]] = sgn * Drow[p - 1];
+    }
+  }
+  (void)m;
+  __syncthreads();
+}
+
+// T rows of sorted DOFs s0 .. s0+R -> DtN output rows colnat[s], columns in
+// natural order (staged through shared memory, coalesced both ways).
+__device__ void wblock_out(const LeafParams& P, Ctx& c, int s0, int R, int leaf) {
+  const int m = P.m;
+  double* T = P.out0 + (size_t)leaf * m * m;
+  const int rows_per = max(1, c.smem_doubles / P.m_pad);
+  __syncthreads();
+  for (int r0 = 0; r0 < R; r0 += rows_per) {
+    const int nr = min(rows_per, R - r0);
+    for (int e = threadIdx.x; e < nr * (m / 2); e += NT) {
+      const int r = e / (m / 2), j = e - r * (m / 2);
+      reinterpret_cast<double2*>(c.smem + r * P.m_pad)[j] =
+          reinterpret_cast<const double2*>(c.M + (size_t)(c.n_piv + r0 + r) * c.ld + c.n_piv)[j];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nr * m; e += NT) {
+      const int r = e / m, j = e - r * m;
+      T[(size_t)P.colnat[s0 + r0 + r] * m + j] = c.smem[r * P.m_pad + P.colpos[j]];
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     hps_leaf_kernel(LeafParams P, const Op* __restrict__ ops, int n_ops, const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(1024) double smem[];
@@ -1764,6 +1840,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
   c.piv = P.piv + (size_t)slot * P.piv_stride;
   c.rhs_tab = c.piv + P.n_pad;
   c.rhs_g = c.rhs_tab + P.n_pad / 16 + 16;
+  c.wf = c.rhs_g + P.m_pad;
   c.scratch = P.scratch + (size_t)slot * 2 * P.n_pad * TRI_BLOCK;
   c.smem = smem;
   c.smem_doubles = P.smem_doubles;
@@ -1806,21 +1883,25 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
         case OP_INV_UPPER: invert_upper(c, op.a, op.b); break;
         case OP_COPY_ABB: copy_abb(P, c, op.a); break;
         case OP_RHS_PROFILE: rhs_profile(P, c); break;
+        case OP_WBLOCK_INIT: wblock_init(P, c, op.a, op.b, op.c); break;
+        case OP_WBLOCK_OUT: wblock_out(P, c, op.a, op.b, leaf); break;
         default: {
           const bool sub = (op.kind == OP_GEMM_SUB || op.kind == OP_GEMM_SUB_ABI);
           const int a_src = op.kind == OP_GEMM_SET ? 1 : (op.kind == OP_GEMM_SUB_ABI ? 2 : 0);
-          const int b_src = op.kind == OP_GEMM_SET_Q ? 1 : 0;
+          const int b_src = op.kind == OP_GEMM_SET_Q ? 1 : (op.kind == OP_GEMM_SET_R ? 2 : 0);
           const int N = op.dyn ? min(op.Ndim, c.rhs_tab[op.dyn >> 4]) : op.Ndim;
           gemm(c, sub, a_src, op.ar, op.ac, b_src, op.br, op.bc, op.cr, op.cc, op.Mdim, N, op.Kdim,
-               op.dyn != 0);
+               op.kmode);
           op.Ndim = N;  // profile counters below count the work done
         }
       }
       if (prof && threadIdx.x == 0) {
         const long long dt = clock64() - t0;
-        prof[op.kind == OP_RHS_PROFILE ? 24 : op.kind] += dt;
+        const int pk = op.kind < OP_RHS_PROFILE ? op.kind
+                       : (op.kind == OP_RHS_PROFILE ? 24 : (op.kind == OP_GEMM_SET_R ? OP_GEMM_SET : 27));
+        prof[pk] += dt;
         if (op.kind == OP_GEMM_SUB || op.kind == OP_GEMM_SET || op.kind == OP_GEMM_SET_Q ||
-            op.kind == OP_GEMM_SUB_ABI) {
+            op.kind == OP_GEMM_SUB_ABI || op.kind == OP_GEMM_SET_R) {
           const int bucket = op.Ndim <= 64 ? 0 : (op.Ndim <= 256 ? 1 : 2);
           prof[16 + bucket] += dt;
           prof[19 + bucket] += (2ull * op.Mdim * op.Ndim * op.Kdim) >> 20;
@@ -1830,6 +1911,8 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     if (prof) t0 = clock64();
     if (P.mode == MODE_DTN && P.legendre) {
       copy_block(c.M + P.col_rb, c.ld, P.out0 + (size_t)leaf * P.m * P.m, P.m, P.m, P.m, false);
+    } else if (P.mode == MODE_DTN && P.wt) {
+      // written block by block by OP_WBLOCK_OUT
     } else if (P.mode == MODE_DTN) {
       double* T = P.out0 + (size_t)leaf * P.m * P.m;
       if ((P.debug & 2) || !dtn_lines_stream(P, c, c.M, c.ld, T)) dtn_lines(P, c.M, c.ld, T);
@@ -1913,6 +1996,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
         h.piv = P.piv + (size_t)tgt * P.piv_stride;
         h.rhs_tab = h.piv + P.n_pad;
         h.rhs_g = h.rhs_tab + P.n_pad / 16 + 16;
+        h.wf = h.rhs_g + P.m_pad;
         h.scratch = P.scratch + (size_t)tgt * 2 * P.n_pad * TRI_BLOCK;
         h.sh = P.share + tgt;
         h.role = 2;
@@ -1920,10 +2004,10 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
         const Op op = ops[s_top];
         const bool sub = (op.kind == OP_GEMM_SUB || op.kind == OP_GEMM_SUB_ABI);
         const int a_src = op.kind == OP_GEMM_SET ? 1 : (op.kind == OP_GEMM_SUB_ABI ? 2 : 0);
-        const int b_src = op.kind == OP_GEMM_SET_Q ? 1 : 0;
+        const int b_src = op.kind == OP_GEMM_SET_Q ? 1 : (op.kind == OP_GEMM_SET_R ? 2 : 0);
         const int N = op.dyn ? min(op.Ndim, h.rhs_tab[op.dyn >> 4]) : op.Ndim;
         gemm(h, sub, a_src, op.ar, op.ac, b_src, op.br, op.bc, op.cr, op.cc, op.Mdim, N, op.Kdim,
-             op.dyn != 0);
+             op.kmode);
         c.pipe = h.pipe;
       }
       __syncthreads();
@@ -1963,10 +2047,28 @@ struct ProgramBuilder {
   }
   void inv(int kind, int r0, int h) { Op o{}; o.kind = kind; o.a = r0; o.b = h; ops.push_back(o); }
   void gemm(int kind, int ar, int ac, int br, int bc, int cr, int cc, int M, int N, int K,
-            int dyn = 0) {
+            int dyn = 0, int kmode = -1) {
     if (M <= 0 || N <= 0 || K <= 0) return;
     Op o{}; o.kind = kind; o.ar = ar; o.ac = ac; o.br = br; o.bc = bc; o.cr = cr; o.cc = cc;
-    o.Mdim = M; o.Ndim = N; o.Kdim = K; o.dyn = dyn; ops.push_back(o);
+    o.Mdim = M; o.Ndim = N; o.Kdim = K; o.dyn = dyn; o.kmode = kmode < 0 ? (dyn ? 1 : 0) : kmode;
+    ops.push_back(o);
+  }
+  // W-trick right solve W U = B on the W-block rows (slot rows n_pad.., M of them),
+  // columns [c0, c0+h) of the upper-triangular recursion tree; W is zero left of
+  // column cst, so subtrees left of it are skipped and k ranges start there.
+  void trsm_right(int c0, int h, int cst, int M) {
+    if (c0 + h <= cst) return;
+    if (h <= TRI_BLOCK) {
+      inv_cached(OP_INV_UPPER, c0, h);
+      gemm(OP_GEMM_SET_R, n_pad, c0, n_pad + c0, 0, n_pad, c0, M, h, h, 0, 2);
+      return;
+    }
+    const int h1 = split16_host(h);
+    trsm_right(c0, h1, cst, M);
+    const int k0 = c0 > cst ? c0 : cst;
+    if (c0 + h1 > k0)
+      gemm(OP_GEMM_SUB, n_pad, k0, k0, c0 + h1, n_pad, c0 + h1, M, h - h1, c0 + h1 - k0, 0, 2);
+    trsm_right(c0 + h1, h - h1, cst, M);
   }
   bool dyn_rhs = false;  // forward solve against the slab-ordered A_ib: clip N by rhs_tab
   void inv_cached(int kind, int r0, int h) {
@@ -2103,8 +2205,9 @@ struct hps_plan_s {
   unsigned long long* prof = nullptr;  // diagnostics counters (device), optional
   int* leaf_counter = nullptr;  // [0] next leaf, [32] CTAs without a leaf (endgame sharing)
   // DtN drop-mode orderings (device copies; host copies for the program builder)
-  int *rowpos = nullptr, *colpos = nullptr, *colnat = nullptr;
+  int *rowpos = nullptr, *colpos = nullptr, *colnat = nullptr, *fsort = nullptr;
   std::vector<int> h_fsort;  // first nonzero slot row of each slot column's line, non-decreasing
+  int wt = 0, RW = 0;        // W-trick DtN (drop mode) and its boundary-row block
   ShareSlot* share = nullptr;
   int share_cap = 0;
   // streamed host-buffer DtN: device copies of all inputs / outputs (grow-only)
@@ -2164,6 +2267,7 @@ static int rows_alloc(const hps_plan_s* P, int mode) {
   int NR, NC;
   mode_dims(P, mode, &NR, &NC);
   if (P->legendre && mode == MODE_DTN && P->m_pad > NR) return P->m_pad;
+  if (!P->legendre && mode == MODE_DTN && P->wt) return NR + P->RW;  // W-block rows
   return NR;
 }
 
@@ -2173,7 +2277,7 @@ static size_t slot_doubles(const hps_plan_s* P, int mode) {
   return (size_t)rows_alloc(P, mode) * NC;
 }
 
-static int piv_stride(const hps_plan_s* P) { return P->n_pad + P->n_pad / 16 + 16 + P->m_pad; }
+static int piv_stride(const hps_plan_s* P) { return P->n_pad + P->n_pad / 16 + 16 + P->m_pad + P->RW; }
 
 static int ensure_workspace(hps_plan_s* P, int mode, int want_slots) {
   const size_t per = slot_doubles(P, mode);
@@ -2206,6 +2310,8 @@ static int ensure_workspace(hps_plan_s* P, int mode, int want_slots) {
           make_map(&m.a_scratch, P->scratch, TRI_BLOCK, 2 * P->n_pad, P->ws_slots, TRI_BLOCK,
                    (size_t)2 * P->n_pad * TRI_BLOCK, A_STRIDE, TM, !A_PAD) ||
           make_map(&m.c_red, P->work, NC, NR, P->ws_slots, NC, per, 16, 8) ||
+          make_map(&m.b_scratch, P->scratch, TRI_BLOCK, 2 * P->n_pad, P->ws_slots, TRI_BLOCK,
+                   (size_t)2 * P->n_pad * TRI_BLOCK, B_STRIDE, KC) ||
           make_map(&m.a_work_n, P->work, NC, NR, P->ws_slots, NC, per, GemmNarrow::AS,
                    GemmNarrow::TM_) ||
           make_map(&m.b_work_n, P->work, NC, NR, P->ws_slots, NC, per, GemmNarrow::BS,
@@ -2258,7 +2364,24 @@ static int ensure_program(hps_plan_s* P, int mode) {
   b.swaps(0, P->n_pad, P->n_pad, NW);
   b.trsm_lower(0, P->n_pad, P->n_pad, NW);
   b.dyn_rhs = false;
-  b.trsm_upper(0, P->n_pad, P->n_pad, NW);
+  const bool use_wt = mode == MODE_DTN && !P->legendre && P->wt && P->colperm[mode];
+  if (use_wt) {
+    // T = A_bb - W Y by blocks of RW sorted boundary DOFs (no backward solve)
+    for (int s0 = 0; s0 < P->m; s0 += P->RW) {
+      const int R = (P->m - s0 < P->RW) ? P->m - s0 : P->RW;
+      const int cst = P->h_fsort[s0] / 16 * 16;
+      Op o{};
+      o.kind = OP_WBLOCK_INIT; o.a = s0; o.b = R; o.c = cst;
+      b.ops.push_back(o);
+      b.trsm_right(0, P->n_pad, cst, R);
+      b.gemm(OP_GEMM_SUB, P->n_pad, cst, cst, P->n_pad, P->n_pad, P->n_pad, R, P->m, P->n_pad - cst, 0, 3);
+      Op w{};
+      w.kind = OP_WBLOCK_OUT; w.a = s0; w.b = R;
+      b.ops.push_back(w);
+    }
+  } else {
+    b.trsm_upper(0, P->n_pad, P->n_pad, NW);
+  }
   if (leg_op && mode == MODE_DTN) {  // T = a_bb - a_bi X in the (now free) R_b region
     Op o{};
     o.kind = OP_COPY_ABB;
@@ -2305,6 +2428,9 @@ static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, c
   L.rowpos = P->rowpos;
   L.colpos = P->colpos;
   L.colnat = P->colnat;
+  L.fsort = P->fsort;
+  L.wt = (mode == MODE_DTN && !P->legendre && P->wt && P->colperm[mode]) ? 1 : 0;
+  L.RW = P->RW;
   L.D1 = P->D1; L.D2 = P->D2; L.a_bi = P->a_bi; L.a_bb = P->a_bb;
   L.prof = P->prof;
   L.leaf_counter = P->leaf_counter;
@@ -2401,8 +2527,12 @@ static int build_orderings(hps_plan_s* P) {
   for (int sc = 0; sc < m; ++sc) { colpos[colnat[sc]] = sc; P->h_fsort[sc] = f[colnat[sc]]; }
   if (cudaMalloc(&P->rowpos, (size_t)n * 4) != cudaSuccess ||
       cudaMalloc(&P->colpos, (size_t)m * 4) != cudaSuccess ||
-      cudaMalloc(&P->colnat, (size_t)m * 4) != cudaSuccess)
+      cudaMalloc(&P->colnat, (size_t)m * 4) != cudaSuccess ||
+      cudaMalloc(&P->fsort, (size_t)P->m_pad * 4) != cudaSuccess)
     return fail("device allocation of orderings failed");
+  cudaMemcpy(P->fsort, P->h_fsort.data(), (size_t)P->m_pad * 4, cudaMemcpyHostToDevice);
+  P->wt = (dbg && (atoi(dbg) & 64)) ? 0 : 1;
+  P->RW = P->m_pad < 256 ? P->m_pad : 256;
   cudaMemcpy(P->rowpos, rowpos.data(), (size_t)n * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(P->colpos, colpos.data(), (size_t)m * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(P->colnat, colnat.data(), (size_t)m * 4, cudaMemcpyHostToDevice);
@@ -2505,6 +2635,7 @@ int hps_plan_destroy(hps_plan_t P) {
   cudaFree(P->rowpos);
   cudaFree(P->colpos);
   cudaFree(P->colnat);
+  cudaFree(P->fsort);
   cudaFree(P->s_coef); cudaFree(P->s_out); cudaFree(P->s_stats); cudaFree(P->s_done);
   cudaFree(P->Q); cudaFree(P->a_bi_pad); cudaFree(P->bpos);
   cudaFree(P->work); cudaFree(P->piv); cudaFree(P->scratch);

@@ -256,13 +256,24 @@ def forward_prefix_rows(q: int, d: int = 3, natural: bool = False) -> np.ndarray
     return np.concatenate(f)
 
 
-def dtn_flops_executed(n: int, m: int, q: int, d: int = 3, skip_prefix: bool = True) -> float:
-    """FLOPs of the algorithm the engine runs: getrf(n) + forward solve of the
-    m right-hand sides (each from its first nonzero row on: sum (n - f_c)^2)
-    + backward solve (n^2 m) + the line-sparse A_bi product (q = p - 2 nodes
-    per boundary row).  skip_prefix=False: dense forward solve (legendre)."""
-    fwd = float(n) * n * m
-    if skip_prefix:
-        f = forward_prefix_rows(q, d).astype(float)
-        fwd = float(((n - f) ** 2).sum())
-    return 2.0 / 3.0 * n ** 3 + fwd + float(n) * n * m + 2.0 * q * m * m
+def dtn_flops_executed(n: int, m: int, q: int, d: int = 3, skip_prefix: bool = True,
+                       wtrick: bool = True) -> float:
+    """FLOPs of the algorithm the engine runs for one leaf (drop mode):
+    getrf(n), the forward solve Y = L^-1 P A_ib from each column's first
+    nonzero row (sum (n - f_c)^2), and then either
+      wtrick:  W = A_bi U^-1 from each row's first nonzero (sum (n - f_b)^2) and
+               T -= W Y over k >= max(f_b, f_c) (sum 2 (n - max(f_b, f_c)));
+      else:    the backward solve (n^2 m) and the line-sparse A_bi X (2 q m^2).
+    f from the engine's interior order (forward_prefix_rows).  skip_prefix=False:
+    the dense variant 2/3 n^3 + 2 n^2 m + 2 q m^2 (legendre faces)."""
+    if not skip_prefix:
+        return 2.0 / 3.0 * n ** 3 + 2.0 * n * n * m + 2.0 * q * m * m
+    f = np.sort(forward_prefix_rows(q, d).astype(float))
+    fwd = float(((n - f) ** 2).sum())
+    lu = 2.0 / 3.0 * n ** 3
+    if not wtrick:
+        return lu + fwd + float(n) * n * m + 2.0 * q * m * m
+    # sum over pairs of (n - max(f_b, f_c)) with f sorted: f_j is the max for 2j+1 pairs
+    j = np.arange(f.size)
+    pairs = float(((2 * j + 1) * (n - f)).sum())
+    return lu + 2.0 * fwd + 2.0 * pairs

@@ -115,15 +115,20 @@ def test_zero_prefix_forward_solve_is_exact(p, d, monkeypatch):
     and each computed column's arithmetic does not depend on its position."""
     from paper_2503_04033_b200.engine import LeafEngine
     tpl, pack = bump_pack(p, 9, kappa=30.0, seed=11, d=d)
-    monkeypatch.setenv("HPS_DEBUG", "32")   # natural interior order, sorted columns, skipping
+    monkeypatch.setenv("HPS_DEBUG", "96")   # natural interior order, sorted columns, skipping,
+                                             # backward solve (no W blocks)
     fast, _ = LeafEngine(tpl, False, True, device=0).dtn_host(pack)
     monkeypatch.setenv("HPS_DEBUG", "4")    # natural interior order and columns, dense solve
     dense, _ = LeafEngine(tpl, False, True, device=0).dtn_host(pack)
     assert np.array_equal(fast, dense)
-    # default: corner-first interior order (different pivoting sequence, same maps to rounding)
+    # default: corner-first interior order (different pivoting sequence) and the W-block
+    # Schur complement T = A_bb - (A_bi U^-1)(L^-1 P A_ib): same maps to rounding
     monkeypatch.delenv("HPS_DEBUG")
     corner, _ = LeafEngine(tpl, False, True, device=0).dtn_host(pack)
     assert rel(corner, dense) <= TOL
+    monkeypatch.setenv("HPS_DEBUG", "64")   # corner order, backward solve
+    back, _ = LeafEngine(tpl, False, True, device=0).dtn_host(pack)
+    assert rel(back, dense) <= TOL
 
 
 def test_endgame_gemm_sharing_is_exact(monkeypatch):

@@ -254,6 +254,8 @@ struct TmaMaps {
   CUtensorMap a_abi;      // legendre: box {A_STRIDE, TM, 1} over the plan's a_bi [m_pad][n_pad]
   CUtensorMap b_q;        // legendre: box {B_STRIDE, KC, 1} over the plan's Q [nb_pad][m_pad]
   CUtensorMap b_scratch;  // box {B_STRIDE, KC, 1} over [slots][2 n_pad][TRI]: inverse as B operand
+  CUtensorMap a_work_t;   // tall tiles: box {12, 128, 1} over [slots][NR][NC]
+  CUtensorMap b_scratch_t;  // tall tiles: box {68, 8, 1} over the inverse cache
   CUtensorMap a_work_n;   // narrow tiles: box {12, 256, 1} over [slots][NR][NC]
   CUtensorMap b_work_n;   // narrow tiles: box {36, 8, 1}
 };
@@ -265,13 +267,20 @@ struct TmaMaps {
 // which use a quarter / half of a wide tile.  Both share the stage ring, the
 // mbarriers and the per-warp epilogue ring.
 struct GemmWide {
-  static constexpr int TM_ = TM, TN_ = TN, KC_ = KC, AS = A_STRIDE, BS = B_STRIDE, WN_ = WN;
+  static constexpr int TM_ = TM, TN_ = TN, KC_ = KC, AS = A_STRIDE, BS = B_STRIDE, WN_ = WN, KIND = 0;
   static constexpr bool SWZ = !A_PAD;
 };
 struct GemmNarrow {
   // k-chunk 8 (row stride 12) with a 3-stage ring; 4 (stride 4) with deeper rings
   static constexpr int TM_ = 256, TN_ = 32, KC_ = STAGES <= 3 ? 8 : 4, AS = KC_ == 8 ? 12 : 4;
-  static constexpr int BS = 36, WN_ = 1;
+  static constexpr int BS = 36, WN_ = 1, KIND = 1;
+  static constexpr bool SWZ = false;
+};
+// Tall: 128 x 64 tiles (4 x 2 warps), k-chunk 8, B stride 68, for the W-block
+// right inverses (N = 64, in place: one tile column, so no tile reads columns
+// another tile already wrote).
+struct GemmTall {
+  static constexpr int TM_ = 128, TN_ = 64, KC_ = 8, AS = 12, BS = 68, WN_ = 2, KIND = 2;
   static constexpr bool SWZ = false;
 };
 template <class G>
@@ -286,6 +295,8 @@ struct GemmShape {
 };
 constexpr int NARROW_SMEM_DBL = STAGES * GemmShape<GemmNarrow>::SDBL + (NT / 32) * EPI_DBL;
 static_assert(NARROW_SMEM_DBL * 8 <= GEMM_SMEM_BYTES, "narrow stages fit the wide GEMM smem");
+static_assert((STAGES * GemmShape<GemmTall>::SDBL + (NT / 32) * EPI_DBL) * 8 <= GEMM_SMEM_BYTES,
+              "tall stages fit the wide GEMM smem");
 
 struct Ctx {
   double* M;
@@ -331,7 +342,7 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   using S = GemmShape<G>;
   constexpr int TM = G::TM_, TN = G::TN_, KC = G::KC_, A_STRIDE = G::AS, B_STRIDE = G::BS;
   constexpr int WN = G::WN_, MI = S::MI_, NJ = S::NJ_, STAGE_A = S::SA, STAGE_DBL = S::SDBL;
-  constexpr bool narrow = (TN == 32);
+  constexpr bool narrow = (G::KIND == 1);
   if (M <= 0 || N <= 0 || K <= 0) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wm = warp / WN, wn = warp % WN;
@@ -341,9 +352,11 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   const int kchunks = K / KC;
   double* smem = c.smem;
   const CUtensorMap* mapA = narrow ? &c.maps->a_work_n
+                           : G::KIND == 2 ? &c.maps->a_work_t
                            : (a_src == 0 ? &c.maps->a_work
                                          : (a_src == 1 ? &c.maps->a_scratch : &c.maps->a_abi));
   const CUtensorMap* mapB = narrow ? &c.maps->b_work_n
+                           : G::KIND == 2 ? &c.maps->b_scratch_t
                            : (b_src == 0 ? &c.maps->b_work : (b_src == 1 ? &c.maps->b_q : &c.maps->b_scratch));
   const int a_slot = a_src == 2 ? 0 : c.slot, b_slot = b_src == 1 ? 0 : c.slot;
   double* C = c.M + (size_t)cr * c.ld + cc;
@@ -594,6 +607,8 @@ __device__ __forceinline__ void gemm(Ctx& c, const bool sub, const int a_src, in
   // tall, narrow slot-only updates (the rank-32/64 steps of the LU recursion) on 256 x 32 tiles
   if (sub && a_src == 0 && b_src == 0 && N <= 64 && M >= 256 && K % 8 == 0)
     gemm_t<GemmNarrow>(c, sub, a_src, ar, ac, b_src, br, bc, cr, cc, M, N, K, kmode);
+  else if (!sub && a_src == 0 && b_src == 2 && N <= 64 && K % 8 == 0)  // W-block right inverse
+    gemm_t<GemmTall>(c, sub, a_src, ar, ac, b_src, br, bc, cr, cc, M, N, K, kmode);
   else
     gemm_t<GemmWide>(c, sub, a_src, ar, ac, b_src, br, bc, cr, cc, M, N, K, kmode);
 }
@@ -2312,6 +2327,9 @@ static int ensure_workspace(hps_plan_s* P, int mode, int want_slots) {
           make_map(&m.c_red, P->work, NC, NR, P->ws_slots, NC, per, 16, 8) ||
           make_map(&m.b_scratch, P->scratch, TRI_BLOCK, 2 * P->n_pad, P->ws_slots, TRI_BLOCK,
                    (size_t)2 * P->n_pad * TRI_BLOCK, B_STRIDE, KC) ||
+          make_map(&m.a_work_t, P->work, NC, NR, P->ws_slots, NC, per, GemmTall::AS, GemmTall::TM_) ||
+          make_map(&m.b_scratch_t, P->scratch, TRI_BLOCK, 2 * P->n_pad, P->ws_slots, TRI_BLOCK,
+                   (size_t)2 * P->n_pad * TRI_BLOCK, GemmTall::BS, GemmTall::KC_) ||
           make_map(&m.a_work_n, P->work, NC, NR, P->ws_slots, NC, per, GemmNarrow::AS,
                    GemmNarrow::TM_) ||
           make_map(&m.b_work_n, P->work, NC, NR, P->ws_slots, NC, per, GemmNarrow::BS,

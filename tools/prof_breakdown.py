@@ -29,13 +29,13 @@ eng.lib.hps_plan_set_profile(eng.plan, ctypes.c_void_p(0))
 ms = e0.elapsed_time(e1)
 c = cnt.view(eng.slots, 28).cpu().numpy().astype(float)
 names = ["small-panel", "swaps", "inv-lower", "inv-upper", "gemm-sub", "gemm-set", "gemm-set-Q", "gemm-sub-abi", "copy-abb"]
-tot = c[:, :9].sum() + c[:, 22].sum() + c[:, 23].sum() + c[:, 24].sum()
+tot = c[:, :9].sum() + c[:, 22].sum() + c[:, 23].sum() + c[:, 24].sum() + c[:, 27].sum()
 leaves = c[:, 9].sum()
 print(f"p={a.p} leaves={a.leaves} mode={a.mode} kernel {ms:.1f} ms, {a.leaves/ms*1e3:.1f} leaves/s, "
       f"{a.leaves*dtn_flops_executed(eng.n, eng.m, a.p-2)/ms/1e9:.2f} TFLOP/s executed, "
       f"{a.leaves*dtn_flops(eng.n, eng.m)/ms/1e9:.2f} reference-equivalent")
 clk = 1.965e9
-for i, nm in list(enumerate(names)) + [(24, "rhs-profile"), (22, "assemble"), (23, "output")]:
+for i, nm in list(enumerate(names)) + [(24, "rhs-profile"), (27, "W-block io"), (22, "assemble"), (23, "output")]:
     if c[:, i].sum() == 0:
         continue
     print(f"  {nm:12s} {100*c[:, i].sum()/tot:6.2f}%   {c[:, i].sum()/leaves/clk*1e3:8.2f} ms/leaf")
@@ -52,7 +52,7 @@ gf = sum(c[:, 19 + b].sum() for b in range(3)) * 2**20
 print(f"  gemm flops/leaf {gf/leaves:.3e}; gemm-only rate per CTA {gf/(c[:, 16:19].sum())*clk/1e9:.1f} GFLOP/s "
       f"(peak 251/SM); per-leaf total {tot/leaves/clk*1e3:.1f} ms")
 # per-CTA spread (one leaf per CTA when leaves == slots): busy cycles by SM id
-busy = c[:, :9].sum(1) + c[:, 22] + c[:, 23] + c[:, 24]
+busy = c[:, :9].sum(1) + c[:, 22] + c[:, 23] + c[:, 24] + c[:, 27]
 per_leaf = busy / np.maximum(c[:, 9], 1)
 sm = c[:, 25].astype(int)
 q = np.quantile(per_leaf, [0, 0.1, 0.5, 0.9, 1.0]) / clk * 1e3

@@ -338,7 +338,7 @@ struct Ctx {
 template <class G>
 __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, int ar, int ac,
                                        const int b_src, int br, int bc, int cr, int cc, int M, int N,
-                                       int K, const int kmode) {
+                                       int K, const int kmode, const int tri) {
   using S = GemmShape<G>;
   constexpr int TM = G::TM_, TN = G::TN_, KC = G::KC_, A_STRIDE = G::AS, B_STRIDE = G::BS;
   constexpr int WN = G::WN_, MI = S::MI_, NJ = S::NJ_, STAGE_A = S::SA, STAGE_DBL = S::SDBL;
@@ -513,8 +513,20 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
             if (!decltype(edge)::value || (i < mv && j < nv)) dmma(acc[i][j], af[i], bf[j]);
       }
     };
-    if (mv == MI && nv == NJ) mainloop(std::false_type{});
-    else if (mv > 0 && nv > 0) mainloop(std::true_type{});
+    // triangular operands (explicit inverses): chunks whose part of this warp's
+    // rows / columns lies entirely in the zero triangle are skipped
+    bool zero_chunk = false;
+    if (tri) {
+      const int k_lo = kc * KC, k_hi = k_lo + KC - 1;
+      const int tm = tile / tiles_n, tn = tile - tm * tiles_n;
+      const int r_lo = tm * TM + wm * (MI * 8), r_hi = r_lo + MI * 8 - 1;
+      const int c_hi = tn * TN + wn * (NJ * 8) + NJ * 8 - 1;
+      zero_chunk = (tri == 1 && k_lo > r_hi) || (tri == 3 && k_hi < r_lo) || (tri == 2 && k_lo > c_hi);
+    }
+    if (!zero_chunk) {
+      if (mv == MI && nv == NJ) mainloop(std::false_type{});
+      else if (mv > 0 && nv > 0) mainloop(std::true_type{});
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(&c.empty[s]);
     if (++kc == kchunks) {
@@ -601,16 +613,18 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
 // nonzero of the tile's columns are zero (rhs_g); bit 2: A = W-block rows
 // (ar >= n_pad), columns left of the tile's first nonzero are zero (wf).
 // The k origin is br (A column ac + k pairs with B row br + k).
+// tri: 1 A lower-triangular, 3 A upper-triangular, 2 B upper-triangular (the
+// explicit inverses of the TRSM base blocks), 0 dense.
 __device__ __forceinline__ void gemm(Ctx& c, const bool sub, const int a_src, int ar, int ac,
                                      const int b_src, int br, int bc, int cr, int cc, int M, int N,
-                                     int K, const int kmode = 0) {
+                                     int K, const int kmode = 0, const int tri = 0) {
   // tall, narrow slot-only updates (the rank-32/64 steps of the LU recursion) on 256 x 32 tiles
   if (sub && a_src == 0 && b_src == 0 && N <= 64 && M >= 256 && K % 8 == 0)
-    gemm_t<GemmNarrow>(c, sub, a_src, ar, ac, b_src, br, bc, cr, cc, M, N, K, kmode);
+    gemm_t<GemmNarrow>(c, sub, a_src, ar, ac, b_src, br, bc, cr, cc, M, N, K, kmode, tri);
   else if (!sub && a_src == 0 && b_src == 2 && N <= 64 && K % 8 == 0)  // W-block right inverse
-    gemm_t<GemmTall>(c, sub, a_src, ar, ac, b_src, br, bc, cr, cc, M, N, K, kmode);
+    gemm_t<GemmTall>(c, sub, a_src, ar, ac, b_src, br, bc, cr, cc, M, N, K, kmode, tri);
   else
-    gemm_t<GemmWide>(c, sub, a_src, ar, ac, b_src, br, bc, cr, cc, M, N, K, kmode);
+    gemm_t<GemmWide>(c, sub, a_src, ar, ac, b_src, br, bc, cr, cc, M, N, K, kmode, tri);
 }
 
 __shared__ double s_pmin, s_pmax;
@@ -1905,8 +1919,10 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
           const int a_src = op.kind == OP_GEMM_SET ? 1 : (op.kind == OP_GEMM_SUB_ABI ? 2 : 0);
           const int b_src = op.kind == OP_GEMM_SET_Q ? 1 : (op.kind == OP_GEMM_SET_R ? 2 : 0);
           const int N = op.dyn ? min(op.Ndim, c.rhs_tab[op.dyn >> 4]) : op.Ndim;
+          const int tri = op.kind == OP_GEMM_SET ? (op.ar < P.n_pad ? 1 : 3)
+                          : (op.kind == OP_GEMM_SET_R ? 2 : 0);
           gemm(c, sub, a_src, op.ar, op.ac, b_src, op.br, op.bc, op.cr, op.cc, op.Mdim, N, op.Kdim,
-               op.kmode);
+               op.kmode, tri);
           op.Ndim = N;  // profile counters below count the work done
         }
       }
@@ -2021,8 +2037,10 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
         const int a_src = op.kind == OP_GEMM_SET ? 1 : (op.kind == OP_GEMM_SUB_ABI ? 2 : 0);
         const int b_src = op.kind == OP_GEMM_SET_Q ? 1 : (op.kind == OP_GEMM_SET_R ? 2 : 0);
         const int N = op.dyn ? min(op.Ndim, h.rhs_tab[op.dyn >> 4]) : op.Ndim;
+        const int tri = op.kind == OP_GEMM_SET ? (op.ar < P.n_pad ? 1 : 3)
+                        : (op.kind == OP_GEMM_SET_R ? 2 : 0);
         gemm(h, sub, a_src, op.ar, op.ac, b_src, op.br, op.bc, op.cr, op.cc, op.Mdim, N, op.Kdim,
-             op.kmode);
+             op.kmode, tri);
         c.pipe = h.pipe;
       }
       __syncthreads();

@@ -2425,6 +2425,14 @@ static int ensure_program(hps_plan_s* P, int mode) {
     b.ops.push_back(o);
     b.gemm(OP_GEMM_SUB_ABI, 0, 0, 0, P->n_pad, 0, col_rb, P->m_pad, P->m_pad, P->n_pad);
   }
+  if (dbg && (atoi(dbg) & 128)) {  // diagnostics: op histogram of the program
+    int hist[16] = {0};
+    for (const Op& o : b.ops) hist[o.kind & 15]++;
+    fprintf(stderr, "hps program mode %d: %zu ops:", mode, b.ops.size());
+    for (int k = 0; k < 16; ++k)
+      if (hist[k]) fprintf(stderr, " k%d=%d", k, hist[k]);
+    fprintf(stderr, "\n");
+  }
   CK(cudaMalloc(&P->prog[mode], b.ops.size() * sizeof(Op)));
   CK(cudaMemcpy(P->prog[mode], b.ops.data(), b.ops.size() * sizeof(Op), cudaMemcpyHostToDevice));
   P->prog_len[mode] = (int)b.ops.size();

@@ -107,6 +107,9 @@ struct ShareSlot {
   int pad[2];
 };
 constexpr int SHARE_MIN_TILES = 16;
+#ifndef HPS_RW
+#define HPS_RW 256  // W-trick block of sorted boundary DOFs (rows below A_ii)
+#endif
 
 struct LeafParams {
   int mode;
@@ -154,7 +157,7 @@ struct LeafParams {
                              // 16 no endgame GEMM sharing
 };
 
-constexpr int PROF_SLOTS = 28;  // 0..8 op kinds, 9 leaves, 10-14 panel steps, 15 interchanges,
+constexpr int PROF_SLOTS = 31;  // 0..8 op kinds, 9 leaves, 10-14 panel steps, 15 interchanges,
                                 // 16-18 GEMM cycles by N (<=64, <=256, >256), 19-21 their MFLOP, 22 assemble, 23 output
 
 // ---------------------------------------------------------------------------
@@ -1901,9 +1904,12 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     if (threadIdx.x == 0) { s_pmin = INFINITY; s_pmax = 0.0; }
     __syncthreads();
     if (prof && threadIdx.x == 0) { prof[22] += clock64() - t0; prof[9] += 1; }
+    int phase = 0;  // profile: 0 LU, 1 forward solve, 2 W blocks / backward solve
     for (int k = 0; k < ((P.debug & 1) ? 0 : n_ops); ++k) {
       Op op = ops[k];
       c.cur_op = k;
+      if (op.kind == OP_RHS_PROFILE) phase = 1;
+      if (op.kind == OP_WBLOCK_INIT || (phase == 1 && op.kind == OP_INV_UPPER)) phase = 2;
       if (prof) t0 = clock64();
       switch (op.kind) {
         case OP_SMALL: lu_small(c, op.a, op.b); break;
@@ -1928,6 +1934,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
       }
       if (prof && threadIdx.x == 0) {
         const long long dt = clock64() - t0;
+        prof[28 + phase] += dt;
         const int pk = op.kind < OP_RHS_PROFILE ? op.kind
                        : (op.kind == OP_RHS_PROFILE ? 24 : (op.kind == OP_GEMM_SET_R ? OP_GEMM_SET : 27));
         prof[pk] += dt;
@@ -2576,7 +2583,7 @@ static int build_orderings(hps_plan_s* P) {
     return fail("device allocation of orderings failed");
   cudaMemcpy(P->fsort, P->h_fsort.data(), (size_t)P->m_pad * 4, cudaMemcpyHostToDevice);
   P->wt = (dbg && (atoi(dbg) & 64)) ? 0 : 1;
-  P->RW = P->m_pad < 256 ? P->m_pad : 256;
+  P->RW = P->m_pad < HPS_RW ? P->m_pad : HPS_RW;
   cudaMemcpy(P->rowpos, rowpos.data(), (size_t)n * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(P->colpos, colpos.data(), (size_t)m * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(P->colnat, colnat.data(), (size_t)m * 4, cudaMemcpyHostToDevice);

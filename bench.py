@@ -226,7 +226,18 @@ def main():
     distributed = "RANK" in os.environ and "WORLD_SIZE" in os.environ  # launched by torchrun
     if distributed:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        # NCCL announces itself on stdout when the communicator is created; keep
+        # stdout for the one JSON line (fd-level redirect: the print is native)
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+            dist.barrier()
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved, 1)
+            os.close(saved)
     from paper_2503_04033_b200.engine import LeafEngine
 
     tpl, pack = make_shard(p, boxes, args.kappa, rank, world, args.leaves, field=args.field)

@@ -107,6 +107,9 @@ struct ShareSlot {
   int pad[2];
 };
 constexpr int SHARE_MIN_TILES = 16;
+#ifndef HPS_PIVOT_TAU
+#define HPS_PIVOT_TAU 0.0
+#endif
 #ifndef HPS_RW
 #define HPS_RW 256  // W-trick block of sorted boundary DOFs (rows below A_ii)
 #endif
@@ -129,7 +132,10 @@ struct LeafParams {
   int* piv;               // slots * piv_stride: pivots (n_pad), then the RHS prefix table
   int piv_stride;         // n_pad + (n_pad / 16 + 16) + m_pad + RW: pivots, rhs_tab, rhs_g, wf
   int colperm;            // DtN drop mode: ordered interior rows / A_ib columns (tables below)
-  const int* rowpos;      // [n]: slot row of natural interior node i
+  const int* rowpos;      // [n]: slot column (unknown order) of natural interior node i
+  const int* eqpos;       // [n]: slot row of node i's collocation equation (rows sorted by first nonzero)
+  const int* gsorted;     // [n_pad]: first nonzero column of the equation in slot row p (padding: p)
+  double pivot_tau;       // threshold partial pivoting factor for the sorted-row LU
   const int* colpos;      // [m]: slot column (after n_pad) of natural boundary DOF b
   const int* colnat;      // [m]: natural boundary DOF in slot column s
   const int* fsort;       // [m_pad]: first slot row of the line of slot column s (non-decreasing)
@@ -157,7 +163,7 @@ struct LeafParams {
                              // 16 no endgame GEMM sharing
 };
 
-constexpr int PROF_SLOTS = 31;  // 0..8 op kinds, 9 leaves, 10-14 panel steps, 15 interchanges,
+constexpr int PROF_SLOTS = 32;  // 0..8 op kinds, 9 leaves, 10-14 panel steps, 15 interchanges,
                                 // 16-18 GEMM cycles by N (<=64, <=256, >256), 19-21 their MFLOP, 22 assemble, 23 output
 
 // ---------------------------------------------------------------------------
@@ -308,6 +314,9 @@ struct Ctx {
   int* rhs_tab;  // [n_pad / 16 + 1]: RHS columns with a nonzero above row 16 g (forward solve)
   int* rhs_g;    // [m_pad]: first row with a nonzero in RHS columns >= s (non-decreasing)
   int* wf;       // [RW]: first nonzero column of each row of the current W block
+  int* gpos;     // [n_pad]: first nonzero column of the equation now in row p (sorted-row LU), or null
+  int* gmin16;   // [n_pad / 16 + 1]: min of gpos over 16-row groups (refreshed by OP_GMIN16)
+  double tau;    // pivot threshold (0: strict partial pivoting)
   double* scratch;
   double* smem;
   int smem_doubles;
@@ -393,7 +402,7 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   const int gmode = s_gmode;
 
   // producer state (thread 0 only)
-  int p_it = 0, p_tile = 0, p_kc = 0, p_next = 0;
+  int p_it = 0, p_tile = 0, p_kc = 0, p_next = 0, p_skipped = 0;
   bool p_end = false, p_in = false;
   auto claim_tile = [&]() -> int {
     if (gmode == 0) return p_next < tiles ? p_next++ : -1;
@@ -417,21 +426,37 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     if (use > 0) mbar_wait(&c.empty[s], (use - 1) & 1);
     const bool first_chunk = !p_in;
     if (!p_in) {
-      p_tile = claim_tile();
+      for (;;) {
+        p_tile = claim_tile();
+        if (p_tile < 0) break;
+        p_kc = 0;
+        if (!kmode) break;
+        // first k with a nonzero in this tile's B columns / A rows
+        int kk = 0;
+        if (kmode & 1) kk = max(kk, c.rhs_g[(p_tile % tiles_n) * TN] - br);
+        if (kmode & 2) kk = max(kk, c.wf[ar + (p_tile / tiles_n) * TM - c.n_piv] - ac);
+        if (kmode & 4) {  // rows of the tile: first nonzero column (16-row group minima)
+          const int r0 = ar + (p_tile / tiles_n) * TM;
+          int gm = 0x7fffffff;
+          for (int r = r0; r < r0 + TM && r < ar + M; r += 16) gm = min(gm, c.gmin16[r >> 4]);
+          kk = max(kk, gm - ac);
+          if (kk >= K) {  // the tile's rows are zero over the whole k range: C unchanged
+            ++p_skipped;
+            if (c.prof) c.prof[31] += ((unsigned long long)K * TM * TN * 2) >> 20;
+            continue;
+          }
+          if (c.prof && kk > 0) c.prof[31] += ((unsigned long long)(kk / KC) * KC * TM * TN * 2) >> 20;
+        }
+        const int k0 = kk / KC;
+        p_kc = k0 > kchunks - 1 ? kchunks - 1 : k0;
+        break;
+      }
       s_tile_ring[s] = p_tile;
       if (p_tile < 0) {  // end marker: a stage with no data
         p_end = true;
         mbar_arrive(&c.full[s]);
         ++p_it;
         return;
-      }
-      p_kc = 0;
-      if (kmode) {  // first k with a nonzero in this tile's B columns / A rows
-        int kk = 0;
-        if (kmode & 1) kk = max(kk, c.rhs_g[(p_tile % tiles_n) * TN] - br);
-        if (kmode & 2) kk = max(kk, c.wf[ar + (p_tile / tiles_n) * TM - c.n_piv] - ac);
-        const int k0 = kk / KC;
-        p_kc = k0 > kchunks - 1 ? kchunks - 1 : k0;
       }
       s_kc0_ring[s] = p_kc;
       p_in = true;
@@ -601,7 +626,7 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     __threadfence();
     __syncthreads();
     if (tid == 0) {
-      if (my_tiles > 0) atomicAdd(&c.sh->done, my_tiles);
+      if (my_tiles + p_skipped > 0) atomicAdd(&c.sh->done, my_tiles + p_skipped);
       if (gmode == 1) {
         while (*reinterpret_cast<volatile int*>(&c.sh->done) < tiles) __nanosleep(200);
         __threadfence();
@@ -907,13 +932,21 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
       if (bi == 0x7fffffff) bi = j;
       double urow[WB], rowj[WB];
 #pragma unroll
-      for (int t = 0; t < WB; ++t) {
-        rowj[t] = s_rowj[par][t];
-        urow[t] = (bi == j) ? rowj[t] : s_cand[par][bw][t];
-      }
+      for (int t = 0; t < WB; ++t) rowj[t] = s_rowj[par][t];
+      // threshold partial pivoting (sorted-row LU): keep the row in place when its
+      // entry is within a factor c.tau of the column maximum — fewer interchanges
+      // keep the equations' first-nonzero order, which the trailing updates use
+      if (c.tau > 0.0 && bi != j && fabs(rowj[j]) >= c.tau * bv) bi = j;
+#pragma unroll
+      for (int t = 0; t < WB; ++t) urow[t] = (bi == j) ? rowj[t] : s_cand[par][bw][t];
       if (tid == 0) {
         c.piv[b0 + j] = b0 + bi;
         if (c.prof && bi != j) c.prof[15] += 1;
+        if (c.gpos && bi != j) {  // the equations' first-nonzero table follows the interchange
+          const int t = c.gpos[b0 + j];
+          c.gpos[b0 + j] = c.gpos[b0 + bi];
+          c.gpos[b0 + bi] = t;
+        }
         if (b0 + j < c.n_real) {
           const double ap = fabs(urow[j]);
           s_pmin = fmin(s_pmin, ap);
@@ -1216,6 +1249,7 @@ enum OpKind : int {
   OP_WBLOCK_INIT = 10, // W-trick: rows [n_pad, n_pad+RW) := A_bi / A_bb rows of sorted DOFs [a, a+b)
   OP_WBLOCK_OUT = 11,  // W-trick: T rows of sorted DOFs [a, a+b) -> DtN output (natural order)
   OP_GEMM_SET_R = 12,  // M[c_r.., c_c..] = M[a_r.., a_c..] * scratch[b_r.., 0..]  (right inverse)
+  OP_GMIN16 = 13,      // gmin16 over rows [a, b) from gpos
 };
 
 struct Op {
@@ -1274,6 +1308,7 @@ __device__ __forceinline__ int boundary_index(const LeafParams& P, int a, int si
 __device__ __forceinline__ int rhs_col(const LeafParams& P, int b) { return P.colperm ? P.colpos[b] : b; }
 __device__ __forceinline__ int rhs_nat(const LeafParams& P, int s) { return P.colperm ? P.colnat[s] : s; }
 __device__ __forceinline__ int slot_row(const LeafParams& P, int i) { return P.colperm ? P.rowpos[i] : i; }
+__device__ __forceinline__ int eq_row(const LeafParams& P, int i) { return P.colperm ? P.eqpos[i] : i; }
 // interior rows of the axis-a line of face DOF t: base + i * stride, i < q
 __device__ __forceinline__ void line_rows(const LeafParams& P, int a, int t, int& base, int& stride) {
   const int q = P.q;
@@ -1321,7 +1356,7 @@ __device__ void rhs_profile(const LeafParams& P, Ctx& c) {
       const int b = rhs_nat(P, sc), face = b / fd;
       int base, stride;
       line_rows(P, face >> 1, b - face * fd, base, stride);
-      for (int i = 0; i < P.q; ++i) f = min(f, pinv[slot_row(P, base + i * stride)]);
+      for (int i = 0; i < P.q; ++i) f = min(f, pinv[eq_row(P, base + i * stride)]);
     }
     g[sc] = f;
   }
@@ -1488,7 +1523,7 @@ __device__ void assemble(const LeafParams& P, double* M, int leaf, double* smem)
     __syncthreads();
   }
   for (int r = warp; r < P.NR; r += NT / 32) {
-    double* row = M + (size_t)(r < P.n ? slot_row(P, r) : r) * P.ld;
+    double* row = M + (size_t)(r < P.n ? eq_row(P, r) : r) * P.ld;
     if (!two_pass) {
       double2* row2 = reinterpret_cast<double2*>(row);
       for (int c2 = lane; c2 < P.NC / 2; c2 += 32) row2[c2] = make_double2(0.0, 0.0);
@@ -1873,6 +1908,9 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
   c.rhs_tab = c.piv + P.n_pad;
   c.rhs_g = c.rhs_tab + P.n_pad / 16 + 16;
   c.wf = c.rhs_g + P.m_pad;
+  c.gpos = P.colperm ? c.wf + P.RW : nullptr;
+  c.tau = P.colperm ? P.pivot_tau : 0.0;
+  c.gmin16 = c.wf + P.RW + P.n_pad;
   c.scratch = P.scratch + (size_t)slot * 2 * P.n_pad * TRI_BLOCK;
   c.smem = smem;
   c.smem_doubles = P.smem_doubles;
@@ -1900,6 +1938,8 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     const int leaf = s_leaf;
     if (leaf >= P.n_leaves) break;
     long long t0 = clock64();
+    if (c.gpos)
+      for (int r = threadIdx.x; r < P.n_pad; r += NT) c.gpos[r] = P.gsorted[r];
     assemble(P, c.M, leaf, c.smem);
     if (threadIdx.x == 0) { s_pmin = INFINITY; s_pmax = 0.0; }
     __syncthreads();
@@ -1912,7 +1952,14 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
       if (op.kind == OP_WBLOCK_INIT || (phase == 1 && op.kind == OP_INV_UPPER)) phase = 2;
       if (prof) t0 = clock64();
       switch (op.kind) {
-        case OP_SMALL: lu_small(c, op.a, op.b); break;
+        case OP_SMALL: {
+          // rows at or beyond op.c are structurally zero in these columns (sorted equations)
+          const int np = c.n_piv, nr = c.NR;
+          if (op.c > 0) { c.n_piv = min(np, op.c); c.NR = min(nr, op.c); }
+          lu_small(c, op.a, op.b);
+          c.n_piv = np; c.NR = nr;
+          break;
+        }
         case OP_SWAP: apply_swaps(c, op.a, op.b, op.c, op.d); break;
         case OP_INV_LOWER: invert_unit_lower(c, op.a, op.b); break;
         case OP_INV_UPPER: invert_upper(c, op.a, op.b); break;
@@ -1920,6 +1967,16 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
         case OP_RHS_PROFILE: rhs_profile(P, c); break;
         case OP_WBLOCK_INIT: wblock_init(P, c, op.a, op.b, op.c); break;
         case OP_WBLOCK_OUT: wblock_out(P, c, op.a, op.b, leaf); break;
+        case OP_GMIN16: {
+          __syncthreads();
+          for (int g = (op.a >> 4) + (int)threadIdx.x; g < ((op.b + 15) >> 4); g += NT) {
+            int mn = 0x7fffffff;
+            for (int r = g * 16; r < g * 16 + 16 && r < P.n_pad; ++r) mn = min(mn, c.gpos[r]);
+            c.gmin16[g] = mn;
+          }
+          __syncthreads();
+          break;
+        }
         default: {
           const bool sub = (op.kind == OP_GEMM_SUB || op.kind == OP_GEMM_SUB_ABI);
           const int a_src = op.kind == OP_GEMM_SET ? 1 : (op.kind == OP_GEMM_SUB_ABI ? 2 : 0);
@@ -1936,7 +1993,8 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
         const long long dt = clock64() - t0;
         prof[28 + phase] += dt;
         const int pk = op.kind < OP_RHS_PROFILE ? op.kind
-                       : (op.kind == OP_RHS_PROFILE ? 24 : (op.kind == OP_GEMM_SET_R ? OP_GEMM_SET : 27));
+                       : (op.kind == OP_RHS_PROFILE ? 24
+                          : (op.kind == OP_GEMM_SET_R ? OP_GEMM_SET : (op.kind == OP_GMIN16 ? 22 : 27)));
         prof[pk] += dt;
         if (op.kind == OP_GEMM_SUB || op.kind == OP_GEMM_SET || op.kind == OP_GEMM_SET_Q ||
             op.kind == OP_GEMM_SUB_ABI || op.kind == OP_GEMM_SET_R) {
@@ -2035,6 +2093,8 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
         h.rhs_tab = h.piv + P.n_pad;
         h.rhs_g = h.rhs_tab + P.n_pad / 16 + 16;
         h.wf = h.rhs_g + P.m_pad;
+        h.gpos = P.colperm ? h.wf + P.RW : nullptr;
+        h.gmin16 = h.wf + P.RW + P.n_pad;
         h.scratch = P.scratch + (size_t)tgt * 2 * P.n_pad * TRI_BLOCK;
         h.sh = P.share + tgt;
         h.role = 2;
@@ -2080,7 +2140,13 @@ struct ProgramBuilder {
   // owner[g] = (r0, h) of the inverse whose rows currently occupy cache rows
   // [16g, 16g + 16); a block is reusable while it still owns all its rows
   std::vector<std::pair<int, int>> owner[2];
-  void small(int c0, int w) { Op o{}; o.kind = OP_SMALL; o.a = c0; o.b = w; ops.push_back(o); }
+  std::vector<int> rowlim;  // equations with a nonzero left of column k (sorted rows), else empty
+  bool tilek = false;       // per-tile k offsets in the LU trailing updates (row first-nonzero table)
+  int rlim(int k) const { return rowlim.empty() ? n_pad : rowlim[k]; }
+  void small(int c0, int w) {
+    Op o{}; o.kind = OP_SMALL; o.a = c0; o.b = w; o.c = rowlim.empty() ? 0 : rowlim[c0 + w];
+    ops.push_back(o);
+  }
   void swaps(int j0, int cnt, int lo, int hi) {
     if (hi <= lo || cnt <= 0) return;
     Op o{}; o.kind = OP_SWAP; o.a = j0; o.b = cnt; o.c = lo; o.d = hi; ops.push_back(o);
@@ -2129,6 +2195,8 @@ struct ProgramBuilder {
     }
     const int h1 = split16_host(h);
     trsm_lower(r0, h1, lo, hi);
+    // (no row clipping here: these are pivot rows, whose first nonzero does not
+    // follow their position once interchanged)
     gemm(OP_GEMM_SUB, r0 + h1, r0, r0, lo, r0 + h1, lo, h - h1, hi - lo, h1, dyn_rhs ? r0 + h1 : 0);
     trsm_lower(r0 + h1, h - h1, lo, hi);
   }
@@ -2150,7 +2218,14 @@ struct ProgramBuilder {
     lu(c0, h, NR);
     swaps(c0, h, c0 + h, c0 + w);
     trsm_lower(c0, h, c0 + h, c0 + w);
-    gemm(OP_GEMM_SUB, c0 + h, c0, c0, c0 + h, c0 + h, c0 + h, NR - c0 - h, w - h, h);
+    // trailing update: only rows with a nonzero left of column c0 + h (sorted equations),
+    // each row tile from the first nonzero column of its rows
+    const int r_end = std::min(NR, rlim(c0 + h));
+    if (tilek && r_end > c0 + h) {
+      Op o{}; o.kind = OP_GMIN16; o.a = c0 + h; o.b = r_end; ops.push_back(o);
+    }
+    gemm(OP_GEMM_SUB, c0 + h, c0, c0, c0 + h, c0 + h, c0 + h, r_end - c0 - h, w - h, h, 0,
+         tilek ? 4 : 0);
     lu(c0 + h, w - h, NR);
     swaps(c0 + h, w - h, c0, c0 + h);
   }
@@ -2245,7 +2320,10 @@ struct hps_plan_s {
   unsigned long long* prof = nullptr;  // diagnostics counters (device), optional
   int* leaf_counter = nullptr;  // [0] next leaf, [32] CTAs without a leaf (endgame sharing)
   // DtN drop-mode orderings (device copies; host copies for the program builder)
-  int *rowpos = nullptr, *colpos = nullptr, *colnat = nullptr, *fsort = nullptr;
+  int *rowpos = nullptr, *colpos = nullptr, *colnat = nullptr, *fsort = nullptr, *eqpos = nullptr;
+  std::vector<int> h_rowlim;  // [n_pad + 1]: equations with a nonzero left of column k
+  std::vector<int> h_gsorted;  // [n_pad]: first nonzero column of the equation in row p
+  int* gsorted = nullptr;
   std::vector<int> h_fsort;  // first nonzero slot row of each slot column's line, non-decreasing
   int wt = 0, RW = 0;        // W-trick DtN (drop mode) and its boundary-row block
   ShareSlot* share = nullptr;
@@ -2317,7 +2395,9 @@ static size_t slot_doubles(const hps_plan_s* P, int mode) {
   return (size_t)rows_alloc(P, mode) * NC;
 }
 
-static int piv_stride(const hps_plan_s* P) { return P->n_pad + P->n_pad / 16 + 16 + P->m_pad + P->RW; }
+static int piv_stride(const hps_plan_s* P) {
+  return P->n_pad + P->n_pad / 16 + 16 + P->m_pad + P->RW + P->n_pad + P->n_pad / 16 + 16;
+}
 
 static int ensure_workspace(hps_plan_s* P, int mode, int want_slots) {
   const size_t per = slot_doubles(P, mode);
@@ -2395,9 +2475,11 @@ static int ensure_program(hps_plan_s* P, int mode) {
   const int col_rb = P->n_pad + P->m_pad;
   if (leg_op)  // A_ib = R_b Q
     b.gemm(OP_GEMM_SET_Q, 0, col_rb, 0, 0, 0, P->n_pad, P->n_pad, P->m_pad, P->nb_pad);
-  b.lu(0, P->n_pad, NR);
   const char* dbg = getenv("HPS_DEBUG");
   P->colperm[mode] = (mode == MODE_DTN && !P->legendre && !(dbg && (atoi(dbg) & 4))) ? 1 : 0;
+  // sorted equations: each LU step touches only the rows with a nonzero left of it
+  if (P->colperm[mode] && !(dbg && (atoi(dbg) & 256))) b.tilek = true;
+  b.lu(0, P->n_pad, NR);
   if (P->colperm[mode]) {
     Op o{};
     o.kind = OP_RHS_PROFILE;
@@ -2479,6 +2561,10 @@ static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, c
   L.rowpos = P->rowpos;
   L.colpos = P->colpos;
   L.colnat = P->colnat;
+  L.eqpos = P->eqpos;
+  L.gsorted = P->gsorted;
+  L.pivot_tau = HPS_PIVOT_TAU;
+  if (const char* t = getenv("HPS_PIVOT_TAU")) L.pivot_tau = atof(t);
   L.fsort = P->fsort;
   L.wt = (mode == MODE_DTN && !P->legendre && P->wt && P->colperm[mode]) ? 1 : 0;
   L.RW = P->RW;
@@ -2542,19 +2628,63 @@ static int build_orderings(hps_plan_s* P) {
   const char* dbg = getenv("HPS_DEBUG");
   const bool natural = dbg && (atoi(dbg) & 32);
   std::vector<int> rowpos(n), colpos(m), colnat(m);
-  {
-    std::vector<long long> key(n);
-    for (int i = 0; i < n; ++i) {
-      int I[3] = {0, 0, 0}, t = i;
-      for (int k = d - 1; k >= 0; --k) { I[k] = t % q; t /= q; }
-      const int mx = std::max(I[0], std::max(I[1], d == 3 ? I[2] : 0));
-      key[i] = natural ? i : (long long)mx * n + i;
+  std::vector<int> shell(n);
+  auto coords = [&](int v, int* I) {
+    I[0] = I[1] = I[2] = 0;
+    for (int k = d - 1; k >= 0; --k) { I[k] = v % q; v /= q; }
+  };
+  // g[v]: first slot position among the nodes on v's d grid lines (v's row's
+  // first structural nonzero, and v's column's first nonzero row)
+  auto first_nonzero = [&](const std::vector<int>& pos, std::vector<int>& g) {
+    for (int v = 0; v < n; ++v) {
+      int I[3];
+      coords(v, I);
+      int mn = pos[v];
+      for (int a = 0; a < d; ++a) {
+        int J[3] = {I[0], I[1], I[2]};
+        for (int x = 0; x < q; ++x) {
+          J[a] = x;
+          int flat = 0;
+          for (int k = 0; k < d; ++k) flat = flat * q + J[k];
+          mn = std::min(mn, pos[flat]);
+        }
+      }
+      g[v] = mn;
     }
+  };
+  auto rank_by = [&](auto less, std::vector<int>& pos) {
     std::vector<int> idx(n);
     for (int i = 0; i < n; ++i) idx[i] = i;
-    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return key[a] < key[b]; });
-    for (int r = 0; r < n; ++r) rowpos[idx[r]] = r;
+    std::stable_sort(idx.begin(), idx.end(), less);
+    for (int r = 0; r < n; ++r) pos[idx[r]] = r;
+  };
+  for (int v = 0; v < n; ++v) {
+    int I[3];
+    coords(v, I);
+    shell[v] = std::max(I[0], std::max(I[1], d == 3 ? I[2] : 0));
   }
+  std::vector<int> g(n);
+  if (natural) {
+    for (int v = 0; v < n; ++v) rowpos[v] = v;
+  } else {
+    // growing cubes from a leaf corner (shell = max coordinate) ...
+    std::vector<int> corner(n);
+    rank_by([&](int a, int b) { return shell[a] != shell[b] ? shell[a] < shell[b] : a < b; }, corner);
+    // ... and within a shell by first nonzero, so each 64-row tile of the LU's
+    // trailing updates starts its k loop late (per-tile k offsets from g)
+    first_nonzero(corner, g);
+    rank_by([&](int a, int b) {
+      if (shell[a] != shell[b]) return shell[a] < shell[b];
+      if (g[a] != g[b]) return g[a] < g[b];
+      return a < b;
+    }, rowpos);
+  }
+  first_nonzero(rowpos, g);
+  // equations in the same order as the unknowns (diagonal pivots stay in place)
+  std::vector<int> eqpos(rowpos);
+  P->h_gsorted.assign(P->n_pad, 0);
+  for (int v = 0; v < n; ++v) P->h_gsorted[rowpos[v]] = g[v];
+  for (int r = n; r < P->n_pad; ++r) P->h_gsorted[r] = r;
   const int fd = (d == 3) ? q * q : q;
   std::vector<int> f(m);
   for (int b = 0; b < m; ++b) {
@@ -2582,6 +2712,11 @@ static int build_orderings(hps_plan_s* P) {
       cudaMalloc(&P->fsort, (size_t)P->m_pad * 4) != cudaSuccess)
     return fail("device allocation of orderings failed");
   cudaMemcpy(P->fsort, P->h_fsort.data(), (size_t)P->m_pad * 4, cudaMemcpyHostToDevice);
+  if (cudaMalloc(&P->eqpos, (size_t)n * 4) != cudaSuccess ||
+      cudaMalloc(&P->gsorted, (size_t)P->n_pad * 4) != cudaSuccess)
+    return fail("device allocation of orderings failed");
+  cudaMemcpy(P->eqpos, eqpos.data(), (size_t)n * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(P->gsorted, P->h_gsorted.data(), (size_t)P->n_pad * 4, cudaMemcpyHostToDevice);
   P->wt = (dbg && (atoi(dbg) & 64)) ? 0 : 1;
   P->RW = P->m_pad < HPS_RW ? P->m_pad : HPS_RW;
   cudaMemcpy(P->rowpos, rowpos.data(), (size_t)n * 4, cudaMemcpyHostToDevice);
@@ -2687,6 +2822,8 @@ int hps_plan_destroy(hps_plan_t P) {
   cudaFree(P->colpos);
   cudaFree(P->colnat);
   cudaFree(P->fsort);
+  cudaFree(P->eqpos);
+  cudaFree(P->gsorted);
   cudaFree(P->s_coef); cudaFree(P->s_out); cudaFree(P->s_stats); cudaFree(P->s_done);
   cudaFree(P->Q); cudaFree(P->a_bi_pad); cudaFree(P->bpos);
   cudaFree(P->work); cudaFree(P->piv); cudaFree(P->scratch);

@@ -19,6 +19,7 @@ library every call raises :class:`NativeUnavailableError`.
 from __future__ import annotations
 
 import ctypes
+import functools
 from typing import Optional, Tuple
 
 import numpy as np
@@ -222,19 +223,32 @@ def dtn_flops(n: int, m: int) -> float:
     return 2.0 / 3.0 * n ** 3 + 2.0 * n * n * m + 2.0 * n * m * m
 
 
+def _first_nonzero(rowpos: np.ndarray, q: int, d: int) -> np.ndarray:
+    """g[v]: smallest slot position among the nodes on v's d grid lines."""
+    pos = rowpos.reshape((q,) * d)
+    mins = [pos.min(axis=a, keepdims=True) for a in range(d)]
+    g = mins[0]
+    for mn in mins[1:]:
+        g = np.minimum(g, mn)
+    return np.broadcast_to(g, (q,) * d).reshape(-1).copy()
+
+
 def interior_order(q: int, d: int = 3, natural: bool = False) -> np.ndarray:
-    """Slot row of every natural interior node in the DtN drop mode (mirror of
-    build_orderings in hps_leaf.cu): growing cubes from a leaf corner, key
-    (max_k I_k, natural index)."""
+    """Slot position of every natural interior node in the DtN drop mode (mirror
+    of build_orderings in hps_leaf.cu): growing cubes from a leaf corner (shell =
+    max coordinate), within a shell by the first nonzero g under the plain
+    shell order, then the natural index."""
     n = q ** d
     idx = np.arange(n)
     if natural:
         return idx
     I = np.stack(np.unravel_index(idx, (q,) * d), axis=1)
-    key = I.max(axis=1).astype(np.int64) * n + idx
-    order = np.argsort(key, kind="stable")
+    shell = I.max(axis=1)
+    corner = np.empty(n, dtype=np.int64)
+    corner[np.lexsort((idx, shell))] = np.arange(n)
+    g = _first_nonzero(corner, q, d)
     rowpos = np.empty(n, dtype=np.int64)
-    rowpos[order] = np.arange(n)
+    rowpos[np.lexsort((idx, g, shell))] = np.arange(n)
     return rowpos
 
 
@@ -256,10 +270,57 @@ def forward_prefix_rows(q: int, d: int = 3, natural: bool = False) -> np.ndarray
     return np.concatenate(f)
 
 
+@functools.lru_cache(maxsize=None)
+def lu_skipped_flops(q: int, d: int = 3) -> float:
+    """Structurally zero work the LU's trailing updates skip (mirror of the op
+    program, without interchanges — 10% of the pivots; interchanges move rows
+    with their first-nonzero entry, so the count is a model): a 64-row tile
+    (256 rows for N <= 64) starts its k loop at the smallest first nonzero of
+    its rows (16-row group minima, 16-wide k chunks) and is skipped when that
+    lies beyond the k range."""
+    n = q ** d
+    n_pad = (n + 15) // 16 * 16
+    rowpos = interior_order(q, d)
+    g = _first_nonzero(rowpos, q, d)
+    gpos = np.arange(n_pad)
+    gpos[rowpos] = g
+    g16 = np.array([gpos[i:i + 16].min() for i in range(0, n_pad, 16)])
+    TN = 128
+
+    def split16(w):
+        if w > 2 * TN:
+            h = (w // 2) // TN * TN
+            return TN if h < TN else h
+        return ((w // 2 + 15) // 16) * 16
+
+    skipped = 0.0
+
+    def lu(c0, w):
+        nonlocal skipped
+        if w <= 32:
+            return
+        h = split16(w)
+        lu(c0, h)
+        r0, M, N, k0, K = c0 + h, n_pad - c0 - h, w - h, c0, h
+        TM = 256 if (N <= 64 and M >= 256) else 64
+        for tr in range(r0, r0 + M, TM):
+            gm = g16[tr // 16:min(tr + TM, r0 + M + 15) // 16].min()
+            kk = gm - k0
+            if kk >= K:
+                skipped += 2.0 * min(TM, r0 + M - tr) * N * K
+            elif kk > 0:
+                skipped += 2.0 * min(TM, r0 + M - tr) * N * (kk // 16 * 16)
+        lu(c0 + h, w - h)
+
+    lu(0, n_pad)
+    return skipped
+
+
 def dtn_flops_executed(n: int, m: int, q: int, d: int = 3, skip_prefix: bool = True,
                        wtrick: bool = True) -> float:
     """FLOPs of the algorithm the engine runs for one leaf (drop mode):
-    getrf(n), the forward solve Y = L^-1 P A_ib from each column's first
+    getrf(n) less the structurally zero tiles its trailing updates skip
+    (lu_skipped_flops), the forward solve Y = L^-1 P A_ib from each column's first
     nonzero row (sum (n - f_c)^2), and then either
       wtrick:  W = A_bi U^-1 from each row's first nonzero (sum (n - f_b)^2) and
                T -= W Y over k >= max(f_b, f_c) (sum 2 (n - max(f_b, f_c)));
@@ -270,7 +331,7 @@ def dtn_flops_executed(n: int, m: int, q: int, d: int = 3, skip_prefix: bool = T
         return 2.0 / 3.0 * n ** 3 + 2.0 * n * n * m + 2.0 * q * m * m
     f = np.sort(forward_prefix_rows(q, d).astype(float))
     fwd = float(((n - f) ** 2).sum())
-    lu = 2.0 / 3.0 * n ** 3
+    lu = 2.0 / 3.0 * n ** 3 - lu_skipped_flops(q, d)
     if not wtrick:
         return lu + fwd + float(n) * n * m + 2.0 * q * m * m
     # sum over pairs of (n - max(f_b, f_c)) with f sorted: f_j is the max for 2j+1 pairs

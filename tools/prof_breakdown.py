@@ -21,13 +21,13 @@ def run():
     else:
         eng.reduce_load(coeffs, f)
 run(); torch.cuda.synchronize()
-cnt = torch.zeros(eng.slots * 31, dtype=torch.int64, device="cuda")
+cnt = torch.zeros(eng.slots * 32, dtype=torch.int64, device="cuda")
 eng.lib.hps_plan_set_profile(eng.plan, ctypes.c_void_p(cnt.data_ptr()))
 e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
 e0.record(); run(); e1.record(); torch.cuda.synchronize()
 eng.lib.hps_plan_set_profile(eng.plan, ctypes.c_void_p(0))
 ms = e0.elapsed_time(e1)
-c = cnt.view(eng.slots, 31).cpu().numpy().astype(float)
+c = cnt.view(eng.slots, 32).cpu().numpy().astype(float)
 names = ["small-panel", "swaps", "inv-lower", "inv-upper", "gemm-sub", "gemm-set", "gemm-set-Q", "gemm-sub-abi", "copy-abb"]
 tot = c[:, :9].sum() + c[:, 22].sum() + c[:, 23].sum() + c[:, 24].sum() + c[:, 27].sum()
 leaves = c[:, 9].sum()
@@ -47,6 +47,7 @@ for b, nm in enumerate(["N<=64", "N<=256", "N>256"]):
 for i, nm in zip(range(10, 15), ["p1-utop", "p2-gather", "p3-pivot", "p4-writeback", "p5-swaps"]):
     print(f"    {nm:12s} {c[:, i].sum()/leaves/clk*1e3:8.2f} ms/leaf")
 print("  phases (all ops): " + ", ".join(f"{nm} {c[:, 28 + i].sum()/leaves/clk*1e3:.1f} ms/leaf" for i, nm in enumerate(["LU", "forward solve", "W blocks / backward"])))
+print(f"  trailing-update k ranges skipped (row first-nonzero): {c[:, 31].sum() * 2**20 / leaves:.3e} flop/leaf")
 print(f"  endgame helper time per CTA (mean over CTAs): {c[:, 26].mean()/clk*1e3:.1f} ms")
 print(f"  row interchanges per leaf: {c[:, 15].sum()/leaves:.0f} of {eng.n} pivots")
 gf = sum(c[:, 19 + b].sum() for b in range(3)) * 2**20

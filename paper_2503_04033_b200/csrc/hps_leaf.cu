@@ -493,11 +493,17 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   // 8x8 sub-tiles of this warp that lie inside the GEMM extent (warp-uniform):
   // edge tiles skip the DMMAs on zero-filled rows / columns.
   int mv = MI, nv = NJ;
+  int wg = 0;  // kmode 4: first A column with a nonzero in this warp's rows of the tile
   auto set_valid = [&](int t) {
     const int tm = t / tiles_n, tn = t - tm * tiles_n;
     const int rows = M - (tm * TM + wm * (MI * 8)), cols = N - (tn * TN + wn * (NJ * 8));
     mv = rows <= 0 ? 0 : (rows >= MI * 8 ? MI : (rows + 7) / 8);
     nv = cols <= 0 ? 0 : (cols >= NJ * 8 ? NJ : (cols + 7) / 8);
+    if (kmode & 4) {
+      const int r0 = ar + tm * TM + wm * (MI * 8);
+      wg = 0x7fffffff;
+      for (int r = r0; r < r0 + MI * 8 && r < ar + M; r += 16) wg = min(wg, c.gmin16[r >> 4]);
+    }
   };
   for (;; ++it) {
     if (tid == 0) produce();
@@ -543,13 +549,14 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     };
     // triangular operands (explicit inverses): chunks whose part of this warp's
     // rows / columns lies entirely in the zero triangle are skipped
-    bool zero_chunk = false;
+    // rows of this warp that are zero over the whole chunk (first nonzero beyond it)
+    bool zero_chunk = (kmode & 4) && (ac + kc * KC + KC <= wg);
     if (tri) {
       const int k_lo = kc * KC, k_hi = k_lo + KC - 1;
       const int tm = tile / tiles_n, tn = tile - tm * tiles_n;
       const int r_lo = tm * TM + wm * (MI * 8), r_hi = r_lo + MI * 8 - 1;
       const int c_hi = tn * TN + wn * (NJ * 8) + NJ * 8 - 1;
-      zero_chunk = (tri == 1 && k_lo > r_hi) || (tri == 3 && k_hi < r_lo) || (tri == 2 && k_lo > c_hi);
+      zero_chunk = zero_chunk || (tri == 1 && k_lo > r_hi) || (tri == 3 && k_hi < r_lo) || (tri == 2 && k_lo > c_hi);
     }
     if (!zero_chunk) {
       if (mv == MI && nv == NJ) mainloop(std::false_type{});
@@ -2195,9 +2202,11 @@ struct ProgramBuilder {
     }
     const int h1 = split16_host(h);
     trsm_lower(r0, h1, lo, hi);
-    // (no row clipping here: these are pivot rows, whose first nonzero does not
-    // follow their position once interchanged)
-    gemm(OP_GEMM_SUB, r0 + h1, r0, r0, lo, r0 + h1, lo, h - h1, hi - lo, h1, dyn_rhs ? r0 + h1 : 0);
+    // (no prefix clipping: these are pivot rows, whose first nonzero does not
+    // follow their position once interchanged; the per-row g table does)
+    if (tilek) { Op o{}; o.kind = OP_GMIN16; o.a = r0 + h1; o.b = r0 + h; ops.push_back(o); }
+    gemm(OP_GEMM_SUB, r0 + h1, r0, r0, lo, r0 + h1, lo, h - h1, hi - lo, h1, dyn_rhs ? r0 + h1 : 0,
+         (dyn_rhs ? 1 : 0) | (tilek ? 4 : 0));
     trsm_lower(r0 + h1, h - h1, lo, hi);
   }
   void trsm_upper(int r0, int h, int lo, int hi) {

@@ -271,13 +271,14 @@ def forward_prefix_rows(q: int, d: int = 3, natural: bool = False) -> np.ndarray
 
 
 @functools.lru_cache(maxsize=None)
-def lu_skipped_flops(q: int, d: int = 3) -> float:
-    """Structurally zero work the LU's trailing updates skip (mirror of the op
-    program, without interchanges — 10% of the pivots; interchanges move rows
-    with their first-nonzero entry, so the count is a model): a 64-row tile
-    (256 rows for N <= 64) starts its k loop at the smallest first nonzero of
-    its rows (16-row group minima, 16-wide k chunks) and is skipped when that
-    lies beyond the k range."""
+def leaf_work_model(q: int, d: int = 3) -> dict:
+    """Work of the engine's DtN op program for one leaf, by phase (drop mode,
+    engine orderings, no interchanges — 10% of the pivots, which move rows
+    together with their first-nonzero entry).  Mirrors the program builder:
+    GEMM tiles of 64 rows (256 for N <= 64) start their k loop at the first
+    nonzero of their rows (16-row group minima) and of their RHS columns, in
+    16-wide chunks, and are skipped when that lies beyond the k range;
+    triangular base blocks count h^2 per column; narrow panels rows * w^2."""
     n = q ** d
     n_pad = (n + 15) // 16 * 16
     rowpos = interior_order(q, d)
@@ -285,6 +286,8 @@ def lu_skipped_flops(q: int, d: int = 3) -> float:
     gpos = np.arange(n_pad)
     gpos[rowpos] = g
     g16 = np.array([gpos[i:i + 16].min() for i in range(0, n_pad, 16)])
+    fs = np.sort(forward_prefix_rows(q, d))          # RHS columns in slot order
+    m = fs.size
     TN = 128
 
     def split16(w):
@@ -293,35 +296,62 @@ def lu_skipped_flops(q: int, d: int = 3) -> float:
             return TN if h < TN else h
         return ((w // 2 + 15) // 16) * 16
 
-    skipped = 0.0
+    def sub(r0, M, k0, K, ncols, col_first=None):
+        """sum over row tiles (and column tiles) of 2 rows cols k_eff"""
+        if M <= 0 or K <= 0 or ncols <= 0:
+            return 0.0
+        TM = 256 if (ncols <= 64 and M >= 256) else 64
+        tot = 0.0
+        for tr in range(r0, r0 + M, TM):
+            rows = min(TM, r0 + M - tr)
+            kr = g16[tr // 16:(tr + rows + 15) // 16].min() - k0
+            for tc in range(0, ncols, TN):
+                cols = min(TN, ncols - tc)
+                kk = kr if col_first is None else max(kr, col_first[tc] - k0)
+                if kk >= K:
+                    continue
+                kk = max(kk, 0) // 16 * 16
+                tot += 2.0 * rows * cols * (K - kk)
+        return tot
+
+    work = {"panel": 0.0, "lu_trsm": 0.0, "lu_update": 0.0, "forward": 0.0}
+
+    def trsm_lower(r0, h, ncols, key, col_first=None, ncl=None):
+        if h <= 64:
+            nc = ncols if ncl is None else ncl(r0 + h)
+            work[key] += float(h) * h * nc
+            return
+        h1 = split16(h)
+        trsm_lower(r0, h1, ncols, key, col_first, ncl)
+        nc = ncols if ncl is None else ncl(r0 + h1)
+        work[key] += sub(r0 + h1, h - h1, r0, h1, nc, col_first)
+        trsm_lower(r0 + h1, h - h1, ncols, key, col_first, ncl)
 
     def lu(c0, w):
-        nonlocal skipped
         if w <= 32:
+            work["panel"] += float(n_pad - c0) * w * w
             return
         h = split16(w)
         lu(c0, h)
-        r0, M, N, k0, K = c0 + h, n_pad - c0 - h, w - h, c0, h
-        TM = 256 if (N <= 64 and M >= 256) else 64
-        for tr in range(r0, r0 + M, TM):
-            gm = g16[tr // 16:min(tr + TM, r0 + M + 15) // 16].min()
-            kk = gm - k0
-            if kk >= K:
-                skipped += 2.0 * min(TM, r0 + M - tr) * N * K
-            elif kk > 0:
-                skipped += 2.0 * min(TM, r0 + M - tr) * N * (kk // 16 * 16)
+        trsm_lower(c0, h, w - h, "lu_trsm")
+        work["lu_update"] += sub(c0 + h, n_pad - c0 - h, c0, h, w - h)
         lu(c0 + h, w - h)
 
     lu(0, n_pad)
-    return skipped
+    trsm_lower(0, n_pad, m, "forward", fs, lambda R: int(np.searchsorted(fs, R, side="left")))
+    j = np.arange(m)
+    f = fs.astype(float)
+    work["W"] = float(((n - f) ** 2).sum())
+    work["T"] = 2.0 * float(((2 * j + 1) * (n - f)).sum())
+    return work
 
 
 def dtn_flops_executed(n: int, m: int, q: int, d: int = 3, skip_prefix: bool = True,
                        wtrick: bool = True) -> float:
-    """FLOPs of the algorithm the engine runs for one leaf (drop mode):
-    getrf(n) less the structurally zero tiles its trailing updates skip
-    (lu_skipped_flops), the forward solve Y = L^-1 P A_ib from each column's first
-    nonzero row (sum (n - f_c)^2), and then either
+    """FLOPs of the algorithm the engine runs for one leaf (drop mode): the LU
+    and the forward solve Y = L^-1 P A_ib with their structurally zero tiles
+    skipped (leaf_work_model: rows from their first nonzero, RHS columns from
+    their line's first row), and then either
       wtrick:  W = A_bi U^-1 from each row's first nonzero (sum (n - f_b)^2) and
                T -= W Y over k >= max(f_b, f_c) (sum 2 (n - max(f_b, f_c)));
       else:    the backward solve (n^2 m) and the line-sparse A_bi X (2 q m^2).
@@ -329,12 +359,8 @@ def dtn_flops_executed(n: int, m: int, q: int, d: int = 3, skip_prefix: bool = T
     the dense variant 2/3 n^3 + 2 n^2 m + 2 q m^2 (legendre faces)."""
     if not skip_prefix:
         return 2.0 / 3.0 * n ** 3 + 2.0 * n * n * m + 2.0 * q * m * m
-    f = np.sort(forward_prefix_rows(q, d).astype(float))
-    fwd = float(((n - f) ** 2).sum())
-    lu = 2.0 / 3.0 * n ** 3 - lu_skipped_flops(q, d)
+    w = leaf_work_model(q, d)
+    lu_fwd = w["panel"] + w["lu_trsm"] + w["lu_update"] + w["forward"]
     if not wtrick:
-        return lu + fwd + float(n) * n * m + 2.0 * q * m * m
-    # sum over pairs of (n - max(f_b, f_c)) with f sorted: f_j is the max for 2j+1 pairs
-    j = np.arange(f.size)
-    pairs = float(((2 * j + 1) * (n - f)).sum())
-    return lu + 2.0 * fwd + 2.0 * pairs
+        return lu_fwd + float(n) * n * m + 2.0 * q * m * m
+    return lu_fwd + w["W"] + w["T"]

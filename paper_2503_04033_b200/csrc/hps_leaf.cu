@@ -2726,7 +2726,8 @@ static int build_orderings(hps_plan_s* P) {
     return fail("device allocation of orderings failed");
   cudaMemcpy(P->eqpos, eqpos.data(), (size_t)n * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(P->gsorted, P->h_gsorted.data(), (size_t)P->n_pad * 4, cudaMemcpyHostToDevice);
-  P->wt = (dbg && (atoi(dbg) & 64)) ? 0 : 1;
+  // W blocks pay off from p ~ 15 on (small leaves: the per-block op overheads dominate)
+  P->wt = (dbg && (atoi(dbg) & 64)) ? 0 : (P->n_pad >= 2048 ? 1 : 0);
   P->RW = P->m_pad < HPS_RW ? P->m_pad : HPS_RW;
   cudaMemcpy(P->rowpos, rowpos.data(), (size_t)n * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(P->colpos, colpos.data(), (size_t)m * 4, cudaMemcpyHostToDevice);

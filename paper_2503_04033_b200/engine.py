@@ -361,6 +361,8 @@ def dtn_flops_executed(n: int, m: int, q: int, d: int = 3, skip_prefix: bool = T
         return 2.0 / 3.0 * n ** 3 + 2.0 * n * n * m + 2.0 * q * m * m
     w = leaf_work_model(q, d)
     lu_fwd = w["panel"] + w["lu_trsm"] + w["lu_update"] + w["forward"]
+    if (n + 15) // 16 * 16 < 2048:   # the engine uses W blocks from n_pad >= 2048 on
+        wtrick = False
     if not wtrick:
         return lu_fwd + float(n) * n * m + 2.0 * q * m * m
     return lu_fwd + w["W"] + w["T"]

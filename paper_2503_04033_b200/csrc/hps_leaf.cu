@@ -837,12 +837,19 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
     }
     const bool owns = 2 * lc < WB;  // lane holds output columns 2lc, 2lc+1
     for (int g0 = b0 + warp * 8 * G; g0 < c.NR; g0 += NW * 8 * G) {
+      // all 32 rows zero in the panel (first structural nonzero beyond it): no loads
+      bool zero_rows = false;
+      if (c.gpos && g0 + 8 * G <= c.n_piv) {
+        int gm = c.gmin16[g0 >> 4];
+        for (int q = 16 - (g0 & 15); q < 8 * G; q += 16) gm = min(gm, c.gmin16[(g0 + q) >> 4]);
+        zero_rows = gm >= c0 + w;
+      }
       double af[G][8], av[G][2];
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         const int r = g0 + g * 8 + lr;
-        const bool ok = r < c.NR;
-        const double* row = c.M + (size_t)(ok ? r : c.NR - 1) * c.ld;
+        const bool ok = r < c.NR && !zero_rows;
+        const double* row = c.M + (size_t)(r < c.NR ? r : c.NR - 1) * c.ld;
 #pragma unroll
         for (int pq = 0; pq < 4; ++pq) {
           double2 v2 = make_double2(0.0, 0.0);
@@ -882,7 +889,8 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
   } else {
     for (int e = tid; e < n_cand * WB; e += NT) {
       const int r = e / WB, j = e - r * WB;
-      S[j * NS + r] = c.M[(size_t)(b0 + r) * c.ld + b0 + j];
+      const bool nz = c.gpos == nullptr || c.gmin16[(b0 + r) >> 4] < c0 + w;
+      S[j * NS + r] = nz ? c.M[(size_t)(b0 + r) * c.ld + b0 + j] : 0.0;
     }
   }
   __syncthreads();
@@ -950,9 +958,14 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
         c.piv[b0 + j] = b0 + bi;
         if (c.prof && bi != j) c.prof[15] += 1;
         if (c.gpos && bi != j) {  // the equations' first-nonzero table follows the interchange
-          const int t = c.gpos[b0 + j];
-          c.gpos[b0 + j] = c.gpos[b0 + bi];
-          c.gpos[b0 + bi] = t;
+          const int ta = c.gpos[b0 + j], tb = c.gpos[b0 + bi];
+          c.gpos[b0 + j] = tb;
+          c.gpos[b0 + bi] = ta;
+          // 16-row minima stay lower bounds (a group may only gain a smaller g)
+          int* ga = c.gmin16 + ((b0 + j) >> 4);
+          int* gb = c.gmin16 + ((b0 + bi) >> 4);
+          *ga = min(*ga, tb);
+          *gb = min(*gb, ta);
         }
         if (b0 + j < c.n_real) {
           const double ap = fabs(urow[j]);
@@ -1945,8 +1958,14 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     const int leaf = s_leaf;
     if (leaf >= P.n_leaves) break;
     long long t0 = clock64();
-    if (c.gpos)
+    if (c.gpos) {
       for (int r = threadIdx.x; r < P.n_pad; r += NT) c.gpos[r] = P.gsorted[r];
+      for (int g = threadIdx.x; g < P.n_pad / 16; g += NT) {
+        int mn = 0x7fffffff;
+        for (int r = 16 * g; r < 16 * g + 16; ++r) mn = min(mn, P.gsorted[r]);
+        c.gmin16[g] = mn;
+      }
+    }
     assemble(P, c.M, leaf, c.smem);
     if (threadIdx.x == 0) { s_pmin = INFINITY; s_pmax = 0.0; }
     __syncthreads();

@@ -131,7 +131,8 @@ struct LeafParams {
   double* work;           // slots * slot_stride
   int* piv;               // slots * piv_stride: pivots (n_pad), then the RHS prefix table
   int piv_stride;         // n_pad + (n_pad / 16 + 16) + m_pad + RW: pivots, rhs_tab, rhs_g, wf
-  int colperm;            // DtN drop mode: ordered interior rows / A_ib columns (tables below)
+  int colperm;            // DtN drop mode: A_ib columns sorted by their line's first row
+  int rowperm;            // drop mode: interior unknowns / equations in the engine's order
   const int* rowpos;      // [n]: slot column (unknown order) of natural interior node i
   const int* eqpos;       // [n]: slot row of node i's collocation equation (rows sorted by first nonzero)
   const int* gsorted;     // [n_pad]: first nonzero column of the equation in slot row p (padding: p)
@@ -1327,8 +1328,8 @@ __device__ __forceinline__ int boundary_index(const LeafParams& P, int a, int si
 // L^{-1} P A_ib skips each column's zero prefix (rhs_tab / rhs_g).
 __device__ __forceinline__ int rhs_col(const LeafParams& P, int b) { return P.colperm ? P.colpos[b] : b; }
 __device__ __forceinline__ int rhs_nat(const LeafParams& P, int s) { return P.colperm ? P.colnat[s] : s; }
-__device__ __forceinline__ int slot_row(const LeafParams& P, int i) { return P.colperm ? P.rowpos[i] : i; }
-__device__ __forceinline__ int eq_row(const LeafParams& P, int i) { return P.colperm ? P.eqpos[i] : i; }
+__device__ __forceinline__ int slot_row(const LeafParams& P, int i) { return P.rowperm ? P.rowpos[i] : i; }
+__device__ __forceinline__ int eq_row(const LeafParams& P, int i) { return P.rowperm ? P.eqpos[i] : i; }
 // interior rows of the axis-a line of face DOF t: base + i * stride, i < q
 __device__ __forceinline__ void line_rows(const LeafParams& P, int a, int t, int& base, int& stride) {
   const int q = P.q;
@@ -1534,7 +1535,7 @@ __device__ void assemble(const LeafParams& P, double* M, int leaf, double* smem)
   __syncthreads();
   const int npat = pattern_size(P);
   // permuted rows (DtN drop orderings): zero the whole slot before any row is filled
-  const bool two_pass = P.colperm != 0;
+  const bool two_pass = P.rowperm != 0;
   if (two_pass) {
     for (int r = warp; r < P.NR; r += NT / 32) {
       double2* row2 = reinterpret_cast<double2*>(M + (size_t)r * P.ld);
@@ -1621,7 +1622,7 @@ __device__ void copy_abb(const LeafParams& P, Ctx& c, int col) {
 // rows x cols block of M (ld) -> dense out (ld_out), 16-byte vectors, 8 in flight
 // per thread; cols and both row strides even.
 __device__ void copy_block(const double* src, int ld, double* out, int ld_out, int rows, int cols,
-                           bool negate) {
+                           bool negate, const int* rmap = nullptr) {
   const int c2 = cols / 2;
   const int total = rows * c2;
   for (int e0 = threadIdx.x; e0 < total; e0 += NT * 4) {
@@ -1631,7 +1632,7 @@ __device__ void copy_block(const double* src, int ld, double* out, int ld_out, i
       const int e = e0 + u * NT;
       if (e < total) {
         const int i = e / c2, j = e - i * c2;
-        v[u] = reinterpret_cast<const double2*>(src + (size_t)i * ld)[j];
+        v[u] = reinterpret_cast<const double2*>(src + (size_t)(rmap ? rmap[i] : i) * ld)[j];
       }
     }
 #pragma unroll
@@ -1668,7 +1669,7 @@ __device__ bool dtn_lines_stream(const LeafParams& P, Ctx& c, const double* M, i
   const int q = P.q, p = P.p, d = P.d, m = P.m;
   const int S = (d == 3) ? q * q : q;
   // int tables in shared memory: slot column -> DtN column, interior node -> slot row
-  const int tab_d = P.colperm ? (m + 1) / 2 + (P.n + 1) / 2 : 0;
+  const int tab_d = P.rowperm ? (m + 1) / 2 + (P.n + 1) / 2 : 0;
   int CW = 8;
   while (CW >= 2 && (2 + LINE_NBUF) * S * CW + tab_d > c.smem_doubles) CW >>= 1;
   if (CW < 2 || q > 32) return false;
@@ -1686,7 +1687,7 @@ __device__ bool dtn_lines_stream(const LeafParams& P, Ctx& c, const double* M, i
   double* ring = c.smem + 2 * S * CW;  // [NBUF][S*CW]
   int* nat_tab = reinterpret_cast<int*>(ring + LINE_NBUF * S * CW);
   int* row_tab = nat_tab + m;
-  if (P.colperm) {
+  if (P.rowperm) {
     for (int e = threadIdx.x; e < m; e += NT) nat_tab[e] = rhs_nat(P, e);
     for (int e = threadIdx.x; e < P.n; e += NT) row_tab[e] = P.rowpos[e];
   }
@@ -1704,7 +1705,7 @@ __device__ bool dtn_lines_stream(const LeafParams& P, Ctx& c, const double* M, i
       double* buf = ring + (i % LINE_NBUF) * SC;
       for (int e = threadIdx.x; e < S * vec; e += NT) {
         const int r = e / vec, v = e - r * vec;
-        const double* src = X + (size_t)(P.colperm ? row_tab[i * S + r] : i * S + r) * ld + c0;
+        const double* src = X + (size_t)(P.rowperm ? row_tab[i * S + r] : i * S + r) * ld + c0;
         cp_async16(buf + r * CW + 2 * v, src + 2 * v, 16);
       }
     }
@@ -1716,7 +1717,7 @@ __device__ bool dtn_lines_stream(const LeafParams& P, Ctx& c, const double* M, i
     int nat[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
-      nat[u] = (col0 + u >= m) ? -1 : (P.colperm ? nat_tab[col0 + u] : col0 + u);
+      nat[u] = (col0 + u >= m) ? -1 : (P.rowperm ? nat_tab[col0 + u] : col0 + u);
       const int col = nat[u];
       const double abb = col == b_lo ? e2[0] : (col == b_hi ? e2[1] : 0.0);
       o[u] = neg ? abb - o[u] : abb + o[u];
@@ -1928,8 +1929,8 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
   c.rhs_tab = c.piv + P.n_pad;
   c.rhs_g = c.rhs_tab + P.n_pad / 16 + 16;
   c.wf = c.rhs_g + P.m_pad;
-  c.gpos = P.colperm ? c.wf + P.RW : nullptr;
-  c.tau = P.colperm ? P.pivot_tau : 0.0;
+  c.gpos = P.rowperm ? c.wf + P.RW : nullptr;
+  c.tau = P.rowperm ? P.pivot_tau : 0.0;
   c.gmin16 = c.wf + P.RW + P.n_pad;
   c.scratch = P.scratch + (size_t)slot * 2 * P.n_pad * TRI_BLOCK;
   c.smem = smem;
@@ -2039,11 +2040,12 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
       double* T = P.out0 + (size_t)leaf * P.m * P.m;
       if ((P.debug & 2) || !dtn_lines_stream(P, c, c.M, c.ld, T)) dtn_lines(P, c.M, c.ld, T);
     } else if (P.mode == MODE_SOLOP) {
-      copy_block(c.M + P.n_pad, c.ld, P.out0 + (size_t)leaf * P.n * P.m, P.m, P.n, P.m, true);
+      copy_block(c.M + P.n_pad, c.ld, P.out0 + (size_t)leaf * P.n * P.m, P.m, P.n, P.m, true,
+                 P.rowperm ? P.rowpos : nullptr);
     } else {
       double* out = P.out0 + (size_t)leaf * P.n;
       if (P.mode == MODE_REDUCE) {
-        for (int i = threadIdx.x; i < P.n; i += NT) out[i] = c.M[(size_t)i * c.ld + P.n_pad];
+        for (int i = threadIdx.x; i < P.n; i += NT) out[i] = c.M[(size_t)slot_row(P, i) * c.ld + P.n_pad];
         __syncthreads();
         // flux = A_bi v : warp per boundary row, lanes stride the interior
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -2058,7 +2060,8 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
         }
       } else {
         const double* v = P.in1 + (size_t)leaf * P.n;
-        for (int i = threadIdx.x; i < P.n; i += NT) out[i] = v[i] - c.M[(size_t)i * c.ld + P.n_pad];
+        for (int i = threadIdx.x; i < P.n; i += NT)
+          out[i] = v[i] - c.M[(size_t)slot_row(P, i) * c.ld + P.n_pad];
       }
     }
     if (threadIdx.x == 0) {
@@ -2119,7 +2122,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
         h.rhs_tab = h.piv + P.n_pad;
         h.rhs_g = h.rhs_tab + P.n_pad / 16 + 16;
         h.wf = h.rhs_g + P.m_pad;
-        h.gpos = P.colperm ? h.wf + P.RW : nullptr;
+        h.gpos = P.rowperm ? h.wf + P.RW : nullptr;
         h.gmin16 = h.wf + P.RW + P.n_pad;
         h.scratch = P.scratch + (size_t)tgt * 2 * P.n_pad * TRI_BLOCK;
         h.sh = P.share + tgt;
@@ -2339,6 +2342,7 @@ struct hps_plan_s {
   size_t work_doubles = 0;
   int* piv = nullptr;
   int colperm[4] = {0, 0, 0, 0};
+  int rowperm[4] = {0, 0, 0, 0};
   double* scratch = nullptr;
   int ws_slots = 0;
   // unrolled LU programs per mode (device copies)
@@ -2505,8 +2509,10 @@ static int ensure_program(hps_plan_s* P, int mode) {
     b.gemm(OP_GEMM_SET_Q, 0, col_rb, 0, 0, 0, P->n_pad, P->n_pad, P->m_pad, P->nb_pad);
   const char* dbg = getenv("HPS_DEBUG");
   P->colperm[mode] = (mode == MODE_DTN && !P->legendre && !(dbg && (atoi(dbg) & 4))) ? 1 : 0;
-  // sorted equations: each LU step touches only the rows with a nonzero left of it
-  if (P->colperm[mode] && !(dbg && (atoi(dbg) & 256))) b.tilek = true;
+  // interior order with the LU's zero skipping: every drop-mode program (the
+  // solve modes keep natural rhs / output order through the tables)
+  P->rowperm[mode] = (!P->legendre && !(dbg && (atoi(dbg) & 4))) ? 1 : 0;
+  if (P->rowperm[mode] && !(dbg && (atoi(dbg) & 256))) b.tilek = true;
   b.lu(0, P->n_pad, NR);
   if (P->colperm[mode]) {
     Op o{};
@@ -2586,6 +2592,7 @@ static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, c
   L.work = P->work; L.piv = P->piv; L.scratch = P->scratch;
   L.piv_stride = piv_stride(P);
   L.colperm = P->colperm[mode];
+  L.rowperm = P->rowperm[mode];
   L.rowpos = P->rowpos;
   L.colpos = P->colpos;
   L.colnat = P->colnat;

@@ -2171,6 +2171,7 @@ struct ProgramBuilder {
   std::vector<std::pair<int, int>> owner[2];
   std::vector<int> rowlim;  // equations with a nonzero left of column k (sorted rows), else empty
   bool tilek = false;       // per-tile k offsets in the LU trailing updates (row first-nonzero table)
+  int small_panel = SMALL_PANEL;  // recursion leaf width (<= 32)
   int rlim(int k) const { return rowlim.empty() ? n_pad : rowlim[k]; }
   void small(int c0, int w) {
     Op o{}; o.kind = OP_SMALL; o.a = c0; o.b = w; o.c = rowlim.empty() ? 0 : rowlim[c0 + w];
@@ -2244,7 +2245,7 @@ struct ProgramBuilder {
     trsm_upper(r0, h1, lo, hi);
   }
   void lu(int c0, int w, int NR) {
-    if (w <= SMALL_PANEL) { small(c0, w); return; }
+    if (w <= small_panel) { small(c0, w); return; }
     const int h = split16_host(w);
     lu(c0, h, NR);
     swaps(c0, h, c0 + h, c0 + w);
@@ -2513,6 +2514,7 @@ static int ensure_program(hps_plan_s* P, int mode) {
   // solve modes keep natural rhs / output order through the tables)
   P->rowperm[mode] = (!P->legendre && !(dbg && (atoi(dbg) & 4))) ? 1 : 0;
   if (P->rowperm[mode] && !(dbg && (atoi(dbg) & 256))) b.tilek = true;
+  if (const char* sp = getenv("HPS_SMALL_PANEL")) b.small_panel = std::max(16, std::min(32, atoi(sp)));
   b.lu(0, P->n_pad, NR);
   if (P->colperm[mode]) {
     Op o{};

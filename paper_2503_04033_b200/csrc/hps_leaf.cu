@@ -803,20 +803,18 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
       T[kk * 32 + q] = c.M[(size_t)(c0 + kk) * c.ld + c0 + q];
     }
     __syncthreads();
-    if (warp == 0) {
-      for (int kk = 0; kk < done; ++kk) {
-        double p[WB];
-        const double t = (lane < kk) ? T[kk * 32 + lane] : 0.0;
-#pragma unroll
-        for (int j = 0; j < WB; ++j) p[j] = (lane < kk) ? t * Ut[j * 32 + lane] : 0.0;
-        int jj;
-        const double sum = reduce_scatter<WB>(p, lane, jj);
-        const double v = T[kk * 32 + done + jj] - sum;
-        if ((lane & (GROUP - 1)) == 0) {
-          Ut[jj * 32 + kk] = v;
-          c.M[(size_t)(c0 + kk) * c.ld + b0 + jj] = v;
-        }
-        __syncwarp();
+    // warp j solves column j of the block by right-looking substitution with the
+    // panel's unit-lower L: lane i holds x_i; one broadcast + one FMA per step
+    if (warp < WB) {
+      const int jj = warp;
+      double x = (lane < done) ? T[lane * 32 + done + jj] : 0.0;
+      for (int kk = 0; kk + 1 < done; ++kk) {
+        const double xk = __shfl_sync(0xffffffffu, x, kk);
+        if (lane > kk && lane < done) x -= T[lane * 32 + kk] * xk;
+      }
+      if (lane < done) {
+        Ut[jj * 32 + lane] = x;
+        c.M[(size_t)(c0 + lane) * c.ld + b0 + jj] = x;
       }
     }
     __syncthreads();

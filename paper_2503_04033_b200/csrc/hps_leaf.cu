@@ -752,34 +752,10 @@ __shared__ int s_pi[2][NT / 32];
 __shared__ double s_cand[2][NT / 32][8];
 __shared__ double s_rowj[2][8];
 
-// Lane-sum of p[j] over the warp; on return lane holds the full sum for column
-// jout (= the high bits of lane after log2(WB) halving steps).
-template <int WB>
-__device__ __forceinline__ double reduce_scatter(double (&p)[WB], int lane, int& jout) {
-  int jb = 0;
-#pragma unroll
-  for (int half = WB / 2, off = 16; half >= 1; half /= 2, off /= 2) {
-    const bool up = (lane & off) != 0;
-#pragma unroll
-    for (int i = 0; i < half; ++i) {
-      const double send = up ? p[i] : p[i + half];
-      const double keep = up ? p[i + half] : p[i];
-      p[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-    }
-    if (up) jb += half;
-  }
-  double v = p[0];
-#pragma unroll
-  for (int off = 16 / WB; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-  jout = jb;
-  return v;
-}
-
 template <int WB>
 __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
-  constexpr int GROUP = 32 / WB;  // lanes sharing one column of the reduce-scatter
   const int n_cand = c.n_piv - b0;
   const int done = b0 - c0, len = done + WB;
   double* S = c.smem;                          // column-major [WB][n_cand]: S[j * NS + r]

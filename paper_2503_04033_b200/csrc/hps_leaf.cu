@@ -318,6 +318,8 @@ struct Ctx {
   int* gpos;     // [n_pad]: first nonzero column of the equation now in row p (sorted-row LU), or null
   int* gmin16;   // [n_pad / 16 + 1]: min of gpos over 16-row groups (refreshed by OP_GMIN16)
   double tau;    // pivot threshold (0: strict partial pivoting)
+  int* gcol16;   // [n_pad / 16 + 1]: first row of U with a nonzero, per 16 columns (symmetric
+                 // pattern: = gmin16 at leaf start); [-1]: first interchange step, a floor
   double* scratch;
   double* smem;
   int smem_doubles;
@@ -436,6 +438,12 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
         int kk = 0;
         if (kmode & 1) kk = max(kk, c.rhs_g[(p_tile % tiles_n) * TN] - br);
         if (kmode & 2) kk = max(kk, c.wf[ar + (p_tile / tiles_n) * TM - c.n_piv] - ac);
+        if (kmode & 8) {  // columns of the tile: first row of U with a nonzero (16-column minima)
+          const int cb = bc + (p_tile % tiles_n) * TN;
+          int gm = c.gcol16[-1];
+          for (int cq = cb; cq < cb + TN && cq < bc + N; cq += 16) gm = min(gm, c.gcol16[cq >> 4]);
+          kk = max(kk, gm - br);
+        }
         if (kmode & 4) {  // rows of the tile: first nonzero column (16-row group minima)
           const int r0 = ar + (p_tile / tiles_n) * TM;
           int gm = 0x7fffffff;
@@ -941,6 +949,9 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
           int* gb = c.gmin16 + ((b0 + bi) >> 4);
           *ga = min(*ga, tb);
           *gb = min(*gb, ta);
+          // column bounds hold only up to the first interchange (the swapped-in row
+          // brings its own columns): floor every column's bound at this step
+          if (c.gcol16[-1] > b0 + j) c.gcol16[-1] = b0 + j;
         }
         if (b0 + j < c.n_real) {
           const double ap = fabs(urow[j]);
@@ -1906,6 +1917,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
   c.gpos = P.rowperm ? c.wf + P.RW : nullptr;
   c.tau = P.rowperm ? P.pivot_tau : 0.0;
   c.gmin16 = c.wf + P.RW + P.n_pad;
+  c.gcol16 = c.gmin16 + P.n_pad / 16 + 17;
   c.scratch = P.scratch + (size_t)slot * 2 * P.n_pad * TRI_BLOCK;
   c.smem = smem;
   c.smem_doubles = P.smem_doubles;
@@ -1939,7 +1951,9 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
         int mn = 0x7fffffff;
         for (int r = 16 * g; r < 16 * g + 16; ++r) mn = min(mn, P.gsorted[r]);
         c.gmin16[g] = mn;
+        c.gcol16[g] = mn;
       }
+      if (threadIdx.x == 0) c.gcol16[-1] = P.n_pad;
     }
     assemble(P, c.M, leaf, c.smem);
     if (threadIdx.x == 0) { s_pmin = INFINITY; s_pmax = 0.0; }
@@ -2098,6 +2112,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
         h.wf = h.rhs_g + P.m_pad;
         h.gpos = P.rowperm ? h.wf + P.RW : nullptr;
         h.gmin16 = h.wf + P.RW + P.n_pad;
+        h.gcol16 = h.gmin16 + P.n_pad / 16 + 17;
         h.scratch = P.scratch + (size_t)tgt * 2 * P.n_pad * TRI_BLOCK;
         h.sh = P.share + tgt;
         h.role = 2;
@@ -2145,6 +2160,7 @@ struct ProgramBuilder {
   std::vector<std::pair<int, int>> owner[2];
   std::vector<int> rowlim;  // equations with a nonzero left of column k (sorted rows), else empty
   bool tilek = false;       // per-tile k offsets in the LU trailing updates (row first-nonzero table)
+  bool colk = true;         // ... and the columns' first-nonzero rows of U (kmode 8)
   int small_panel = SMALL_PANEL;  // recursion leaf width (<= 32)
   int rlim(int k) const { return rowlim.empty() ? n_pad : rowlim[k]; }
   void small(int c0, int w) {
@@ -2231,7 +2247,7 @@ struct ProgramBuilder {
       Op o{}; o.kind = OP_GMIN16; o.a = c0 + h; o.b = r_end; ops.push_back(o);
     }
     gemm(OP_GEMM_SUB, c0 + h, c0, c0, c0 + h, c0 + h, c0 + h, r_end - c0 - h, w - h, h, 0,
-         tilek ? 4 : 0);
+         tilek ? (colk ? 12 : 4) : 0);
     lu(c0 + h, w - h, NR);
     swaps(c0 + h, w - h, c0, c0 + h);
   }
@@ -2403,7 +2419,7 @@ static size_t slot_doubles(const hps_plan_s* P, int mode) {
 }
 
 static int piv_stride(const hps_plan_s* P) {
-  return P->n_pad + P->n_pad / 16 + 16 + P->m_pad + P->RW + P->n_pad + P->n_pad / 16 + 16;
+  return P->n_pad + P->n_pad / 16 + 16 + P->m_pad + P->RW + P->n_pad + 2 * (P->n_pad / 16 + 16) + 1;
 }
 
 static int ensure_workspace(hps_plan_s* P, int mode, int want_slots) {
@@ -2488,6 +2504,7 @@ static int ensure_program(hps_plan_s* P, int mode) {
   // solve modes keep natural rhs / output order through the tables)
   P->rowperm[mode] = (!P->legendre && !(dbg && (atoi(dbg) & 4))) ? 1 : 0;
   if (P->rowperm[mode] && !(dbg && (atoi(dbg) & 256))) b.tilek = true;
+  if (dbg && (atoi(dbg) & 512)) b.colk = false;
   if (const char* sp = getenv("HPS_SMALL_PANEL")) b.small_panel = std::max(16, std::min(32, atoi(sp)));
   b.lu(0, P->n_pad, NR);
   if (P->colperm[mode]) {

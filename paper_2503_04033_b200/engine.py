@@ -276,7 +276,8 @@ def leaf_work_model(q: int, d: int = 3) -> dict:
     engine orderings, no interchanges — 10% of the pivots, which move rows
     together with their first-nonzero entry).  Mirrors the program builder:
     GEMM tiles of 64 rows (256 for N <= 64) start their k loop at the first
-    nonzero of their rows (16-row group minima) and of their RHS columns, in
+    nonzero of their rows (16-row group minima), of their trailing LU columns
+    (first row of U with a nonzero) and of their RHS columns, in
     16-wide chunks, and are skipped when that lies beyond the k range;
     triangular base blocks count h^2 per column; narrow panels rows * w^2."""
     n = q ** d
@@ -334,7 +335,12 @@ def leaf_work_model(q: int, d: int = 3) -> dict:
         h = split16(w)
         lu(c0, h)
         trsm_lower(c0, h, w - h, "lu_trsm")
-        work["lu_update"] += sub(c0 + h, n_pad - c0 - h, c0, h, w - h)
+        # trailing columns start at their first nonzero row of U (symmetric pattern:
+        # g of the column's node), valid up to the first interchange
+        cf = np.full(w - h, 0)
+        for tc in range(0, w - h, TN):
+            cf[tc] = gpos[c0 + h + tc:c0 + min(w, h + tc + TN)].min()
+        work["lu_update"] += sub(c0 + h, n_pad - c0 - h, c0, h, w - h, cf)
         lu(c0 + h, w - h)
 
     lu(0, n_pad)

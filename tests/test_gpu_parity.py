@@ -183,3 +183,22 @@ def test_legendre_cross_batch_vs_oracle():
         ref, sref, _ = O.leaf_dtn(otpl, c[:3].T, c[6:9].T, c[9], c[3:6].T)
         assert rel(dtn[k], ref) <= TOL
         assert rel(s[k], sref) <= TOL
+
+
+@pytest.mark.parametrize("kappa", [30.0, 160.0])
+def test_column_zero_skipping_is_exact(kappa, monkeypatch):
+    """The LU trailing updates start each column tile at the first row of U with a
+    nonzero (the columns' g; floored at the first row interchange).  The skipped
+    products are exact zeros, so the maps equal the unskipped run (HPS_DEBUG=512)
+    bit for bit — also at a large wavenumber, where partial pivoting interchanges
+    rows early."""
+    from paper_2503_04033_b200.engine import LeafEngine
+    tpl, pack = bump_pack(12, 8, kappa=kappa, seed=21)
+    fast, stats = LeafEngine(tpl, False, True, device=0).dtn_host(pack)
+    monkeypatch.setenv("HPS_DEBUG", "512")
+    full, _ = LeafEngine(tpl, False, True, device=0).dtn_host(pack)
+    assert np.array_equal(fast, full)
+    otpl = O.OracleTemplate(tpl.widths, 12)
+    for k in (0, 7):
+        ref, _, _ = O.leaf_dtn(otpl, pack[k, :3].T, None, pack[k, 3])
+        assert rel(fast[k], ref) <= TOL

@@ -2206,7 +2206,8 @@ struct ProgramBuilder {
     for (int g = r0 / 16; g < (r0 + h + 15) / 16; ++g) own[g] = {r0, h};
     inv(kind, r0, h);
   }
-  void trsm_lower(int r0, int h, int lo, int hi) {
+  // colb: the columns are LU columns (< n_pad), whose U rows start at gcol16 (kmode 8)
+  void trsm_lower(int r0, int h, int lo, int hi, bool colb = false) {
     if (hi <= lo) return;
     if (h <= TRI_BLOCK) {
       inv_cached(OP_INV_LOWER, r0, h);
@@ -2214,13 +2215,13 @@ struct ProgramBuilder {
       return;
     }
     const int h1 = split16_host(h);
-    trsm_lower(r0, h1, lo, hi);
+    trsm_lower(r0, h1, lo, hi, colb);
     // (no prefix clipping: these are pivot rows, whose first nonzero does not
     // follow their position once interchanged; the per-row g table does)
     if (tilek) { Op o{}; o.kind = OP_GMIN16; o.a = r0 + h1; o.b = r0 + h; ops.push_back(o); }
     gemm(OP_GEMM_SUB, r0 + h1, r0, r0, lo, r0 + h1, lo, h - h1, hi - lo, h1, dyn_rhs ? r0 + h1 : 0,
-         (dyn_rhs ? 1 : 0) | (tilek ? 4 : 0));
-    trsm_lower(r0 + h1, h - h1, lo, hi);
+         (dyn_rhs ? 1 : 0) | (tilek ? 4 : 0) | (tilek && colk && colb ? 8 : 0));
+    trsm_lower(r0 + h1, h - h1, lo, hi, colb);
   }
   void trsm_upper(int r0, int h, int lo, int hi) {
     if (hi <= lo) return;
@@ -2239,7 +2240,7 @@ struct ProgramBuilder {
     const int h = split16_host(w);
     lu(c0, h, NR);
     swaps(c0, h, c0 + h, c0 + w);
-    trsm_lower(c0, h, c0 + h, c0 + w);
+    trsm_lower(c0, h, c0 + h, c0 + w, true);
     // trailing update: only rows with a nonzero left of column c0 + h (sorted equations),
     // each row tile from the first nonzero column of its rows
     const int r_end = std::min(NR, rlim(c0 + h));

@@ -334,12 +334,12 @@ def leaf_work_model(q: int, d: int = 3) -> dict:
             return
         h = split16(w)
         lu(c0, h)
-        trsm_lower(c0, h, w - h, "lu_trsm")
         # trailing columns start at their first nonzero row of U (symmetric pattern:
         # g of the column's node), valid up to the first interchange
         cf = np.full(w - h, 0)
         for tc in range(0, w - h, TN):
             cf[tc] = gpos[c0 + h + tc:c0 + min(w, h + tc + TN)].min()
+        trsm_lower(c0, h, w - h, "lu_trsm", cf)
         work["lu_update"] += sub(c0 + h, n_pad - c0 - h, c0, h, w - h, cf)
         lu(c0 + h, w - h)
 

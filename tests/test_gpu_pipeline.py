@@ -24,6 +24,8 @@ CASES = [
     ("convdiff3_2x1x2_p5", "convdiff_step", 3, {}, (2, 1, 2), 5),
     ("curved2_2x2_p6_leg", "curved_helmholtz", 2, {"kappa": 4.0}, (2, 2), 6),
     ("curved3_2x1x1_p5_leg", "curved_helmholtz", 3, {"kappa": 4.0}, (2, 1, 1), 5),
+    # BASELINE configs[0]: 3D Poisson, p = 8, 2x2x2 leaves, manufactured (Green's function) solution
+    ("poisson3_2x2x2_p8", "poisson_green", 3, {}, (2, 2, 2), 8),
 ]
 
 

@@ -655,7 +655,11 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
 // kmode: per-tile k offsets where an operand has structural zero prefixes —
 // bit 1: B = the sorted RHS (bc = first RHS column), rows above the first
 // nonzero of the tile's columns are zero (rhs_g); bit 2: A = W-block rows
-// (ar >= n_pad), columns left of the tile's first nonzero are zero (wf).
+// (ar >= n_pad), columns left of the tile's first nonzero are zero (wf);
+// bit 4: A = LU rows, zero left of their first nonzero column (gmin16, 16-row
+// minima; tiles whose rows are zero over all of K are skipped); bit 8: B = U
+// rows of LU columns, zero above each column's first nonzero row (gcol16,
+// floored at the first interchange).
 // The k origin is br (A column ac + k pairs with B row br + k).
 // tri: 1 A lower-triangular, 3 A upper-triangular, 2 B upper-triangular (the
 // explicit inverses of the TRSM base blocks), 0 dense.

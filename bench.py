@@ -63,6 +63,31 @@ def bump_b(x):
     return 1.0 - 0.5 * np.exp(-r2 / (2 * 0.15 ** 2))
 
 
+def host_mem_available():
+    """MemAvailable of the node in bytes (Linux), or a large number if unknown."""
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 1 << 50
+
+
+def pinned_host(shape):
+    """Page-locked float64 host array of exactly this size (cudaHostRegister on a numpy
+    buffer; the torch pinned allocator rounds large requests up to a power of two)."""
+    import torch
+    a = np.empty(shape, dtype=np.float64)
+    torch.cuda.check_error(torch.cuda.cudart().cudaHostRegister(a.ctypes.data, a.nbytes, 0))
+    return a
+
+
+def unpin_host(a):
+    import torch
+    torch.cuda.check_error(torch.cuda.cudart().cudaHostUnregister(a.ctypes.data))
+
+
 def make_shard(p, boxes, kappa, rank, world, leaves_override=0, field="bump"):
     """Coefficient packs (L, 4, n) for this rank's slab of the unit-cube-stacked leaf grid.
     field "bump": -Lap u - kappa^2 b(x) u (configs 2-3); "const": b = 1 (configs[1])."""
@@ -296,9 +321,18 @@ def main():
         # H2D of the coefficients and D2H of every DtN map inside the timed region.
         del out
         torch.cuda.empty_cache()
-        h_coef = torch.from_numpy(pack).pin_memory().numpy()
-        h_out = torch.empty((L, m, m), dtype=torch.float64, pin_memory=True).numpy()
         chunk = eng.slots // 2   # D2H granularity of the single-launch streamed path
+        # host memory: every rank of the node pins its coefficients and DtN maps
+        # (p = 16: 45 GB per 16^3 leaves); cap the e2e batch to half of what the
+        # node has available so a multi-GPU run cannot exhaust host RAM
+        per_leaf = pack[0].nbytes + m * m * 8
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+        budget = 0.5 * host_mem_available() / max(local_world, 1)
+        Le = L if L * per_leaf <= budget else max(chunk, int(budget // per_leaf) // chunk * chunk)
+        Le = min(Le, L)
+        h_coef = pinned_host((Le,) + pack.shape[1:])
+        h_coef[:] = pack[:Le]
+        h_out = pinned_host((Le, m, m))
         # untimed warm-up over the full batch: sizes the device streaming buffers
         eng.dtn_host(h_coef, out=h_out, chunk_leaves=chunk)
         barrier()
@@ -312,9 +346,11 @@ def main():
             t = torch.tensor([e2e_t], device=f"cuda:{local}", dtype=torch.float64)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             e2e_t = float(t.item())
+        unpin_host(h_coef)
+        unpin_host(h_out)
         del h_coef, h_out
-        e2e = {"value": world * L / e2e_t, "unit": "leaf DtN maps/s",
-               "h2d_bytes_per_step": int(pack.nbytes), "d2h_bytes_per_step": int(L * m * m * 8),
+        e2e = {"value": world * Le / e2e_t, "unit": "leaf DtN maps/s", "leaves_per_gpu": Le,
+               "h2d_bytes_per_step": int(Le * pack[0].nbytes), "d2h_bytes_per_step": int(Le * m * m * 8),
                "path": "LeafEngine.dtn_host -> hps_leaf_dtn_host (C ABI): H2D of all coefficients, "
                        "one persistent launch, D2H of each finished "
                        f"{chunk}-leaf chunk overlapped via device completion counters"}

@@ -242,6 +242,12 @@ __device__ __forceinline__ void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+// bulk (non-tensor) copy shared -> global through the async proxy (TMA unit)
+__device__ __forceinline__ void bulk_store_s2g(void* gdst, const void* ssrc, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst),
+               "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
@@ -1525,10 +1531,31 @@ __device__ void assemble(const LeafParams& P, double* M, int leaf, double* smem)
   const int npat = pattern_size(P);
   // permuted rows (DtN drop orderings): zero the whole slot before any row is filled
   const bool two_pass = P.rowperm != 0;
-  if (two_pass) {
+  if (two_pass && P.smem_doubles < 1024 + 2 * dpp) {
     for (int r = warp; r < P.NR; r += NT / 32) {
       double2* row2 = reinterpret_cast<double2*>(M + (size_t)r * P.ld);
       for (int c2 = lane; c2 < P.NC / 2; c2 += 32) row2[c2] = make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+  } else if (two_pass) {
+    // bulk stores from a zeroed smem block at the end of the dynamic smem (past the
+    // derivative tables): the TMA unit writes the slot, the LSUs stay free for the
+    // co-resident CTA
+    constexpr int ZB = 1024;  // doubles per bulk store (8 KB)
+    double* zb = smem + (P.smem_doubles - ZB);
+    for (int e = threadIdx.x; e < ZB; e += NT) zb[e] = 0.0;
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (lane == 0) {
+      const size_t row_bytes = (size_t)P.NC * 8;
+      for (int r = warp; r < P.NR; r += NT / 32) {
+        char* row = reinterpret_cast<char*>(M + (size_t)r * P.ld);
+        for (size_t o = 0; o < row_bytes; o += ZB * 8)
+          bulk_store_s2g(row + o, zb, (unsigned)min((size_t)ZB * 8, row_bytes - o));
+      }
+      bulk_commit();
+      bulk_wait_all();
+      fence_proxy_async_global();
     }
     __syncthreads();
   }

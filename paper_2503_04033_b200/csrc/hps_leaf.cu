@@ -769,17 +769,56 @@ __shared__ double s_pv[2][NT / 32];
 __shared__ int s_pi[2][NT / 32];
 __shared__ double s_cand[2][NT / 32][8];
 __shared__ double s_rowj[2][8];
+// compacted pivot candidates: the 16-row groups after the block's own group that
+// have a structural nonzero in the panel
+constexpr int MAXG = 768;
+__shared__ int s_glist[MAXG];
+__shared__ int s_ng;
+
+// candidate index -> slot row: the head (rows b0 .. end of b0's 16-row group), then
+// the listed groups
+__device__ __forceinline__ int cand_row(int i, int b0, int head, bool compact) {
+  if (!compact || i < head) return b0 + i;
+  const int k = i - head;
+  return (s_glist[k >> 4] << 4) + (k & 15);
+}
 
 template <int WB>
 __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
-  const int n_cand = c.n_piv - b0;
+  const int n_full = c.n_piv - b0;
+  // rows whose 16-row group is zero over the whole panel (gmin16 >= c0 + w: a lower
+  // bound on the group's first nonzero column) are neither pivot candidates nor
+  // updated — their panel entries stay exact zeros — so they are left out
+  const int head = min(16 - (b0 & 15), n_full);
+  const bool compact = c.gpos != nullptr && ((c.n_piv + 15) >> 4) - (b0 >> 4) <= MAXG;
+  int n_cand = n_full;
+  if (compact) {
+    __syncthreads();  // s_glist of the previous block is no longer read
+    if (warp == 0) {
+      const int g_end = (c.n_piv + 15) >> 4;
+      int cnt = 0;
+      for (int g0 = (b0 >> 4) + 1; g0 < g_end; g0 += 32) {
+        const int g = g0 + lane;
+        const bool act = g < g_end && c.gmin16[g] < c0 + w;
+        const unsigned bal = __ballot_sync(0xffffffffu, act);
+        if (act) s_glist[cnt + __popc(bal & ((1u << lane) - 1u))] = g;
+        cnt += __popc(bal);
+      }
+      if (lane == 0) s_ng = cnt;
+    }
+    __syncthreads();
+    const int ng = s_ng;
+    n_cand = head + 16 * ng;
+    // a listed last group that crosses n_piv (clipped row range) is partial
+    if (ng > 0 && (c.n_piv & 15) && s_glist[ng - 1] == ((c.n_piv - 1) >> 4)) n_cand -= 16 - (c.n_piv & 15);
+  }
   const int done = b0 - c0, len = done + WB;
   double* S = c.smem;                          // column-major [WB][n_cand]: S[j * NS + r]
   const int NS = n_cand;
   // staging T (<= 32 x 32) and Q (<= 16 x 32) alias S; Ut sits after all of them
-  double* Ut = c.smem + (size_t)max(n_cand * WB, 1024);  // WB x 32, Ut[j*32 + kk]
+  double* Ut = c.smem + (size_t)max(n_full * WB, 1024);  // WB x 32, Ut[j*32 + kk]
   unsigned long long* prof = c.prof;
   long long tp = (prof && tid == 0) ? clock64() : 0;
 #define PANEL_TICK(slot)                                   \
@@ -829,19 +868,17 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
       bfr[kq] = ((kq >> 1) < nkp && lr < WB && k < done) ? Ut[lr * 32 + k] : 0.0;
     }
     const bool owns = 2 * lc < WB;  // lane holds output columns 2lc, 2lc+1
-    for (int g0 = b0 + warp * 8 * G; g0 < c.NR; g0 += NW * 8 * G) {
-      // all 32 rows zero in the panel (first structural nonzero beyond it): no loads
-      bool zero_rows = false;
-      if (c.gpos && g0 + 8 * G <= c.n_piv) {
-        int gm = c.gmin16[g0 >> 4];
-        for (int q = 16 - (g0 & 15); q < 8 * G; q += 16) gm = min(gm, c.gmin16[(g0 + q) >> 4]);
-        zero_rows = gm >= c0 + w;
-      }
+    // candidate rows by compacted index, then the non-candidate rows [n_piv, NR)
+    const int n_ext = n_cand + (c.NR - c.n_piv);
+    for (int i0 = warp * 8 * G; i0 < n_ext; i0 += NW * 8 * G) {
       double af[G][8], av[G][2];
+      int rg[G];
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        const int r = g0 + g * 8 + lr;
-        const bool ok = r < c.NR && !zero_rows;
+        const int i = i0 + g * 8 + lr;
+        const int r = i < n_cand ? cand_row(i, b0, head, compact) : c.n_piv + (i - n_cand);
+        rg[g] = i < n_cand ? i : -1 - r;  // candidate index, or -1 - row
+        const bool ok = i < n_ext;
         const double* row = c.M + (size_t)(r < c.NR ? r : c.NR - 1) * c.ld;
 #pragma unroll
         for (int pq = 0; pq < 4; ++pq) {
@@ -866,13 +903,14 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
 #pragma unroll
         for (int kq = 0; kq < 8; ++kq)
           if ((kq >> 1) < nkp) dmma(acc, af[g][kq], bfr[kq]);
-        const int r = g0 + g * 8 + lr;
-        if (r < c.NR && owns) {
+        const int i = i0 + g * 8 + lr;
+        if (i < n_ext && owns) {
           const double v0 = av[g][0] - acc[0], v1 = av[g][1] - acc[1];
-          if (r < c.n_piv) {
-            S[(2 * lc) * NS + (r - b0)] = v0;
-            if (2 * lc + 1 < WB) S[(2 * lc + 1) * NS + (r - b0)] = v1;
+          if (rg[g] >= 0) {
+            S[(2 * lc) * NS + rg[g]] = v0;
+            if (2 * lc + 1 < WB) S[(2 * lc + 1) * NS + rg[g]] = v1;
           } else {
+            const int r = -1 - rg[g];
             c.M[(size_t)r * c.ld + b0 + 2 * lc] = v0;
             if (2 * lc + 1 < WB) c.M[(size_t)r * c.ld + b0 + 2 * lc + 1] = v1;
           }
@@ -882,8 +920,9 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
   } else {
     for (int e = tid; e < n_cand * WB; e += NT) {
       const int r = e / WB, j = e - r * WB;
-      const bool nz = c.gpos == nullptr || c.gmin16[(b0 + r) >> 4] < c0 + w;
-      S[j * NS + r] = nz ? c.M[(size_t)(b0 + r) * c.ld + b0 + j] : 0.0;
+      const int row = cand_row(r, b0, head, compact);
+      const bool nz = c.gpos == nullptr || c.gmin16[row >> 4] < c0 + w;
+      S[j * NS + r] = nz ? c.M[(size_t)row * c.ld + b0 + j] : 0.0;
     }
   }
   __syncthreads();
@@ -948,15 +987,16 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
 #pragma unroll
       for (int t = 0; t < WB; ++t) urow[t] = (bi == j) ? rowj[t] : s_cand[par][bw][t];
       if (tid == 0) {
-        c.piv[b0 + j] = b0 + bi;
+        const int prow = cand_row(bi, b0, head, compact);
+        c.piv[b0 + j] = prow;
         if (c.prof && bi != j) c.prof[15] += 1;
         if (c.gpos && bi != j) {  // the equations' first-nonzero table follows the interchange
-          const int ta = c.gpos[b0 + j], tb = c.gpos[b0 + bi];
+          const int ta = c.gpos[b0 + j], tb = c.gpos[prow];
           c.gpos[b0 + j] = tb;
-          c.gpos[b0 + bi] = ta;
+          c.gpos[prow] = ta;
           // 16-row minima stay lower bounds (a group may only gain a smaller g)
           int* ga = c.gmin16 + ((b0 + j) >> 4);
-          int* gb = c.gmin16 + ((b0 + bi) >> 4);
+          int* gb = c.gmin16 + (prow >> 4);
           *ga = min(*ga, tb);
           *gb = min(*gb, ta);
           // column bounds hold only up to the first interchange (the swapped-in row
@@ -1025,7 +1065,7 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
   // 4. write-back; non-candidate rows L = A U^{-1}
   for (int e = tid; e < n_cand * WB; e += NT) {
     const int r = e / WB, j = e - r * WB;
-    c.M[(size_t)(b0 + r) * c.ld + b0 + j] = S[j * NS + r];
+    c.M[(size_t)cand_row(r, b0, head, compact) * c.ld + b0 + j] = S[j * NS + r];
   }
   {
     // 8 rows per thread in flight: loads first, then the WB x WB substitution

@@ -2264,7 +2264,8 @@ struct ProgramBuilder {
     trsm_right(c0, h1, cst, M);
     const int k0 = c0 > cst ? c0 : cst;
     if (c0 + h1 > k0)
-      gemm(OP_GEMM_SUB, n_pad, k0, k0, c0 + h1, n_pad, c0 + h1, M, h - h1, c0 + h1 - k0, 0, 2);
+      gemm(OP_GEMM_SUB, n_pad, k0, k0, c0 + h1, n_pad, c0 + h1, M, h - h1, c0 + h1 - k0, 0,
+           2 | (tilek && colk ? 8 : 0));
     trsm_right(c0 + h1, h - h1, cst, M);
   }
   bool dyn_rhs = false;  // forward solve against the slab-ordered A_ib: clip N by rhs_tab

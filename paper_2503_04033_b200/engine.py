@@ -347,7 +347,12 @@ def leaf_work_model(q: int, d: int = 3) -> dict:
     trsm_lower(0, n_pad, m, "forward", fs, lambda R: int(np.searchsorted(fs, R, side="left")))
     j = np.arange(m)
     f = fs.astype(float)
-    work["W"] = float(((n - f) ** 2).sum())
+    # W = A_bi U^-1: row b from its first nonzero f_b; column c of U from its first
+    # nonzero row (16-column minima of g, as the kernel's column bounds)
+    gc = np.repeat(g16, 16)[:n]
+    cols = np.arange(n)
+    work["W"] = float(sum(2.0 * np.maximum(cols[fb:] - np.maximum(fb, gc[fb:]), 0).sum()
+                          for fb in fs))
     work["T"] = 2.0 * float(((2 * j + 1) * (n - f)).sum())
     return work
 
@@ -358,7 +363,8 @@ def dtn_flops_executed(n: int, m: int, q: int, d: int = 3, skip_prefix: bool = T
     and the forward solve Y = L^-1 P A_ib with their structurally zero tiles
     skipped (leaf_work_model: rows from their first nonzero, RHS columns from
     their line's first row), and then either
-      wtrick:  W = A_bi U^-1 from each row's first nonzero (sum (n - f_b)^2) and
+      wtrick:  W = A_bi U^-1 from each row's first nonzero and each column's first
+               row of U (sum over j >= f_b of 2 (j - max(f_b, g_j))) and
                T -= W Y over k >= max(f_b, f_c) (sum 2 (n - max(f_b, f_c)));
       else:    the backward solve (n^2 m) and the line-sparse A_bi X (2 q m^2).
     f from the engine's interior order (forward_prefix_rows).  skip_prefix=False:

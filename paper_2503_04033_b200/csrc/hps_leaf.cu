@@ -508,16 +508,36 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   // 8x8 sub-tiles of this warp that lie inside the GEMM extent (warp-uniform):
   // edge tiles skip the DMMAs on zero-filled rows / columns.
   int mv = MI, nv = NJ;
-  int wg = 0;  // kmode 4: first A column with a nonzero in this warp's rows of the tile
+  // first k this warp's part of the tile needs: the kmode bounds of the tile,
+  // taken over the warp's own rows (A) and columns (B)
+  int wk = 0;
   auto set_valid = [&](int t) {
     const int tm = t / tiles_n, tn = t - tm * tiles_n;
     const int rows = M - (tm * TM + wm * (MI * 8)), cols = N - (tn * TN + wn * (NJ * 8));
     mv = rows <= 0 ? 0 : (rows >= MI * 8 ? MI : (rows + 7) / 8);
     nv = cols <= 0 ? 0 : (cols >= NJ * 8 ? NJ : (cols + 7) / 8);
-    if (kmode & 4) {
-      const int r0 = ar + tm * TM + wm * (MI * 8);
-      wg = 0x7fffffff;
-      for (int r = r0; r < r0 + MI * 8 && r < ar + M; r += 16) wg = min(wg, c.gmin16[r >> 4]);
+    wk = 0;
+    if (kmode && mv > 0 && nv > 0) {
+      const int r0 = ar + tm * TM + wm * (MI * 8), r1 = min(r0 + MI * 8, ar + M);
+      const int c0w = tn * TN + wn * (NJ * 8), c1w = min(c0w + NJ * 8, N);
+      if (kmode & 1) wk = max(wk, c.rhs_g[c0w] - br);  // suffix minima: first column is the min
+      if (kmode & 2) {  // W rows: per-row first nonzero, warp-reduced
+        int f = 0x7fffffff;
+        for (int r = r0 + lane; r < r1; r += 32) f = min(f, c.wf[r - c.n_piv]);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) f = min(f, __shfl_xor_sync(0xffffffffu, f, off));
+        wk = max(wk, f - ac);
+      }
+      if (kmode & 4) {
+        int gm = 0x7fffffff;
+        for (int r = r0; r < r1; r += 16) gm = min(gm, c.gmin16[r >> 4]);
+        wk = max(wk, gm - ac);
+      }
+      if (kmode & 8) {
+        int gm = c.gcol16[-1];
+        for (int cq = bc + c0w; cq < bc + c1w; cq += 16) gm = min(gm, c.gcol16[cq >> 4]);
+        wk = max(wk, gm - br);
+      }
     }
   };
   for (;; ++it) {
@@ -565,7 +585,7 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     // triangular operands (explicit inverses): chunks whose part of this warp's
     // rows / columns lies entirely in the zero triangle are skipped
     // rows of this warp that are zero over the whole chunk (first nonzero beyond it)
-    bool zero_chunk = (kmode & 4) && (ac + kc * KC + KC <= wg);
+    bool zero_chunk = kc * KC + KC <= wk;
     if (tri) {
       const int k_lo = kc * KC, k_hi = k_lo + KC - 1;
       const int tm = tile / tiles_n, tn = tile - tm * tiles_n;

@@ -275,10 +275,10 @@ def leaf_work_model(q: int, d: int = 3) -> dict:
     """Work of the engine's DtN op program for one leaf, by phase (drop mode,
     engine orderings, no interchanges — 10% of the pivots, which move rows
     together with their first-nonzero entry).  Mirrors the program builder:
-    GEMM tiles of 64 rows (256 for N <= 64) start their k loop at the first
-    nonzero of their rows (16-row group minima), of their trailing LU columns
-    (first row of U with a nonzero) and of their RHS columns, in
-    16-wide chunks, and are skipped when that lies beyond the k range;
+    every 32 x 32 warp block of a GEMM tile starts its k loop at the first
+    nonzero of its rows (16-row group minima), of its trailing LU columns
+    (first row of U with a nonzero) and of its RHS columns, in k chunks of 16
+    (8 on the 256 x 32 tiles), and is skipped when that lies beyond the k range;
     triangular base blocks count h^2 per column; narrow panels rows * w^2."""
     n = q ** d
     n_pad = (n + 15) // 16 * 16
@@ -298,20 +298,23 @@ def leaf_work_model(q: int, d: int = 3) -> dict:
         return ((w // 2 + 15) // 16) * 16
 
     def sub(r0, M, k0, K, ncols, col_first=None):
-        """sum over row tiles (and column tiles) of 2 rows cols k_eff"""
+        """sum over the 32 x 32 warp blocks of every tile of 2 rows cols k_eff: each
+        warp starts at the first k chunk its own rows (16-row minima of g) and
+        columns (col_first, per column) need, chunk KC = 16 (64 x 128 tiles) or
+        8 (256 x 32 tiles for N <= 64), as the kernel's per-warp bounds"""
         if M <= 0 or K <= 0 or ncols <= 0:
             return 0.0
-        TM = 256 if (ncols <= 64 and M >= 256) else 64
+        kc = 8 if (ncols <= 64 and M >= 256) else 16
         tot = 0.0
-        for tr in range(r0, r0 + M, TM):
-            rows = min(TM, r0 + M - tr)
+        for tr in range(r0, r0 + M, 32):
+            rows = min(32, r0 + M - tr)
             kr = g16[tr // 16:(tr + rows + 15) // 16].min() - k0
-            for tc in range(0, ncols, TN):
-                cols = min(TN, ncols - tc)
-                kk = kr if col_first is None else max(kr, col_first[tc] - k0)
+            for tc in range(0, ncols, 32):
+                cols = min(32, ncols - tc)
+                kk = kr if col_first is None else max(kr, col_first[tc:tc + cols].min() - k0)
                 if kk >= K:
                     continue
-                kk = max(kk, 0) // 16 * 16
+                kk = max(kk, 0) // kc * kc
                 tot += 2.0 * rows * cols * (K - kk)
         return tot
 
@@ -336,9 +339,7 @@ def leaf_work_model(q: int, d: int = 3) -> dict:
         lu(c0, h)
         # trailing columns start at their first nonzero row of U (symmetric pattern:
         # g of the column's node), valid up to the first interchange
-        cf = np.full(w - h, 0)
-        for tc in range(0, w - h, TN):
-            cf[tc] = gpos[c0 + h + tc:c0 + min(w, h + tc + TN)].min()
+        cf = gpos[c0 + h:c0 + w]
         trsm_lower(c0, h, w - h, "lu_trsm", cf)
         work["lu_update"] += sub(c0 + h, n_pad - c0 - h, c0, h, w - h, cf)
         lu(c0 + h, w - h)

@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--leaves", type=int, default=0, help="override leaves per rank (profiling)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-seconds", type=float, default=60.0,
+                    help="reference arm: total CPU seconds over warmup + timed steps")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -174,11 +176,23 @@ def traffic_per_launch(leaves):
     return per_leaf * leaves
 
 
+def blas_threads():
+    """Threads the host BLAS (OpenBLAS under numpy/scipy) actually uses."""
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i["num_threads"] for i in threadpool_info() if i.get("user_api") == "blas"]
+        if n:
+            return int(max(n))
+    except Exception:
+        pass
+    return os.cpu_count() or 1
+
+
 def cpu_reference(tpl, pack, seconds, steps=1):
     """The reference's CPU algorithm (oracle port of local_ops.build_leaf_factors) on host cores."""
     from oracle import hps_oracle as O
     otpl = O.OracleTemplate(tpl.widths, tpl.p)
-    cores = os.cpu_count() or 1
+    cores = blas_threads()
     times, done = [], 0
     t_start = time.perf_counter()
     for _ in range(steps):
@@ -223,7 +237,7 @@ def main():
         tpl, pack = make_shard(p, boxes, args.kappa, 0, 1, leaves_override=min(64, boxes ** 3),
                                field=args.field)
         steps = max(1, args.steps)
-        per_step = max(2.0, 60.0 / (steps + args.warmup))
+        per_step = max(min(2.0, args.ref_seconds), args.ref_seconds / (steps + args.warmup))
         for _ in range(args.warmup):
             cpu_reference(tpl, pack, seconds=min(per_step, 2.0))
         base = cpu_reference(tpl, pack, seconds=per_step, steps=steps)

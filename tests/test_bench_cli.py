@@ -1,0 +1,41 @@
+"""bench.py's reference arm under torchrun (CPU only): rank 0 alone runs the CPU
+reference and prints one JSON line; the other ranks exit 0 without work."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(cmd, env_extra=None):
+    env = dict(os.environ, OMP_NUM_THREADS="2", OPENBLAS_NUM_THREADS="2", MASTER_ADDR="127.0.0.1")
+    env.update(env_extra or {})
+    return subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
+
+
+def _lines(stdout):
+    return [json.loads(s) for s in stdout.splitlines() if s.startswith("{")]
+
+
+def test_reference_arm_single_process():
+    res = _run([sys.executable, "bench.py", "--impl", "reference", "--p", "8", "--boxes", "2",
+                "--steps", "1", "--warmup", "1", "--ref-seconds", "2"])
+    assert res.returncode == 0, res.stderr[-2000:]
+    (line,) = _lines(res.stdout)
+    assert line["impl"] == "reference" and line["n_gpus"] == 1
+    assert line["metric"] == "leaf DtN maps/sec" and line["value"] > 0
+    assert line["e2e"]["value"] == line["value"]
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] == 2  # OPENBLAS_NUM_THREADS
+    assert line["config"]["p"] == 8 and line["config"]["leaves_per_gpu"] == 8
+
+
+def test_reference_arm_under_torchrun_prints_one_line():
+    res = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                "--master-addr", "127.0.0.1", "--master-port", "29561", "bench.py", "--impl",
+                "reference", "--gpus", "2", "--p", "8", "--boxes", "2", "--steps", "1",
+                "--warmup", "1", "--ref-seconds", "2"])
+    assert res.returncode == 0, res.stderr[-2000:]
+    (line,) = _lines(res.stdout)
+    assert line["impl"] == "reference" and line["n_gpus"] == 2

@@ -2232,12 +2232,18 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
 // Left part of a recursive split: multiples of TN (128) above 256 columns so the
 // big GEMMs see tile-aligned N/M extents (p=16: tile utilisation 0.85 -> 0.91),
 // multiples of 16 (the TMA/K-chunk granule) below.
+// Tuning knobs (diagnostics): HPS_SPLIT_ALIGN (default TN), HPS_SPLIT_PCT (left
+// part in percent of w, default 50).
+static int g_split_align = TN, g_split_pct = 50;
 int split16_host(int w) {
-  if (w > 2 * TN) {
-    const int h = (w / 2) / TN * TN;
-    return h < TN ? TN : h;
+  const int A = g_split_align;
+  const int half = (int)((long long)w * g_split_pct / 100);
+  if (w > 2 * A) {
+    const int h = half / A * A;
+    return h < A ? A : (h >= w ? w - A : h);
   }
-  return ((w / 2 + 15) / 16) * 16;
+  const int h = ((half + 15) / 16) * 16;
+  return h < 16 ? 16 : (h >= w ? w - 16 : h);
 }
 
 struct ProgramBuilder {
@@ -2599,6 +2605,8 @@ static int ensure_program(hps_plan_s* P, int mode) {
   if (P->rowperm[mode] && !(dbg && (atoi(dbg) & 256))) b.tilek = true;
   if (dbg && (atoi(dbg) & 512)) b.colk = false;
   if (const char* sp = getenv("HPS_SMALL_PANEL")) b.small_panel = std::max(16, std::min(32, atoi(sp)));
+  if (const char* sa = getenv("HPS_SPLIT_ALIGN")) g_split_align = std::max(16, atoi(sa) / 16 * 16);
+  if (const char* sp = getenv("HPS_SPLIT_PCT")) g_split_pct = std::max(20, std::min(80, atoi(sp)));
   b.lu(0, P->n_pad, NR);
   if (P->colperm[mode]) {
     Op o{};

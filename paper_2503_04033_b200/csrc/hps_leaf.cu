@@ -110,6 +110,10 @@ constexpr int SHARE_MIN_TILES = 16;
 #ifndef HPS_PIVOT_TAU
 #define HPS_PIVOT_TAU 0.0
 #endif
+#ifndef HPS_PF
+#define HPS_PF 0  // GEMM operand L2 prefetch distance in k chunks (0: off)
+#endif
+constexpr int PF_DIST = HPS_PF;
 #ifndef HPS_RW
 #define HPS_RW 256  // W-trick block of sorted boundary DOFs (rows below A_ii)
 #endif
@@ -482,6 +486,10 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     mbar_expect_tx(&c.full[s], S::BYTES);
     tma_load_3d(sa, mapA, ac + p_kc * KC, ar + tm * TM, a_slot, &c.full[s]);
     tma_load_3d(sb, mapB, bc + tn * TN, br + p_kc * KC, b_slot, &c.full[s]);
+    if (PF_DIST > 0 && p_kc + PF_DIST < kchunks) {  // operand chunks further ahead into L2
+      tma_prefetch_3d(mapA, ac + (p_kc + PF_DIST) * KC, ar + tm * TM, a_slot);
+      tma_prefetch_3d(mapB, bc + tn * TN, br + (p_kc + PF_DIST) * KC, b_slot);
+    }
     if (sub && first_chunk) {  // C tile into L2 ahead of the reduce-add epilogue
       if (narrow) {
         for (int r = 0; r < TM; r += 8) tma_prefetch_3d(&c.maps->b_work_n, cc + tn * TN, cr + tm * TM + r, c.slot);

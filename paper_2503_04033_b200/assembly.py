@@ -1,0 +1,154 @@
+"""Interface assembly on the device: the leaves' DtN maps scattered into T.
+
+Reference: condensation.py:230-246 (each leaf's T^tau added into the sparse
+interface matrix T over its interface DOFs, its Dirichlet columns into the
+coupling matrix).  The host mirror (``SparseMatrix`` triplets -> COO -> CSR,
+sparse_backend.py) copies every DtN map to the host first; here the maps stay
+in HBM and one kernel (``hps_interface_scatter``) adds them into the CSR value
+arrays of T and of the coupling C, so only the assembled values cross PCIe.
+
+T is block sparse at face granularity: geometry lays out every face as a
+contiguous id range, and a leaf's boundary concatenates its faces
+(geometry.py), so the CSR pattern is built from face tables alone — row r of
+interface face F holds, in id order, the DOFs of every interface face that
+shares a leaf with F — and a scatter job is one (row face, column face) block
+of one leaf.  The result is bit-identical to the host path: each entry of T
+has at most two contributors and IEEE addition is commutative.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Dict, List, Tuple
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _native
+from .errors import ConfigError
+from .geometry import Discretization
+
+INTERFACE = "interface"
+
+
+def _ranges(starts: np.ndarray, sizes: np.ndarray) -> np.ndarray:
+    """Concatenation of arange(s, s + n) over (s, n) pairs."""
+    if len(sizes) == 0:
+        return np.empty(0, dtype=np.int64)
+    tot = int(sizes.sum())
+    first = np.repeat(starts - np.concatenate([[0], np.cumsum(sizes)[:-1]]), sizes)
+    return first + np.arange(tot, dtype=np.int64)
+
+
+class InterfacePattern:
+    """CSR patterns of T (n_int x n_int) and C (n_int x n_dir) and the per-leaf
+    scatter jobs {row0, col0, rows, cols, target, base, stride} (host integers)."""
+
+    def __init__(self, disc: Discretization):
+        lo, hi = disc.interface_offset, disc.dirichlet_offset
+        self.n_int, self.n_dir = int(disc.n_interface), int(disc.n_dirichlet)
+        start: Dict = {}
+        size: Dict = {}
+        for key, f in disc.faces.items():
+            ids = f.node_ids
+            if len(ids) and not np.array_equal(ids, np.arange(ids[0], ids[0] + len(ids))):
+                raise ConfigError(f"face {key} is not a contiguous id range")
+            start[key] = int(ids[0]) - (lo if f.kind == INTERFACE else hi) if len(ids) else 0
+            size[key] = len(ids)
+        iface = sorted((k for k, f in disc.faces.items() if f.kind == INTERFACE), key=start.get)
+        cols: Dict = {}
+        row_len = np.zeros((2, len(iface)), dtype=np.int64)
+        for i, key in enumerate(iface):
+            nb = set()
+            for leaf_id in disc.faces[key].leaf_ids:
+                if leaf_id is not None:
+                    nb.update(disc.leaves[leaf_id].face_keys)
+            for t, kind in enumerate((True, False)):
+                sel = sorted((g for g in nb if (disc.faces[g].kind == INTERFACE) == kind), key=start.get)
+                offs = np.concatenate([[0], np.cumsum([size[g] for g in sel])]).astype(np.int64)
+                cols[(t, key)] = dict(zip(sel, offs[:-1].tolist()))
+                row_len[t, i] = offs[-1]
+        sizes = np.asarray([size[k] for k in iface], dtype=np.int64)
+        self.indptr, self.indices, base = [], [], []
+        for t in range(2):
+            per_row = np.repeat(row_len[t], sizes)
+            indptr = np.zeros(self.n_int + 1, dtype=np.int64)
+            np.cumsum(per_row, out=indptr[1:])
+            nnz = int(indptr[-1])
+            idx_t = np.int32 if max(nnz, self.n_int, self.n_dir) < 2 ** 31 - 1 else np.int64
+            parts = []
+            for i, key in enumerate(iface):
+                sel = list(cols[(t, key)])
+                row = _ranges(np.asarray([start[g] for g in sel], dtype=np.int64),
+                              np.asarray([size[g] for g in sel], dtype=np.int64))
+                parts.append(np.tile(row.astype(idx_t), size[key]))
+            self.indices.append(np.concatenate(parts) if parts else np.empty(0, dtype=idx_t))
+            self.indptr.append(indptr.astype(idx_t))
+            base.append({key: int(indptr[start[key]]) for key in iface})
+        self.nnz = (int(self.indptr[0][-1]), int(self.indptr[1][-1]))
+        pos = {k: i for i, k in enumerate(iface)}
+        self.leaf_jobs: List[np.ndarray] = []
+        for leaf in disc.leaves:
+            jobs = []
+            offs = np.concatenate([[0], np.cumsum([size[k] for k in leaf.face_keys])])
+            for fi, fk in enumerate(leaf.face_keys):
+                if disc.faces[fk].kind != INTERFACE:
+                    continue
+                for gi, gk in enumerate(leaf.face_keys):
+                    t = 0 if disc.faces[gk].kind == INTERFACE else 1
+                    stride = int(row_len[t, pos[fk]])
+                    jobs.append((offs[fi], offs[gi], size[fk], size[gk], t,
+                                 base[t][fk] + cols[(t, fk)][gk], stride))
+            self.leaf_jobs.append(np.asarray(jobs, dtype=np.int64).reshape(-1, 7))
+
+    def jobs_for(self, ids) -> np.ndarray:
+        """int64 [jobs][8] for a flush of leaves ids (column 0 = position in the flush)."""
+        parts = []
+        for k, leaf_id in enumerate(ids):
+            j = self.leaf_jobs[leaf_id]
+            parts.append(np.concatenate([np.full((len(j), 1), k, dtype=np.int64), j], axis=1))
+        return np.ascontiguousarray(np.concatenate(parts) if parts else np.empty((0, 8), np.int64))
+
+    def matrices(self, t_vals: np.ndarray, c_vals: np.ndarray) -> Tuple[sp.csr_matrix, sp.csr_matrix]:
+        t = sp.csr_matrix((t_vals, self.indices[0], self.indptr[0]), shape=(self.n_int, self.n_int))
+        c = sp.csr_matrix((c_vals, self.indices[1], self.indptr[1]), shape=(self.n_int, self.n_dir))
+        t.has_sorted_indices = True
+        c.has_sorted_indices = True
+        return t, c
+
+
+class DeviceAssembler:
+    """Accumulates flushes of device DtN maps into device CSR values of T and C."""
+
+    def __init__(self, pattern: InterfacePattern, device: int):
+        import torch
+        self.torch, self.pattern, self.device = torch, pattern, int(device)
+        dev = f"cuda:{self.device}"
+        self.t_vals = torch.zeros(max(pattern.nnz[0], 1), dtype=torch.float64, device=dev)
+        self.c_vals = torch.zeros(max(pattern.nnz[1], 1), dtype=torch.float64, device=dev)
+        self.lib = _native.load()
+
+    def add(self, dtn, ids, stream=None) -> None:
+        """Scatter-add the DtN maps of a flush (device tensor [len(ids)][m][m])."""
+        torch = self.torch
+        if dtn.dim() != 3 or dtn.shape[0] != len(ids) or dtn.shape[1] != dtn.shape[2]:
+            raise ConfigError(f"DtN batch of shape {tuple(dtn.shape)} for {len(ids)} leaves")
+        dtn = dtn.contiguous()
+        jobs_h = self.pattern.jobs_for(ids)
+        if len(jobs_h) == 0:
+            return
+        jobs = torch.from_numpy(jobs_h).to(f"cuda:{self.device}", non_blocking=False)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        m = int(dtn.shape[1])
+        _native.check(self.lib.hps_interface_scatter(
+            self.device, ctypes.c_void_p(dtn.data_ptr()), m, m * m, len(jobs_h),
+            ctypes.c_void_p(jobs.data_ptr()), ctypes.c_void_p(self.t_vals.data_ptr()),
+            ctypes.c_void_p(self.c_vals.data_ptr()), ctypes.c_void_p(s.cuda_stream)))
+        self._keep = (dtn, jobs)  # alive until the next add / finish
+
+    def finish(self) -> Tuple[sp.csr_matrix, sp.csr_matrix]:
+        nt, nc = self.pattern.nnz
+        t_vals = self.t_vals[:nt].cpu().numpy()
+        c_vals = self.c_vals[:nc].cpu().numpy()
+        self._keep = None
+        return self.pattern.matrices(t_vals, c_vals)

@@ -2741,6 +2741,31 @@ static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, c
   return 0;
 }
 
+
+// ---------------------------------------------------------------------------
+// Interface assembly on the device: scatter-add of the leaves' DtN blocks into
+// the CSR values of T (and of the Dirichlet coupling C), reference
+// condensation.py:230-246.  T is block sparse at face granularity — every face
+// is a contiguous id range and a leaf's boundary concatenates its faces — so a
+// job is one (row face, column face) block of one leaf: nr x nc doubles read
+// row by row from the DtN map and added to out[base + a * stride + b].  Each
+// entry of T has at most two contributors (the two leaves of a face), and
+// 0 + x + y == 0 + y + x in IEEE arithmetic, so the atomics give the host
+// COO -> CSR sum bit for bit.  HBM-bound: 8 bytes read + one 8-byte atomic
+// per element; warps walk rows, lanes walk columns (coalesced both sides).
+__global__ void __launch_bounds__(256) hps_interface_scatter_kernel(
+    const double* __restrict__ blocks, long long ld, long long block_stride,
+    const long long* __restrict__ jobs, double* __restrict__ out0, double* __restrict__ out1) {
+  const long long* j = jobs + 8 * (long long)blockIdx.x;
+  const long long leaf = j[0], r0 = j[1], c0 = j[2], nr = j[3], nc = j[4];
+  double* out = (j[5] ? out1 : out0) + j[6];
+  const long long stride = j[7];
+  const double* src = blocks + leaf * block_stride + r0 * ld + c0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (long long a = warp; a < nr; a += blockDim.x >> 5)
+    for (long long b = lane; b < nc; b += 32) atomicAdd(out + a * stride + b, __ldg(src + a * ld + b));
+}
+
 extern "C" {
 
 const char* hps_last_error(void) { return g_last_error.c_str(); }
@@ -3180,6 +3205,19 @@ int hps_leaf_dtn_host(hps_plan_t P, int n_leaves, const double* coeffs_host, dou
   if (rc != 0) return rc;
   const cudaError_t e = e1 != cudaSuccess ? e1 : e2;
   if (e != cudaSuccess) return fail(std::string("streamed dtn failed: ") + cudaGetErrorString(e));
+  return 0;
+}
+
+int hps_interface_scatter(int device, const double* blocks, long long ld, long long block_stride,
+                          int n_jobs, const long long* jobs, double* out_t, double* out_c,
+                          void* stream) {
+  if (n_jobs < 0 || ld <= 0 || block_stride < 0) return fail("hps_interface_scatter: bad sizes");
+  if (n_jobs == 0) return 0;
+  if (!blocks || !jobs || !out_t) return fail("hps_interface_scatter: null pointer");
+  CK(cudaSetDevice(device));
+  hps_interface_scatter_kernel<<<n_jobs, 256, 0, (cudaStream_t)stream>>>(blocks, ld, block_stride, jobs,
+                                                                        out_t, out_c ? out_c : out_t);
+  CK(cudaGetLastError());
   return 0;
 }
 

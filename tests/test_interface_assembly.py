@@ -1,0 +1,126 @@
+"""Device interface assembly (assembly.py) against the reference's host scatter
+(condensation.py:230-246 -> scatter_leaf_blocks / finalize_host).
+
+CPU tests replay the kernel's scatter jobs with numpy on random DtN maps; the
+GPU tests run hps_interface_scatter and whole builds through both paths.  The
+bar is bit-exact: same CSR structure, same values."""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from paper_2503_04033_b200.assembly import InterfacePattern
+from paper_2503_04033_b200.condensation import (_make_dof_map, finalize_host,
+                                                scatter_leaf_blocks)
+from paper_2503_04033_b200.geometry import DomainBox, MeshConfig, build_discretization
+from paper_2503_04033_b200.local_ops import LeafTemplate
+from paper_2503_04033_b200.sparse_backend import SparseMatrix
+
+CASES = [((1, 1), 6, "drop"), ((3, 2), 6, "drop"), ((2, 2), 5, "legendre"),
+         ((1, 1, 1), 5, "drop"), ((2, 1, 1), 5, "drop"), ((3, 2, 2), 6, "drop"),
+         ((2, 2, 2), 5, "legendre")]
+
+
+def _disc(boxes, p, mode):
+    d = len(boxes)
+    return build_discretization(DomainBox((0.0,) * d, (1.0,) * d), MeshConfig(boxes, p, mode))
+
+
+def _host(disc, dtn):
+    tpl = LeafTemplate(disc.leaf_widths, disc.p, disc.corner_mode, False)
+    dof_map = _make_dof_map(disc, tpl)
+    tb, cr, cc, cv = SparseMatrix(disc.n_interface), [], [], []
+    scatter_leaf_blocks(dof_map, range(len(disc.leaves)), dtn, tb, cr, cc, cv)
+    return finalize_host(tb, cr, cc, cv, disc.n_interface, disc.n_dirichlet)
+
+
+def _replay(pat, dtn, ids):
+    """numpy replay of hps_interface_scatter_kernel over jobs_for(ids)."""
+    out = [np.zeros(pat.nnz[0]), np.zeros(pat.nnz[1])]
+    for k, r0, c0, nr, nc, tgt, base, stride in pat.jobs_for(ids):
+        blk = dtn[k, r0:r0 + nr, c0:c0 + nc]
+        idx = base + np.arange(nr)[:, None] * stride + np.arange(nc)[None, :]
+        np.add.at(out[tgt], idx, blk)
+    return out
+
+
+def _same(a, b):
+    a, b = sp.csr_matrix(a), sp.csr_matrix(b)
+    assert a.shape == b.shape
+    assert np.array_equal(a.indptr, b.indptr)
+    assert np.array_equal(a.indices, b.indices)
+    assert np.array_equal(a.data, b.data)  # bit-exact (no tolerance)
+
+
+@pytest.mark.parametrize("boxes,p,mode", CASES)
+def test_pattern_and_jobs_reproduce_host_scatter(boxes, p, mode):
+    disc = _disc(boxes, p, mode)
+    m = len(disc.leaves[0].boundary_ids)
+    rng = np.random.default_rng(len(disc.leaves) * 31 + p)
+    dtn = rng.standard_normal((len(disc.leaves), m, m))
+    t_ref, c_ref = _host(disc, dtn)
+    pat = InterfacePattern(disc)
+    ids = list(range(len(disc.leaves)))
+    t_vals, c_vals = _replay(pat, dtn, ids)
+    t, c = pat.matrices(t_vals, c_vals)
+    _same(t, t_ref)
+    _same(c, c_ref)
+
+
+def test_flushes_in_any_order_give_the_same_values():
+    disc = _disc((3, 2, 2), 5, "drop")
+    m = len(disc.leaves[0].boundary_ids)
+    dtn = np.random.default_rng(3).standard_normal((len(disc.leaves), m, m))
+    pat = InterfacePattern(disc)
+    full = _replay(pat, dtn, list(range(len(disc.leaves))))
+    order = [7, 2, 11, 0, 5, 9, 1, 3, 10, 4, 8, 6]
+    acc = [np.zeros(pat.nnz[0]), np.zeros(pat.nnz[1])]
+    for chunk in (order[:5], order[5:]):
+        part = _replay(pat, dtn[chunk], chunk)
+        acc[0] += part[0]
+        acc[1] += part[1]
+    assert np.array_equal(acc[0], full[0]) and np.array_equal(acc[1], full[1])
+
+
+def test_every_entry_has_at_most_two_contributors():
+    """The bit-exactness argument: 0 + x + y is order independent."""
+    disc = _disc((3, 2, 2), 5, "drop")
+    pat = InterfacePattern(disc)
+    m = len(disc.leaves[0].boundary_ids)
+    count = _replay(pat, np.ones((len(disc.leaves), m, m)), list(range(len(disc.leaves))))
+    assert count[0].max() == 2 and count[0].min() >= 1
+    assert count[1].max() == 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("boxes,p,mode", CASES)
+def test_device_scatter_is_bit_exact(boxes, p, mode):
+    import torch
+    from paper_2503_04033_b200.assembly import DeviceAssembler
+    disc = _disc(boxes, p, mode)
+    m = len(disc.leaves[0].boundary_ids)
+    dtn = np.random.default_rng(7).standard_normal((len(disc.leaves), m, m))
+    t_ref, c_ref = _host(disc, dtn)
+    asm = DeviceAssembler(InterfacePattern(disc), 0)
+    ids = list(range(len(disc.leaves)))
+    for lo in range(0, len(ids), 5):  # several flushes
+        chunk = ids[lo:lo + 5]
+        asm.add(torch.from_numpy(dtn[chunk]).cuda(), chunk)
+    t, c = asm.finish()
+    _same(t, t_ref)
+    _same(c, c_ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("boxes,p", [((2, 2, 2), 8), ((4, 3), 10)])
+def test_build_device_and_host_assembly_identical(boxes, p, monkeypatch):
+    from paper_2503_04033_b200.condensation import build
+    from paper_2503_04033_b200.local_ops import isotropic_field
+    disc = _disc(boxes, p, "drop")
+    field = isotropic_field(len(boxes), zeroth=lambda x: -150.0 * (1.0 - 0.5 * np.exp(-((x - 0.4) ** 2).sum(1) / 0.05)))
+    monkeypatch.setenv("HPS_HOST_ASSEMBLY", "1")
+    host = build(disc, field)
+    monkeypatch.setenv("HPS_HOST_ASSEMBLY", "0")
+    dev = build(disc, field)
+    _same(dev.t, host.t)
+    _same(dev.dirichlet_coupling, host.dirichlet_coupling)

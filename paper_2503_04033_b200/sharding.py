@@ -5,7 +5,10 @@ into contiguous shards, one per rank; every rank reduces its shard on its own
 GPU with no collective on the data path.  The only exchange is the return of
 the finished DtN blocks to the rank that owns the host-side sparse assembly
 and factorization (paper §3.2: DtNs are "transferred collectively to the
-CPU"), done once per flush with a gather.
+CPU"), done once per flush with a gather — or, with the interface assembly
+on the device (``sharded_interface``), one sum-reduce of each rank's partial
+CSR values of T and C, which carries nnz(T) + nnz(C) doubles instead of every
+m x m map and leaves root nothing to scatter.
 """
 
 from __future__ import annotations
@@ -85,3 +88,51 @@ def sharded_dtn(disc, coeffs, world: int, rank: int,
     for part_ids, part_blocks in parts:
         out[part_ids] = part_blocks
     return out
+
+
+def sharded_interface(disc, coeffs, world: int, rank: int, root: int = 0, pattern=None,
+                      compute: Optional[Callable[[np.ndarray], np.ndarray]] = None,
+                      scatter: Optional[Callable] = None, template=None):
+    """T and the Dirichlet coupling C, assembled from every rank's leaf shard.
+
+    Each rank reduces its shard and adds the DtN maps into its own partial CSR
+    values of T and C (``hps_interface_scatter`` on its GPU); one sum-reduce
+    of the value arrays onto ``root`` is the only exchange.  An entry of T has
+    at most two nonzero partials and x + 0 = x, so the result is bit-identical
+    to a single-process assembly.  ``compute`` / ``scatter`` replace the
+    rank's GPU (pack -> DtN maps; (pattern, maps, ids) -> (t_vals, c_vals))
+    for CPU tests.  Returns (T, C) on root, None elsewhere.
+    """
+    import torch
+    import torch.distributed as dist
+    from .assembly import DeviceAssembler, InterfacePattern
+    from .condensation import interior_points
+    from .local_ops import LeafTemplate, check_pivots, pack_coefficients
+    pattern = pattern or InterfacePattern(disc)
+    start, stop = shard_range(len(disc.leaves), world, rank)
+    ids = list(range(start, stop))
+    pack = pack_coefficients(coeffs, interior_points(disc, ids), len(ids)) if ids else None
+    if compute is None:
+        from .engine import LeafEngine
+        template = template or LeafTemplate(disc.leaf_widths, disc.p, disc.corner_mode,
+                                            coeffs.has_cross_terms)
+        device = torch.cuda.current_device()
+        asm = DeviceAssembler(pattern, device)
+        if ids:
+            eng = LeafEngine.for_template(template, coeffs, device=device)
+            dtn, stats = eng.dtn(pack)
+            check_pivots(stats.cpu().numpy(), [disc.leaves[i].index for i in ids])
+            asm.add(dtn, ids)
+        vals = [asm.t_vals[:pattern.nnz[0]], asm.c_vals[:pattern.nnz[1]]]
+    else:
+        if ids:
+            t_vals, c_vals = scatter(pattern, compute(pack), ids)
+        else:
+            t_vals, c_vals = np.zeros(pattern.nnz[0]), np.zeros(pattern.nnz[1])
+        vals = [torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)) for v in (t_vals, c_vals)]
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        for v in vals:
+            dist.reduce(v, dst=root, op=dist.ReduceOp.SUM)
+        if dist.get_rank() != root:
+            return None
+    return pattern.matrices(vals[0].cpu().numpy(), vals[1].cpu().numpy())

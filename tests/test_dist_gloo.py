@@ -77,3 +77,56 @@ def test_sharded_build_matches_single_process(tmp_path):
                                                    len(disc.leaves)))
     assert np.array_equal(res["blocks"], full)
     assert float(res["slowest"]) == 2.0
+
+
+def _replay_scatter(pattern, dtn, ids):
+    """numpy replay of hps_interface_scatter (the rank's GPU in this CPU test)."""
+    out = [np.zeros(pattern.nnz[0]), np.zeros(pattern.nnz[1])]
+    for k, r0, c0, nr, nc, tgt, base, stride in pattern.jobs_for(ids):
+        idx = base + np.arange(nr)[:, None] * stride + np.arange(nc)[None, :]
+        np.add.at(out[tgt], idx, dtn[k, r0:r0 + nr, c0:c0 + nc])
+    return out
+
+
+def _interface_worker(rank, world, port, out_path):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2503_04033_b200.sharding import sharded_interface
+        spec, disc = _problem()
+        res = sharded_interface(disc, spec.coeffs, world, rank, compute=_oracle_compute(disc),
+                                scatter=_replay_scatter)
+        if rank == 0:
+            t, c = res
+            np.savez(out_path, t_data=t.data, t_indices=t.indices, t_indptr=t.indptr,
+                     c_data=c.data, c_indices=c.indices, c_indptr=c.indptr)
+        else:
+            assert res is None
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_interface_reduce_matches_host_assembly(tmp_path, world):
+    """Partial CSR values of T and C per rank, one sum-reduce: bit-identical to
+    the single-process host scatter of all DtN maps."""
+    out = str(tmp_path / "iface.npz")
+    mp.start_processes(_interface_worker, args=(world, _free_port(), out), nprocs=world,
+                       start_method="spawn")
+    res = np.load(out)
+    spec, disc = _problem()
+    from paper_2503_04033_b200.condensation import (_make_dof_map, finalize_host, interior_points,
+                                                    scatter_leaf_blocks)
+    from paper_2503_04033_b200.local_ops import LeafTemplate, pack_coefficients
+    from paper_2503_04033_b200.sparse_backend import SparseMatrix
+    ids = list(range(len(disc.leaves)))
+    full = _oracle_compute(disc)(pack_coefficients(spec.coeffs, interior_points(disc, ids), len(ids)))
+    dof_map = _make_dof_map(disc, LeafTemplate(disc.leaf_widths, disc.p, disc.corner_mode, False))
+    tb, cr, cc, cv = SparseMatrix(disc.n_interface), [], [], []
+    scatter_leaf_blocks(dof_map, ids, full, tb, cr, cc, cv)
+    t, c = finalize_host(tb, cr, cc, cv, disc.n_interface, disc.n_dirichlet)
+    for name, ref in (("t", t), ("c", c)):
+        assert np.array_equal(res[f"{name}_indptr"], ref.indptr)
+        assert np.array_equal(res[f"{name}_indices"], ref.indices)
+        assert np.array_equal(res[f"{name}_data"], ref.data)

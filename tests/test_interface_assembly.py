@@ -124,3 +124,18 @@ def test_build_device_and_host_assembly_identical(boxes, p, monkeypatch):
     dev = build(disc, field)
     _same(dev.t, host.t)
     _same(dev.dirichlet_coupling, host.dirichlet_coupling)
+
+
+@pytest.mark.gpu
+def test_sharded_interface_single_rank_matches_build():
+    import torch
+    from paper_2503_04033_b200 import make_problem
+    from paper_2503_04033_b200.condensation import build
+    from paper_2503_04033_b200.sharding import sharded_interface
+    spec = make_problem("bump_helmholtz", d=3, kappa=20.0)
+    disc = build_discretization(spec.domain, MeshConfig((3, 2, 2), 8))
+    torch.cuda.set_device(0)
+    t, c = sharded_interface(disc, spec.coeffs, 1, 0)
+    ref = build(disc, spec.coeffs)
+    _same(t, ref.t)
+    _same(c, ref.dirichlet_coupling)

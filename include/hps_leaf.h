@@ -102,14 +102,15 @@ int hps_leaf_interior_solve(hps_plan_t plan, int n_leaves, const double* coeffs,
 
 /* Interface assembly (reference condensation.py:230-246, the scatter of each
  * leaf's DtN map T^tau into the interface matrix T and the Dirichlet coupling):
- * blocks = device DtN maps, block k at blocks + k * block_stride, row stride ld;
- * jobs = device int64 [n_jobs][8] = {block k, row0, col0, rows, cols, target
+ * blocks = device DtN maps of leaves leaf0, leaf0 + 1, ...: leaf l at
+ * blocks + (l - leaf0) * block_stride, row stride ld;
+ * jobs = device int64 [n_jobs][8] = {leaf l, row0, col0, rows, cols, target
  * (0: out_t, 1: out_c), base, row stride}; adds block rows into
  * target[base + a * stride + b] (the CSR value arrays, zeroed by the caller).
  * Entries with at most two contributors are bit-identical to the host COO sum. */
 int hps_interface_scatter(int device, const double* blocks, long long ld, long long block_stride,
-                          int n_jobs, const long long* jobs, double* out_t, double* out_c,
-                          void* stream);
+                          long long leaf0, int n_jobs, const long long* jobs, double* out_t,
+                          double* out_c, void* stream);
 
 #ifdef __cplusplus
 }

@@ -48,8 +48,8 @@ def _sig(lib):
     lib.hps_leaf_interior_solve.argtypes = [_P, _I, _P, _P, _P, _P, _P, _P]
     lib.hps_leaf_solution_operator.argtypes = [_P, _I, _P, _P, _P, _P]
     lib.hps_plan_set_profile.argtypes = [_P, _P]
-    lib.hps_interface_scatter.argtypes = [_I, _P, ctypes.c_longlong, ctypes.c_longlong, _I, _P, _P,
-                                          _P, _P]
+    lib.hps_interface_scatter.argtypes = [_I, _P, ctypes.c_longlong, ctypes.c_longlong,
+                                          ctypes.c_longlong, _I, _P, _P, _P, _P]
     for name in EXPORTS:
         if name not in ("hps_abi_version", "hps_last_error", "hps_device_count"):
             getattr(lib, name).restype = _I

@@ -100,6 +100,12 @@ class InterfacePattern:
                     jobs.append((offs[fi], offs[gi], size[fk], size[gk], t,
                                  base[t][fk] + cols[(t, fk)][gk], stride))
             self.leaf_jobs.append(np.asarray(jobs, dtype=np.int64).reshape(-1, 7))
+        counts = [len(j) for j in self.leaf_jobs]
+        self.job_offsets = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        # every leaf's jobs with its global leaf id in column 0 (uploaded once)
+        self.all_jobs = np.concatenate(
+            [np.repeat(np.arange(len(counts), dtype=np.int64), counts)[:, None],
+             np.concatenate(self.leaf_jobs) if counts else np.empty((0, 7), np.int64)], axis=1)
 
     def jobs_for(self, ids) -> np.ndarray:
         """int64 [jobs][8] for a flush of leaves ids (column 0 = position in the flush)."""
@@ -126,6 +132,7 @@ class DeviceAssembler:
         dev = f"cuda:{self.device}"
         self.t_vals = torch.zeros(max(pattern.nnz[0], 1), dtype=torch.float64, device=dev)
         self.c_vals = torch.zeros(max(pattern.nnz[1], 1), dtype=torch.float64, device=dev)
+        self.jobs = torch.from_numpy(np.ascontiguousarray(pattern.all_jobs)).to(dev)
         self.lib = _native.load()
 
     def add(self, dtn, ids, stream=None) -> None:
@@ -134,14 +141,23 @@ class DeviceAssembler:
         if dtn.dim() != 3 or dtn.shape[0] != len(ids) or dtn.shape[1] != dtn.shape[2]:
             raise ConfigError(f"DtN batch of shape {tuple(dtn.shape)} for {len(ids)} leaves")
         dtn = dtn.contiguous()
-        jobs_h = self.pattern.jobs_for(ids)
-        if len(jobs_h) == 0:
+        ids = list(ids)
+        if not ids:
             return
-        jobs = torch.from_numpy(jobs_h).to(f"cuda:{self.device}", non_blocking=False)
+        off = self.pattern.job_offsets
+        if ids == list(range(ids[0], ids[0] + len(ids))):  # a contiguous flush: the resident table
+            lo, hi = int(off[ids[0]]), int(off[ids[-1] + 1])
+            jobs, n_jobs, leaf0 = self.jobs[lo:hi], hi - lo, ids[0]
+        else:
+            jobs_h = self.pattern.jobs_for(ids)
+            jobs = torch.from_numpy(jobs_h).to(f"cuda:{self.device}")
+            n_jobs, leaf0 = len(jobs_h), 0
+        if n_jobs == 0:
+            return
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         m = int(dtn.shape[1])
         _native.check(self.lib.hps_interface_scatter(
-            self.device, ctypes.c_void_p(dtn.data_ptr()), m, m * m, len(jobs_h),
+            self.device, ctypes.c_void_p(dtn.data_ptr()), m, m * m, leaf0, n_jobs,
             ctypes.c_void_p(jobs.data_ptr()), ctypes.c_void_p(self.t_vals.data_ptr()),
             ctypes.c_void_p(self.c_vals.data_ptr()), ctypes.c_void_p(s.cuda_stream)))
         self._keep = (dtn, jobs)  # alive until the next add / finish

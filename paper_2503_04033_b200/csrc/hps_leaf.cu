@@ -2754,16 +2754,21 @@ static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, c
 // COO -> CSR sum bit for bit.  HBM-bound: 8 bytes read + one 8-byte atomic
 // per element; warps walk rows, lanes walk columns (coalesced both sides).
 __global__ void __launch_bounds__(256) hps_interface_scatter_kernel(
-    const double* __restrict__ blocks, long long ld, long long block_stride,
+    const double* __restrict__ blocks, long long ld, long long block_stride, long long leaf0,
     const long long* __restrict__ jobs, double* __restrict__ out0, double* __restrict__ out1) {
   const long long* j = jobs + 8 * (long long)blockIdx.x;
-  const long long leaf = j[0], r0 = j[1], c0 = j[2], nr = j[3], nc = j[4];
+  const long long leaf = j[0] - leaf0, r0 = j[1], c0 = j[2];
+  const int nr = (int)j[3], nc = (int)j[4];
   double* out = (j[5] ? out1 : out0) + j[6];
   const long long stride = j[7];
   const double* src = blocks + leaf * block_stride + r0 * ld + c0;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (long long a = warp; a < nr; a += blockDim.x >> 5)
-    for (long long b = lane; b < nc; b += 32) atomicAdd(out + a * stride + b, __ldg(src + a * ld + b));
+  // flattened over the block so that narrow faces (nc < 32 at low p) keep
+  // every lane busy; consecutive threads stay on consecutive columns
+  const int total = nr * nc;
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int a = e / nc, b = e - a * nc;
+    atomicAdd(out + a * stride + b, __ldg(src + a * ld + b));
+  }
 }
 
 extern "C" {
@@ -3209,13 +3214,13 @@ int hps_leaf_dtn_host(hps_plan_t P, int n_leaves, const double* coeffs_host, dou
 }
 
 int hps_interface_scatter(int device, const double* blocks, long long ld, long long block_stride,
-                          int n_jobs, const long long* jobs, double* out_t, double* out_c,
-                          void* stream) {
+                          long long leaf0, int n_jobs, const long long* jobs, double* out_t,
+                          double* out_c, void* stream) {
   if (n_jobs < 0 || ld <= 0 || block_stride < 0) return fail("hps_interface_scatter: bad sizes");
   if (n_jobs == 0) return 0;
   if (!blocks || !jobs || !out_t) return fail("hps_interface_scatter: null pointer");
   CK(cudaSetDevice(device));
-  hps_interface_scatter_kernel<<<n_jobs, 256, 0, (cudaStream_t)stream>>>(blocks, ld, block_stride, jobs,
+  hps_interface_scatter_kernel<<<n_jobs, 256, 0, (cudaStream_t)stream>>>(blocks, ld, block_stride, leaf0, jobs,
                                                                         out_t, out_c ? out_c : out_t);
   CK(cudaGetLastError());
   return 0;

@@ -82,6 +82,17 @@ def test_flushes_in_any_order_give_the_same_values():
     assert np.array_equal(acc[0], full[0]) and np.array_equal(acc[1], full[1])
 
 
+def test_resident_job_table_matches_per_flush_jobs():
+    pat = InterfacePattern(_disc((3, 2, 2), 5, "drop"))
+    n = len(pat.leaf_jobs)
+    per_flush = pat.jobs_for(range(n))
+    assert np.array_equal(pat.all_jobs, per_flush)  # position == global id for the full range
+    lo, hi = pat.job_offsets[4], pat.job_offsets[9]
+    sub = pat.jobs_for(range(4, 9))
+    assert np.array_equal(pat.all_jobs[lo:hi, 1:], sub[:, 1:])
+    assert np.array_equal(pat.all_jobs[lo:hi, 0] - 4, sub[:, 0])
+
+
 def test_every_entry_has_at_most_two_contributors():
     """The bit-exactness argument: 0 + x + y is order independent."""
     disc = _disc((3, 2, 2), 5, "drop")
@@ -103,9 +114,15 @@ def test_device_scatter_is_bit_exact(boxes, p, mode):
     t_ref, c_ref = _host(disc, dtn)
     asm = DeviceAssembler(InterfacePattern(disc), 0)
     ids = list(range(len(disc.leaves)))
-    for lo in range(0, len(ids), 5):  # several flushes
-        chunk = ids[lo:lo + 5]
-        asm.add(torch.from_numpy(dtn[chunk]).cuda(), chunk)
+    perm = list(np.random.default_rng(1).permutation(len(ids)))
+    flushes = [ids[lo:lo + 5] for lo in range(0, len(ids), 5)]  # contiguous: resident job table
+    flushes = flushes[1::2]
+    done = {i for f in flushes for i in f}
+    rest = [int(i) for i in perm if i not in done]  # non-contiguous: per-flush job tables
+    flushes += [rest[:len(rest) // 2], rest[len(rest) // 2:]]
+    for chunk in flushes:
+        if chunk:
+            asm.add(torch.from_numpy(dtn[chunk]).cuda(), chunk)
     t, c = asm.finish()
     _same(t, t_ref)
     _same(c, c_ref)

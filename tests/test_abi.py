@@ -54,3 +54,30 @@ def test_no_cpu_fallback():
     from paper_2503_04033_b200.local_ops import LeafTemplate
     with pytest.raises(NativeUnavailableError):
         LeafEngine(LeafTemplate((1.0, 1.0, 1.0), 6, "drop", False), False, True)
+
+
+def test_interface_scatter_argument_errors():
+    """hps_interface_scatter validates sizes and pointers before touching the
+    device (same error convention as the other entry points), and an empty job
+    list is a no-op."""
+    lib = _native.load()
+    assert lib.hps_interface_scatter(0, None, 0, 0, 0, 5, None, None, None, None) != 0
+    assert b"bad sizes" in lib.hps_last_error()
+    assert lib.hps_interface_scatter(0, None, 4, 16, 0, -1, None, None, None, None) != 0
+    assert lib.hps_interface_scatter(0, None, 4, 16, 0, 3, None, None, None, None) != 0
+    assert b"null pointer" in lib.hps_last_error()
+    assert lib.hps_interface_scatter(0, None, 4, 16, 0, 0, None, None, None, None) == 0
+
+
+def test_no_cpu_fallback_for_device_assembly():
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("GPU present")
+    except ImportError:
+        pass
+    from paper_2503_04033_b200.assembly import DeviceAssembler, InterfacePattern
+    from paper_2503_04033_b200.geometry import DomainBox, MeshConfig, build_discretization
+    pat = InterfacePattern(build_discretization(DomainBox((0.0, 0.0), (1.0, 1.0)), MeshConfig((2, 2), 6)))
+    with pytest.raises(Exception):
+        DeviceAssembler(pat, 0)

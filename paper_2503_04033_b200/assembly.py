@@ -76,13 +76,14 @@ class InterfacePattern:
             np.cumsum(per_row, out=indptr[1:])
             nnz = int(indptr[-1])
             idx_t = np.int32 if max(nnz, self.n_int, self.n_dir) < 2 ** 31 - 1 else np.int64
-            parts = []
-            for i, key in enumerate(iface):
+            indices = np.empty(nnz, dtype=idx_t)
+            for i, key in enumerate(iface):  # rows of a face share one column list: broadcast it
                 sel = list(cols[(t, key)])
                 row = _ranges(np.asarray([start[g] for g in sel], dtype=np.int64),
                               np.asarray([size[g] for g in sel], dtype=np.int64))
-                parts.append(np.tile(row.astype(idx_t), size[key]))
-            self.indices.append(np.concatenate(parts) if parts else np.empty(0, dtype=idx_t))
+                b0 = int(indptr[start[key]])
+                indices[b0:b0 + size[key] * len(row)].reshape(size[key], len(row))[:] = row
+            self.indices.append(indices)
             self.indptr.append(indptr.astype(idx_t))
             base.append({key: int(indptr[start[key]]) for key in iface})
         self.nnz = (int(self.indptr[0][-1]), int(self.indptr[1][-1]))

@@ -1,6 +1,6 @@
 # round-end style verification on HEAD: GPU tests, smoke, default bench, reference arm
 set -x
-O=gpurun_out/c6; mkdir -p $O
+O=gpurun_out/${OUT:-c6}; mkdir -p $O
 timeout 900 python -m pytest tests -m gpu -x -q > $O/gpu_tests.log 2>&1; echo "tests rc=$?" >> $O/gpu_tests.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke.log 2>&1
 timeout 600 python bench.py > $O/bench_default.json 2> $O/bench_default.err

@@ -135,6 +135,7 @@ class DeviceAssembler:
         self.c_vals = torch.zeros(max(pattern.nnz[1], 1), dtype=torch.float64, device=dev)
         self.jobs = torch.from_numpy(np.ascontiguousarray(pattern.all_jobs)).to(dev)
         self.lib = _native.load()
+        self._keep = None  # the last flush's maps / job table, alive until the kernel is ordered
 
     def add(self, dtn, ids, stream=None) -> None:
         """Scatter-add the DtN maps of a flush (device tensor [len(ids)][m][m])."""

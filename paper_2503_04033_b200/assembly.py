@@ -101,18 +101,32 @@ class InterfacePattern:
                     jobs.append((offs[fi], offs[gi], size[fk], size[gk], t,
                                  base[t][fk] + cols[(t, fk)][gk], stride))
             self.leaf_jobs.append(np.asarray(jobs, dtype=np.int64).reshape(-1, 7))
-        counts = [len(j) for j in self.leaf_jobs]
-        self.job_offsets = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
-        # every leaf's jobs with its global leaf id in column 0 (uploaded once)
-        self.all_jobs = np.concatenate(
-            [np.repeat(np.arange(len(counts), dtype=np.int64), counts)[:, None],
-             np.concatenate(self.leaf_jobs) if counts else np.empty((0, 7), np.int64)], axis=1)
+        # vector jobs (interface fluxes into g_b): one column per interface face
+        self.leaf_vec_jobs = [
+            np.asarray([(offs_l[fi], 0, size[fk], 1, 0, start[fk], 1)
+                        for fi, fk in enumerate(leaf.face_keys) if disc.faces[fk].kind == INTERFACE],
+                       dtype=np.int64).reshape(-1, 7)
+            for leaf in disc.leaves
+            for offs_l in [np.concatenate([[0], np.cumsum([size[k] for k in leaf.face_keys])])]]
+        self.job_offsets, self.all_jobs = self._table(self.leaf_jobs)
+        self.vec_offsets, self.all_vec_jobs = self._table(self.leaf_vec_jobs)
 
-    def jobs_for(self, ids) -> np.ndarray:
+    @staticmethod
+    def _table(leaf_jobs):
+        """Every leaf's jobs with its global leaf id in column 0, and per-leaf row offsets."""
+        counts = [len(j) for j in leaf_jobs]
+        offsets = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        table = np.concatenate(
+            [np.repeat(np.arange(len(counts), dtype=np.int64), counts)[:, None],
+             np.concatenate(leaf_jobs) if counts else np.empty((0, 7), np.int64)], axis=1)
+        return offsets, table
+
+    def jobs_for(self, ids, vectors: bool = False) -> np.ndarray:
         """int64 [jobs][8] for a flush of leaves ids (column 0 = position in the flush)."""
+        source = self.leaf_vec_jobs if vectors else self.leaf_jobs
         parts = []
         for k, leaf_id in enumerate(ids):
-            j = self.leaf_jobs[leaf_id]
+            j = source[leaf_id]
             parts.append(np.concatenate([np.full((len(j), 1), k, dtype=np.int64), j], axis=1))
         return np.ascontiguousarray(np.concatenate(parts) if parts else np.empty((0, 8), np.int64))
 
@@ -125,44 +139,65 @@ class InterfacePattern:
 
 
 class DeviceAssembler:
-    """Accumulates flushes of device DtN maps into device CSR values of T and C."""
+    """Accumulates flushes of device DtN maps into device CSR values of T and C
+    (or, with ``vectors=True``, interface fluxes into the interface RHS)."""
 
-    def __init__(self, pattern: InterfacePattern, device: int):
+    def __init__(self, pattern: InterfacePattern, device: int, vectors: bool = False):
         import torch
         self.torch, self.pattern, self.device = torch, pattern, int(device)
         dev = f"cuda:{self.device}"
-        self.t_vals = torch.zeros(max(pattern.nnz[0], 1), dtype=torch.float64, device=dev)
-        self.c_vals = torch.zeros(max(pattern.nnz[1], 1), dtype=torch.float64, device=dev)
-        self.jobs = torch.from_numpy(np.ascontiguousarray(pattern.all_jobs)).to(dev)
         self.lib = _native.load()
-        self._keep = None  # the last flush's maps / job table, alive until the kernel is ordered
+        if vectors:
+            self.g = torch.zeros(max(pattern.n_int, 1), dtype=torch.float64, device=dev)
+            table, self.offsets = pattern.all_vec_jobs, pattern.vec_offsets
+        else:
+            self.t_vals = torch.zeros(max(pattern.nnz[0], 1), dtype=torch.float64, device=dev)
+            self.c_vals = torch.zeros(max(pattern.nnz[1], 1), dtype=torch.float64, device=dev)
+            table, self.offsets = pattern.all_jobs, pattern.job_offsets
+        self.vectors = vectors
+        self.jobs = torch.from_numpy(np.ascontiguousarray(table)).to(dev)  # uploaded once
+        self._keep = None  # the last flush's inputs / job table, alive until the kernel is ordered
 
-    def add(self, dtn, ids, stream=None) -> None:
-        """Scatter-add the DtN maps of a flush (device tensor [len(ids)][m][m])."""
+    def _launch(self, blocks, ld: int, block_stride: int, ids, out0, out1, stream) -> None:
         torch = self.torch
-        if dtn.dim() != 3 or dtn.shape[0] != len(ids) or dtn.shape[1] != dtn.shape[2]:
-            raise ConfigError(f"DtN batch of shape {tuple(dtn.shape)} for {len(ids)} leaves")
-        dtn = dtn.contiguous()
         ids = list(ids)
         if not ids:
             return
-        off = self.pattern.job_offsets
+        off = self.offsets
         if ids == list(range(ids[0], ids[0] + len(ids))):  # a contiguous flush: the resident table
             lo, hi = int(off[ids[0]]), int(off[ids[-1] + 1])
             jobs, n_jobs, leaf0 = self.jobs[lo:hi], hi - lo, ids[0]
         else:
-            jobs_h = self.pattern.jobs_for(ids)
+            jobs_h = self.pattern.jobs_for(ids, vectors=self.vectors)
             jobs = torch.from_numpy(jobs_h).to(f"cuda:{self.device}")
             n_jobs, leaf0 = len(jobs_h), 0
         if n_jobs == 0:
             return
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
-        m = int(dtn.shape[1])
         _native.check(self.lib.hps_interface_scatter(
-            self.device, ctypes.c_void_p(dtn.data_ptr()), m, m * m, leaf0, n_jobs,
-            ctypes.c_void_p(jobs.data_ptr()), ctypes.c_void_p(self.t_vals.data_ptr()),
-            ctypes.c_void_p(self.c_vals.data_ptr()), ctypes.c_void_p(s.cuda_stream)))
-        self._keep = (dtn, jobs)  # alive until the next add / finish
+            self.device, ctypes.c_void_p(blocks.data_ptr()), ld, block_stride, leaf0, n_jobs,
+            ctypes.c_void_p(jobs.data_ptr()), ctypes.c_void_p(out0.data_ptr()),
+            ctypes.c_void_p(out1.data_ptr()), ctypes.c_void_p(s.cuda_stream)))
+        self._keep = (blocks, jobs)
+
+    def add(self, dtn, ids, stream=None) -> None:
+        """Scatter-add the DtN maps of a flush (device tensor [len(ids)][m][m])."""
+        if self.vectors:
+            raise ConfigError("this assembler accumulates interface vectors")
+        if dtn.dim() != 3 or dtn.shape[0] != len(ids) or dtn.shape[1] != dtn.shape[2]:
+            raise ConfigError(f"DtN batch of shape {tuple(dtn.shape)} for {len(ids)} leaves")
+        dtn = dtn.contiguous()
+        m = int(dtn.shape[1])
+        self._launch(dtn, m, m * m, ids, self.t_vals, self.c_vals, stream)
+
+    def add_vectors(self, flux, ids, stream=None) -> None:
+        """Add the interface part of per-leaf boundary vectors (device [len(ids)][m])."""
+        if not self.vectors:
+            raise ConfigError("this assembler accumulates T and C")
+        if flux.dim() != 2 or flux.shape[0] != len(ids):
+            raise ConfigError(f"flux batch of shape {tuple(flux.shape)} for {len(ids)} leaves")
+        flux = flux.contiguous()
+        self._launch(flux, 1, int(flux.shape[1]), ids, self.g, self.g, stream)
 
     def finish(self) -> Tuple[sp.csr_matrix, sp.csr_matrix]:
         nt, nc = self.pattern.nnz
@@ -170,3 +205,7 @@ class DeviceAssembler:
         c_vals = self.c_vals[:nc].cpu().numpy()
         self._keep = None
         return self.pattern.matrices(t_vals, c_vals)
+
+    def finish_vector(self) -> np.ndarray:
+        self._keep = None
+        return self.g[:self.pattern.n_int].cpu().numpy()

@@ -156,3 +156,38 @@ def test_sharded_interface_single_rank_matches_build():
     ref = build(disc, spec.coeffs)
     _same(t, ref.t)
     _same(c, ref.dirichlet_coupling)
+
+
+@pytest.mark.parametrize("boxes,p,mode", CASES)
+def test_vector_jobs_reproduce_host_flux_sum(boxes, p, mode):
+    """g_b = -(sum of interface fluxes) through the vector jobs == the host loop
+    g_b[t_rows] -= flux (reference condensation.py:314-323), bit for bit."""
+    disc = _disc(boxes, p, mode)
+    m = len(disc.leaves[0].boundary_ids)
+    flux = np.random.default_rng(5).standard_normal((len(disc.leaves), m))
+    tpl = LeafTemplate(disc.leaf_widths, disc.p, disc.corner_mode, False)
+    dof_map = _make_dof_map(disc, tpl)
+    ref = np.zeros(disc.n_interface)
+    for k, dofs in enumerate(dof_map.per_leaf):
+        ref[dofs.t_rows] -= flux[k][dofs.interface_mask]
+    pat = InterfacePattern(disc)
+    acc = np.zeros(disc.n_interface)
+    for k, r0, c0, nr, nc, tgt, base, stride in pat.jobs_for(range(len(disc.leaves)), vectors=True):
+        assert (c0, nc, tgt, stride) == (0, 1, 0, 1)
+        np.add.at(acc, base + np.arange(nr), flux[k, r0:r0 + nr])
+    assert np.array_equal(-acc, ref)
+
+
+@pytest.mark.gpu
+def test_reduce_load_device_and_host_identical(monkeypatch):
+    from paper_2503_04033_b200 import make_problem
+    from paper_2503_04033_b200.condensation import build, reduce_load
+    spec = make_problem("bump_helmholtz", d=3, kappa=20.0)
+    disc = build_discretization(spec.domain, MeshConfig((3, 2, 2), 8))
+    sys_ = build(disc, spec.coeffs)
+    assert sys_.pattern is not None
+    v_dev, g_dev = reduce_load(disc, spec.coeffs, spec.f, spec.g, sys_)
+    monkeypatch.setenv("HPS_HOST_ASSEMBLY", "1")
+    v_host, g_host = reduce_load(disc, spec.coeffs, spec.f, spec.g, sys_)
+    assert np.array_equal(g_dev, g_host)
+    assert all(np.array_equal(a, b) for a, b in zip(v_dev, v_host))

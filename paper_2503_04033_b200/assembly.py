@@ -19,6 +19,7 @@ has at most two contributors and IEEE addition is commutative.
 from __future__ import annotations
 
 import ctypes
+from itertools import accumulate
 from typing import Dict, List, Tuple
 
 import numpy as np
@@ -29,15 +30,6 @@ from .errors import ConfigError
 from .geometry import Discretization
 
 INTERFACE = "interface"
-
-
-def _ranges(starts: np.ndarray, sizes: np.ndarray) -> np.ndarray:
-    """Concatenation of arange(s, s + n) over (s, n) pairs."""
-    if len(sizes) == 0:
-        return np.empty(0, dtype=np.int64)
-    tot = int(sizes.sum())
-    first = np.repeat(starts - np.concatenate([[0], np.cumsum(sizes)[:-1]]), sizes)
-    return first + np.arange(tot, dtype=np.int64)
 
 
 class InterfacePattern:
@@ -65,8 +57,8 @@ class InterfacePattern:
                     nb.update(disc.leaves[leaf_id].face_keys)
             for t, kind in enumerate((True, False)):
                 sel = sorted((g for g in nb if (disc.faces[g].kind == INTERFACE) == kind), key=start.get)
-                offs = np.concatenate([[0], np.cumsum([size[g] for g in sel])]).astype(np.int64)
-                cols[(t, key)] = dict(zip(sel, offs[:-1].tolist()))
+                offs = list(accumulate((size[g] for g in sel), initial=0))
+                cols[(t, key)] = dict(zip(sel, offs[:-1]))
                 row_len[t, i] = offs[-1]
         sizes = np.asarray([size[k] for k in iface], dtype=np.int64)
         self.indptr, self.indices, base = [], [], []
@@ -77,21 +69,22 @@ class InterfacePattern:
             nnz = int(indptr[-1])
             idx_t = np.int32 if max(nnz, self.n_int, self.n_dir) < 2 ** 31 - 1 else np.int64
             indices = np.empty(nnz, dtype=idx_t)
-            for i, key in enumerate(iface):  # rows of a face share one column list: broadcast it
-                sel = list(cols[(t, key)])
-                row = _ranges(np.asarray([start[g] for g in sel], dtype=np.int64),
-                              np.asarray([size[g] for g in sel], dtype=np.int64))
-                b0 = int(indptr[start[key]])
+            bases = indptr[[start[key] for key in iface]].tolist() if iface else []
+            for key, b0 in zip(iface, bases):  # rows of a face share one column list: broadcast it
+                sel = cols[(t, key)]
+                if not sel:
+                    continue
+                row = np.concatenate([np.arange(start[g], start[g] + size[g]) for g in sel])
                 indices[b0:b0 + size[key] * len(row)].reshape(size[key], len(row))[:] = row
             self.indices.append(indices)
             self.indptr.append(indptr.astype(idx_t))
-            base.append({key: int(indptr[start[key]]) for key in iface})
+            base.append(dict(zip(iface, bases)))
         self.nnz = (int(self.indptr[0][-1]), int(self.indptr[1][-1]))
         pos = {k: i for i, k in enumerate(iface)}
         self.leaf_jobs: List[np.ndarray] = []
         for leaf in disc.leaves:
             jobs = []
-            offs = np.concatenate([[0], np.cumsum([size[k] for k in leaf.face_keys])])
+            offs = list(accumulate((size[k] for k in leaf.face_keys), initial=0))
             for fi, fk in enumerate(leaf.face_keys):
                 if disc.faces[fk].kind != INTERFACE:
                     continue
@@ -107,7 +100,7 @@ class InterfacePattern:
                         for fi, fk in enumerate(leaf.face_keys) if disc.faces[fk].kind == INTERFACE],
                        dtype=np.int64).reshape(-1, 7)
             for leaf in disc.leaves
-            for offs_l in [np.concatenate([[0], np.cumsum([size[k] for k in leaf.face_keys])])]]
+            for offs_l in [list(accumulate((size[k] for k in leaf.face_keys), initial=0))]]
         self.job_offsets, self.all_jobs = self._table(self.leaf_jobs)
         self.vec_offsets, self.all_vec_jobs = self._table(self.leaf_vec_jobs)
 

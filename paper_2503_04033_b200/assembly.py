@@ -131,6 +131,16 @@ class InterfacePattern:
         return t, c
 
 
+def pattern_for(disc: Discretization) -> InterfacePattern:
+    """The mesh's pattern, built once per discretization (it depends only on
+    the face and leaf tables, which never change after construction)."""
+    pat = getattr(disc, "_interface_pattern", None)
+    if pat is None:
+        pat = InterfacePattern(disc)
+        disc._interface_pattern = pat
+    return pat
+
+
 class DeviceAssembler:
     """Accumulates flushes of device DtN maps into device CSR values of T and C
     (or, with ``vectors=True``, interface fluxes into the interface RHS)."""

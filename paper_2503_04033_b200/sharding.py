@@ -105,10 +105,10 @@ def sharded_interface(disc, coeffs, world: int, rank: int, root: int = 0, patter
     """
     import torch
     import torch.distributed as dist
-    from .assembly import DeviceAssembler, InterfacePattern
+    from .assembly import DeviceAssembler, pattern_for
     from .condensation import interior_points
     from .local_ops import LeafTemplate, check_pivots, pack_coefficients
-    pattern = pattern or InterfacePattern(disc)
+    pattern = pattern or pattern_for(disc)
     start, stop = shard_range(len(disc.leaves), world, rank)
     ids = list(range(start, stop))
     pack = pack_coefficients(coeffs, interior_points(disc, ids), len(ids)) if ids else None

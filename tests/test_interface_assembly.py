@@ -191,3 +191,10 @@ def test_reduce_load_device_and_host_identical(monkeypatch):
     v_host, g_host = reduce_load(disc, spec.coeffs, spec.f, spec.g, sys_)
     assert np.array_equal(g_dev, g_host)
     assert all(np.array_equal(a, b) for a, b in zip(v_dev, v_host))
+
+
+def test_pattern_is_built_once_per_discretization():
+    from paper_2503_04033_b200.assembly import pattern_for
+    disc = _disc((2, 2, 1), 6, "drop")
+    assert pattern_for(disc) is pattern_for(disc)
+    assert pattern_for(_disc((2, 2, 1), 6, "drop")) is not pattern_for(disc)

@@ -1,15 +1,22 @@
 """Leaf DtN throughput on B200: the two-level HPS solver's batched leaf-box reduction.
 
-Workload (BASELINE.json configs[2]): 3D variable-coefficient Helmholtz
+Headline workload (BASELINE.json configs[2]): 3D variable-coefficient Helmholtz
     -Lap u - kappa^2 b(x) u,  b(x) = 1 - 0.5 exp(-|x - c|^2 / (2 * 0.15^2)),
-p = 16 Chebyshev nodes per axis, 16 x 16 x 16 leaf boxes per GPU, kappa = 40.
-One step = the DtN maps of every leaf of the rank's shard (operator assembly,
-pivoted LU of A_ii, Schur complement), inputs resident in HBM.  Under torchrun
-each rank owns its own 16^3-leaf slab of a 16 x 16 x 16N leaf grid (weak
-scaling, no collective on the data path).
+p = 16 Chebyshev nodes per axis, one 16 x 16 x 16 leaf grid on the unit cube,
+kappa = 40.  One step = the DtN maps of every leaf of the rank's share
+(operator assembly, pivoted LU of A_ii, Schur complement), inputs resident in
+HBM.  Under torchrun the grid is split by leaf index — rank r owns leaves
+[L r / N, L (r + 1) / N) — with no collective on the data path (strong
+scaling: the grid is the same at every N).
 
-Prints ONE JSON line (rank 0).  ``--impl reference`` times the reference's CPU
-algorithm (the numpy/LAPACK oracle port in oracle/) on the host cores instead.
+Second workload, reported as the ``configs3`` sub-object (BASELINE configs[3]):
+p = 20, 16^3 leaves, kappa = 80, sharded across 8 GPUs by leaf index; rank r
+times share r (leaves 512 r .. 512 r + 511), so at N = 1 it is rank 0's share.
+
+Prints ONE JSON line (rank 0).  ``--impl reference`` times the reference's own
+CPU path on the host cores instead: ``steklov.local_ops.build_leaf_factors``
+from the installed reference (``baseline/_ref``) over the reference's worker
+pool, or — if that install is missing — the oracle port in ``oracle/``.
 """
 
 from __future__ import annotations
@@ -20,7 +27,6 @@ import os
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 
 import numpy as np
@@ -30,16 +36,21 @@ sys.path.insert(0, ROOT)
 
 PEAK_FP64_TFLOPS = 37.1   # measured DMMA issue peak, profiles/r01_fp64_probe_dmma_dfma.log
 PEAK_FP64_CUBLAS = 35.5   # measured cuBLAS DGEMM, profiles/r01_fp64_probe_cublas_cusolver.log
+TOL = 1e-10               # north star: relative Frobenius error vs the CPU reference
+CONFIGS3 = {"p": 20, "boxes": 16, "kappa": 80.0, "shards": 8}
+FIXTURES = os.path.join(ROOT, "tests", "golden", "bench_cases.npz")
+METRIC = "leaf DtN maps/sec"
+UNIT = "leaf DtN maps/s"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--p", type=int, default=16)
-    ap.add_argument("--boxes", type=int, default=16, help="leaf boxes per axis per GPU")
+    ap.add_argument("--boxes", type=int, default=16, help="leaf boxes per axis of the grid")
     ap.add_argument("--kappa", type=float, default=40.0)
     ap.add_argument("--field", default="bump", choices=["bump", "const"],
                     help="bump: variable-coefficient b(x) (configs 2-3); const: b = 1 (configs[1])")
@@ -47,10 +58,12 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seconds", type=float, default=60.0,
-                    help="reference arm: total CPU seconds over warmup + timed steps")
+                    help="reference arm: CPU seconds over the timed steps")
+    ap.add_argument("--configs3-steps", type=int, default=5,
+                    help="timed steps of the p = 20 configs[3] share (0: skip)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def dist_env():
@@ -76,6 +89,13 @@ def host_mem_available():
     return 1 << 50
 
 
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 def pinned_host(shape):
     """Page-locked float64 host array of exactly this size (cudaHostRegister on a numpy
     buffer; the torch pinned allocator rounds large requests up to a power of two)."""
@@ -90,26 +110,38 @@ def unpin_host(a):
     torch.cuda.check_error(torch.cuda.cudart().cudaHostUnregister(a.ctypes.data))
 
 
-def make_shard(p, boxes, kappa, rank, world, leaves_override=0, field="bump"):
-    """Coefficient packs (L, 4, n) for this rank's slab of the unit-cube-stacked leaf grid.
-    field "bump": -Lap u - kappa^2 b(x) u (configs 2-3); "const": b = 1 (configs[1])."""
+def shard_ids(n_leaves, world, rank):
+    from paper_2503_04033_b200.sharding import shard_range
+    start, stop = shard_range(n_leaves, world, rank)
+    return list(range(start, stop))
+
+
+def make_shard(p, boxes, kappa, rank=0, world=1, leaves_override=0, field="bump", leaf_ids=None):
+    """Coefficient packs (L, 4, n) of leaves of the boxes^3 grid on the unit cube.
+
+    ``leaf_ids`` (flat C-order indices of the grid) default to rank's leaf-index
+    share of the grid; ``leaves_override`` takes the first L leaves (cycling),
+    for profiling tools.  field "bump": -Lap u - kappa^2 b(x) u (configs 2-3);
+    "const": b = 1 (configs[1]).  The nodes are the reference's leaf grid
+    (local_ops.py build_leaf_operator: lo + h * ref_offsets)."""
     from paper_2503_04033_b200.local_ops import LeafTemplate
     h = 1.0 / boxes
     tpl = LeafTemplate((h, h, h), p, "drop", False)
-    L = leaves_override or boxes ** 3
+    if leaf_ids is None:
+        leaf_ids = ([k % boxes ** 3 for k in range(leaves_override)] if leaves_override
+                    else shard_ids(boxes ** 3, world, rank))
+    leaf_ids = np.asarray(leaf_ids, dtype=np.int64)
+    L = len(leaf_ids)
     n = tpl.n_interior
     inner = tpl.ref_offsets[1:-1]
+    q = len(inner)
     pack = np.empty((L, 4, n))
     pack[:, :3, :] = 1.0
-    idx = np.array(list(np.ndindex(boxes, boxes, boxes)))[:L] if L <= boxes ** 3 else \
-        np.array([np.unravel_index(k % boxes ** 3, (boxes,) * 3) for k in range(L)])
-    idx = idx.astype(float)
-    idx[:, 2] += rank * boxes
+    idx = np.stack(np.unravel_index(leaf_ids, (boxes,) * 3), axis=1).astype(float)
     for k0 in range(0, L, 256):
         lo = idx[k0:k0 + 256] * h
         B = len(lo)
         g = [lo[:, a, None] + h * inner[None, :] for a in range(3)]
-        q = len(inner)
         X = np.broadcast_to(g[0][:, :, None, None], (B, q, q, q))
         Y = np.broadcast_to(g[1][:, None, :, None], (B, q, q, q))
         Z = np.broadcast_to(g[2][:, None, None, :], (B, q, q, q))
@@ -117,6 +149,38 @@ def make_shard(p, boxes, kappa, rank, world, leaves_override=0, field="bump"):
         b = bump_b(pts) if field == "bump" else np.ones(len(pts))
         pack[k0:k0 + B, 3, :] = (-kappa * kappa * b).reshape(B, n)
     return tpl, pack
+
+
+def centre_leaf(boxes):
+    """Flat index of the leaf whose upper corner is the bump centre (0.5, 0.5, 0.5)."""
+    c = max(boxes // 2 - 1, 0)
+    return int(np.ravel_multi_index((c, c, c), (boxes,) * 3))
+
+
+def spread_sample(ids, k, must=()):
+    """k leaf ids of ``ids``: the ``must`` ids that are present, then evenly spaced ones."""
+    ids = list(ids)
+    present = set(ids)
+    out = [i for i in must if i in present]
+    for pos in np.linspace(0, len(ids) - 1, num=max(k, 1)).round().astype(int):
+        if len(out) >= k:
+            break
+        if ids[pos] not in out:
+            out.append(ids[pos])
+    return out[:k]
+
+
+def low_discrepancy_ids(n_leaves, first):
+    """Every leaf id once, ``first`` leading, then a golden-ratio sequence over the grid
+    (each prefix spreads over the whole grid)."""
+    phi = (np.sqrt(5.0) - 1.0) / 2.0
+    seq = np.floor(((np.arange(4 * n_leaves) * phi) % 1.0) * n_leaves).astype(int)
+    out, seen = [first], {first}
+    for i in seq.tolist() + list(range(n_leaves)):
+        if i not in seen:
+            seen.add(i)
+            out.append(i)
+    return out
 
 
 class ClockSampler:
@@ -166,99 +230,305 @@ class ClockSampler:
                 "power_w_max": max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())}
 
 
-def traffic_per_launch(leaves):
-    """DRAM bytes per launch from the committed ncu --set full capture (per-leaf, scaled)."""
-    path = os.path.join(ROOT, "profiles", "r01_ncu_summary.json")
-    try:
-        per_leaf = json.load(open(path))["traffic_bytes_per_leaf"]
-    except (OSError, KeyError, ValueError):
-        return None
-    return per_leaf * leaves
+def traffic_per_leaf(p):
+    """DRAM bytes per leaf from the committed ncu --set full capture at this order."""
+    for name in ("r02_ncu_summary.json", "r01_ncu_summary.json"):
+        path = os.path.join(ROOT, "profiles", name)
+        try:
+            s = json.load(open(path))
+        except (OSError, ValueError):
+            continue
+        if int(s.get("p", 16)) == p and "traffic_bytes_per_leaf" in s:
+            return s["traffic_bytes_per_leaf"], "profiles/" + name
+    return None, None
 
 
-def blas_threads():
-    """Threads the host BLAS (OpenBLAS under numpy/scipy) actually uses."""
-    try:
-        from threadpoolctl import threadpool_info
-        n = [i["num_threads"] for i in threadpool_info() if i.get("user_api") == "blas"]
-        if n:
-            return int(max(n))
-    except Exception:
-        pass
-    return os.cpu_count() or 1
+# ---------------------------------------------------------------------------
+# the reference's CPU path (reference arm and cpu_baseline)
+# ---------------------------------------------------------------------------
 
+class ReferenceCPU:
+    """Per-leaf DtN maps on the host cores, through the reference's own API when it is
+    installed (baseline/_ref: steklov.local_ops.build_leaf_factors on the leaf grid the
+    reference's build() uses, condensation.py:218-221, over a worker pool like its
+    ``BatchSchedule.workers``; one BLAS thread per worker), else the oracle port
+    (oracle/hps_oracle.py, the same algorithm restated)."""
 
-def cpu_reference(tpl, pack, seconds, steps=1):
-    """The reference's CPU algorithm (oracle port of local_ops.build_leaf_factors) on host cores."""
-    from oracle import hps_oracle as O
-    otpl = O.OracleTemplate(tpl.widths, tpl.p)
-    cores = blas_threads()
-    times, done = [], 0
-    t_start = time.perf_counter()
-    for _ in range(steps):
+    def __init__(self, p, boxes, kappa, field, workers=0):
+        self.p, self.boxes, self.kappa, self.field = p, boxes, kappa, field
+        self.workers = workers or int(os.environ.get("HPS_REF_WORKERS", "0")) or host_cores()
+        self.h = 1.0 / boxes
+        ref = os.path.join(ROOT, "baseline", "_ref")
+        self.kind = "port"
+        try:
+            if os.path.isdir(os.path.join(ref, "steklov")):
+                if ref not in sys.path:
+                    sys.path.insert(0, ref)
+                from steklov import local_ops as SL
+                self.SL = SL
+                self.kind = "reference"
+        except Exception:
+            self.kind = "port"
+        if self.kind == "reference":
+            SL = self.SL
+            if field == "bump":
+                zeroth = lambda x: -kappa * kappa * bump_b(x)  # noqa: E731
+            else:
+                zeroth = lambda x: np.full(x.shape[0], -kappa * kappa)  # noqa: E731
+            self.coeffs = SL.isotropic_field(3, zeroth=zeroth)
+            self.tpl = SL.LeafTemplate(np.array([self.h] * 3), p, SL.DROP_CORNERS, False)
+        else:
+            from oracle import hps_oracle as O
+            self.O = O
+            self.otpl = O.OracleTemplate((self.h,) * 3, p)
+
+    def leaf(self, leaf_id):
+        if self.kind == "reference":
+            lo = np.asarray(np.unravel_index(leaf_id, (self.boxes,) * 3), dtype=float) * self.h
+            nodes = []
+            for k in range(3):
+                x = lo[k] + self.h * self.tpl.ref_offsets
+                x[0], x[-1] = lo[k], lo[k] + self.h
+                nodes.append(x)
+            grid = self.tpl.leaf_grid(nodes)
+            return self.SL.build_leaf_factors(self.tpl, self.coeffs, grid).dtn
+        _, pack = make_shard(self.p, self.boxes, self.kappa, field=self.field, leaf_ids=[leaf_id])
+        return self.O.leaf_dtn(self.otpl, pack[0, :3].T, None, pack[0, 3])[0]
+
+    def run(self, ids):
+        """DtN maps of ``ids`` over the worker pool; returns seconds."""
+        from concurrent.futures import ThreadPoolExecutor
+        from threadpoolctl import threadpool_limits
         t0 = time.perf_counter()
-        k = 0
-        while True:
-            c = pack[(done + k) % pack.shape[0]]
-            O.leaf_dtn(otpl, c[:3].T, None, c[3])
-            k += 1
-            if time.perf_counter() - t0 >= seconds and k >= 2:
-                break
-        done += k
-        times.append((time.perf_counter() - t0) / k)
-    per_leaf = float(np.median(times))
-    return {"value": 1.0 / per_leaf, "unit": "leaf DtN maps/s", "cores": cores, "kind": "port",
-            "sample": f"{done} leaves of the workload (p={tpl.p}), numpy/scipy LAPACK getrf+getrs+gemm "
-                      f"with OpenBLAS on {cores} host threads, {time.perf_counter() - t_start:.1f} s"}
+        with threadpool_limits(limits=1, user_api="blas"):
+            with ThreadPoolExecutor(max_workers=self.workers) as pool:
+                list(pool.map(self.leaf, ids))
+        return time.perf_counter() - t0
+
+    def describe(self):
+        if self.kind == "reference":
+            return (f"reference steklov.local_ops.build_leaf_factors (baseline/_ref, scipy LAPACK "
+                    f"getrf/getrs + numpy GEMM) on {self.workers} worker threads x 1 BLAS thread")
+        return (f"oracle port of build_leaf_factors (numpy/scipy LAPACK getrf/getrs + GEMM) on "
+                f"{self.workers} worker threads x 1 BLAS thread")
 
 
-def main():
-    args = parse()
-    world, rank, local = dist_env()
+def cpu_baseline(p, boxes, kappa, field, seconds):
+    """Bounded CPU sample of the workload (rank 0, N = 1 leg of the GPU line)."""
+    ref = ReferenceCPU(p, boxes, kappa, field)
+    order = low_discrepancy_ids(boxes ** 3, centre_leaf(boxes))
+    done, spent = 0, 0.0
+    while spent < seconds or done == 0:
+        ids = order[done:done + ref.workers]
+        spent += ref.run(ids)
+        done += len(ids)
+    return {"value": done / spent, "unit": UNIT, "cores": ref.workers, "kind": ref.kind,
+            "sample": f"{done} leaves spread over the {boxes}^3 grid (bump-centre leaf first), "
+                      f"{ref.describe()}, {spent:.1f} s"}
+
+
+def config_of(args, world, leaves_per_gpu):
     p, boxes = args.p, args.boxes
-    leaves_per_gpu = args.leaves or boxes ** 3
-    grid = (f"{boxes}x{boxes}x{boxes} leaves per GPU" if leaves_per_gpu == boxes ** 3 else
-            f"{leaves_per_gpu} leaves per GPU (a 1/{boxes ** 3 // max(leaves_per_gpu, 1)} shard of a "
-            f"{boxes}x{boxes}x{boxes} leaf grid)")
+    n, m = (p - 2) ** 3, 6 * (p - 2) ** 2
     kind = ("3D variable-coefficient Helmholtz b(x) (Gaussian bump)" if args.field == "bump"
             else "3D constant-coefficient Helmholtz")
-    workload = (f"{kind}, p={p}, {grid}, "
-                f"kappa={args.kappa:g}")
-    n = (p - 2) ** 3
-    m = 6 * (p - 2) ** 2
-    from paper_2503_04033_b200.engine import dtn_flops, dtn_flops_executed
-    flops_ref = dtn_flops(n, m)                     # the reference's dense algorithm
-    flops_leaf = dtn_flops_executed(n, m, p - 2)    # what the kernel executes
-    metric = "leaf DtN maps/sec"
+    share = (f"{boxes}x{boxes}x{boxes} leaves" if not args.leaves else
+             f"{leaves_per_gpu} leaves per GPU of a {boxes}x{boxes}x{boxes} grid (profiling override)")
+    return {"workload": f"{kind}, p={p}, {share}, kappa={args.kappa:g}", "p": p,
+            "grid": [boxes] * 3, "leaves": (args.leaves * world) if args.leaves else boxes ** 3,
+            "leaves_per_gpu": leaves_per_gpu, "n_interior": n, "n_boundary": m,
+            "kappa": args.kappa, "field": args.field,
+            "l2": "inputs (coefficients %.0f MB) and outputs (%.1f GB) per GPU exceed the 126 MB L2"
+                  % (leaves_per_gpu * 4 * n * 8 / 1e6, leaves_per_gpu * m * m * 8 / 1e9),
+            "parallelism": f"leaf-index shards x{world}, no data-path collective"}
 
-    if args.impl == "reference":
-        if rank != 0:
-            return
-        tpl, pack = make_shard(p, boxes, args.kappa, 0, 1, leaves_override=min(64, boxes ** 3),
-                               field=args.field)
-        steps = max(1, args.steps)
-        per_step = max(min(2.0, args.ref_seconds), args.ref_seconds / (steps + args.warmup))
-        for _ in range(args.warmup):
-            cpu_reference(tpl, pack, seconds=min(per_step, 2.0))
-        base = cpu_reference(tpl, pack, seconds=per_step, steps=steps)
-        line = {"metric": metric, "value": base["value"], "unit": "leaf DtN maps/s", "impl": "reference",
-                "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
-                "ms_per_step": 1e3 * leaves_per_gpu / base["value"], "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": workload, "p": p, "leaves_per_gpu": leaves_per_gpu,
-                           "kappa": args.kappa, "step": "bounded CPU sample of the workload"},
-                "fp64_tflops": base["value"] * flops_ref / 1e12,
-                "cpu_baseline": base,
-                "e2e": {"value": base["value"], "unit": "leaf DtN maps/s", "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
+
+def reference_arm(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
         return
+    ref = ReferenceCPU(args.p, args.boxes, args.kappa, args.field)
+    L = args.boxes ** 3
+    order = low_discrepancy_ids(L, centre_leaf(args.boxes))
+    steps = max(1, args.steps)
+    pos = 0
+
+    def take(k):
+        nonlocal pos
+        ids = [order[(pos + i) % L] for i in range(k)]
+        pos += k
+        return ids
+
+    # warm-up steps: one leaf per worker each; the last one sizes the timed steps
+    rate = None
+    for _ in range(max(1, args.warmup)):
+        ids = take(ref.workers)
+        rate = len(ids) / ref.run(ids)
+    per_step = max(ref.workers, int(round(rate * args.ref_seconds / steps / ref.workers)) * ref.workers)
+    times, timed = [], 0
+    for _ in range(steps):
+        ids = take(per_step)
+        times.append(ref.run(ids))
+        timed += len(ids)
+    total = float(sum(times))
+    value = timed / total
+    n, m = (args.p - 2) ** 3, 6 * (args.p - 2) ** 2
+    from paper_2503_04033_b200.engine import dtn_flops
+    config = config_of(args, world, L // world)
+    config["sample_leaves"] = per_step
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+            "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * total / steps, "leaves_timed": timed,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config,
+            "step": f"one step = DtN maps of {per_step} leaves drawn over the whole grid "
+                    f"(bump-centre leaf first, golden-ratio sequence), the CPU analogue of the "
+                    f"GPU step's {L // world} leaves",
+            "fp64_tflops": value * dtn_flops(n, m) / 1e12,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": ref.workers, "kind": ref.kind,
+                             "sample": f"{timed} leaves in {steps} steps, {ref.describe()}, {total:.1f} s"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# the GPU arm
+# ---------------------------------------------------------------------------
+
+def parity_check(out, pack, leaf_ids, tpl, fixture_name, k):
+    """This run's maps vs the CPU oracle on ``k`` leaves spread over the share (the
+    bump-centre and fixture leaves first) and vs the reference's own outputs where the
+    share holds a fixture leaf (tests/golden/bench_cases.npz: T R for a probe R and
+    sampled rows of T)."""
+    from oracle import hps_oracle as O
+    p = tpl.p
+    boxes = int(round(1.0 / tpl.widths[0]))
+    fx = {}
+    if fixture_name and os.path.exists(FIXTURES):
+        G = np.load(FIXTURES)
+        for key in G.files:
+            parts = key.split("/")
+            if parts[0] == fixture_name and len(parts) == 3 and parts[2] == "dtn_R":
+                idx = tuple(int(x) for x in parts[1].split("_"))
+                fx[int(np.ravel_multi_index(idx, (boxes,) * 3))] = (
+                    G[f"{parts[0]}/{parts[1]}/dtn_R"], G[f"{parts[0]}/R"],
+                    G[f"{parts[0]}/{parts[1]}/dtn_rows_idx"], G[f"{parts[0]}/{parts[1]}/dtn_rows"])
+    pos = {leaf: i for i, leaf in enumerate(leaf_ids)}
+    chosen = spread_sample(leaf_ids, k, must=[centre_leaf(boxes)] + sorted(fx))
+    otpl = O.OracleTemplate(tpl.widths, p)
+    errs, ferrs, checked_fx = [], [], []
+    for leaf in chosen:
+        i = pos[leaf]
+        got = out[i].cpu().numpy()
+        ref, _, _ = O.leaf_dtn(otpl, pack[i, :3].T, None, pack[i, 3])
+        errs.append(float(np.linalg.norm(got - ref) / np.linalg.norm(ref)))
+        if leaf in fx:
+            tR, R, rows, trow = fx[leaf]
+            ferrs.append(max(float(np.linalg.norm(got @ R - tR) / np.linalg.norm(tR)),
+                             float(np.linalg.norm(got[rows] - trow) / np.linalg.norm(trow))))
+            checked_fx.append(leaf)
+    res = {"checked_leaves": chosen, "max_rel_fro_err_vs_oracle": max(errs), "tolerance": TOL}
+    if checked_fx:
+        res["reference_fixture_leaves"] = checked_fx
+        res["max_rel_err_vs_reference_fixture"] = max(ferrs)
+    res["ok"] = max(errs + ferrs) <= TOL
+    return res
+
+
+def timed_dtn(eng, coeffs, out, stats, steps, warmup, local, barrier):
+    """W untimed launches, then K launches bracketed by barrier + synchronize; CUDA
+    events on the launching stream.  Returns (per-step ms list, wall s, clocks)."""
+    import torch
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        eng.dtn(coeffs, out, stats, stream=stream)
+    torch.cuda.synchronize()
+    barrier()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t_wall = time.perf_counter()
+        for k in range(steps):
+            starts[k].record(stream)
+            eng.dtn(coeffs, out, stats, stream=stream)
+            ends[k].record(stream)
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall
+    barrier()
+    return [s.elapsed_time(e) for s, e in zip(starts, ends)], t_wall, clk.summary()
+
+
+def max_over_ranks(x, distributed, local):
+    if not distributed:
+        return x
+    import torch
+    t = torch.tensor([float(x)], device=f"cuda:{local}", dtype=torch.float64)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
+def roofline(p, leaves, kernel_ms):
+    from paper_2503_04033_b200.engine import dtn_flops_executed
+    n, m = (p - 2) ** 3, 6 * (p - 2) ** 2
+    achieved = leaves * dtn_flops_executed(n, m, p - 2) / (kernel_ms / 1e3) / 1e12
+    per_leaf, src = traffic_per_leaf(p)
+    return {"bound": "tensor", "achieved": achieved, "peak": PEAK_FP64_TFLOPS, "unit": "TFLOP/s",
+            "frac": achieved / PEAK_FP64_TFLOPS,
+            "traffic": per_leaf * leaves if per_leaf is not None else None,
+            "kernel": "hps_leaf_kernel (assembly + LU + Schur, DMMA m8n8k4 f64)",
+            "peak_source": "measured FP64 DMMA peak 37.1 TFLOP/s (cuBLAS DGEMM 35.5); "
+                           "MEASURED_PEAKS.json has no FP64 entry",
+            "traffic_source": (f"{src} (ncu --set full, DRAM bytes per leaf x leaves)" if src else
+                               "no ncu capture at this order")}
+
+
+def configs3_share(args, world, rank, local, distributed, barrier):
+    """configs[3]: p = 20, 16^3 leaves, kappa = 80, 1/8 leaf-index share per GPU."""
+    import torch
+    from paper_2503_04033_b200.engine import LeafEngine
+    c = CONFIGS3
+    p, boxes, shards = c["p"], c["boxes"], c["shards"]
+    share = rank % shards
+    ids = shard_ids(boxes ** 3, shards, share)
+    tpl, pack = make_shard(p, boxes, c["kappa"], leaf_ids=ids)
+    L = len(ids)
+    m = tpl.n_boundary
+    eng = LeafEngine(tpl, False, True, device=local)
+    coeffs = torch.from_numpy(pack).to(f"cuda:{local}")
+    out = torch.empty((L, m, m), dtype=torch.float64, device=f"cuda:{local}")
+    stats = torch.empty((L, 2), dtype=torch.float64, device=f"cuda:{local}")
+    steps, warmup = args.configs3_steps, max(3, min(args.warmup, 3))
+    step_ms, t_wall, clocks = timed_dtn(eng, coeffs, out, stats, steps, warmup, local, barrier)
+    total_ms = max_over_ranks(float(sum(step_ms)), distributed, local)
+    parity = parity_check(out, pack, ids, tpl, "c3_p20_bump_k80", 4) if rank == 0 else None
+    del out, coeffs, stats, eng
+    torch.cuda.empty_cache()
+    value = world * L * steps / (total_ms / 1e3)
+    return {"workload": f"3D variable-coefficient Helmholtz b(x), p={p}, {boxes}x{boxes}x{boxes} leaves, "
+                        f"kappa={c['kappa']:g}, sharded across 8 GPUs by leaf index; rank r times "
+                        f"share r ({L} leaves) — at N={world}, {world} of the 8 shares",
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+            "warmup": warmup, "ms_per_step": total_ms / steps, "leaves_per_gpu": L,
+            "leaf_ids_rank0": [ids[0], ids[-1]],
+            "l2": "outputs (%.1f GB) per GPU exceed the 126 MB L2" % (L * m * m * 8 / 1e9),
+            "roofline": roofline(p, L, float(np.mean(step_ms))), "gpu_launches": steps,
+            "parity": parity, "clocks": clocks, "wall_s_timed": t_wall}
+
+
+def main(argv=None):
+    args = parse(argv)
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+    world, rank, local = dist_env()
+    p, boxes = args.p, args.boxes
+    n, m = (p - 2) ** 3, 6 * (p - 2) ** 2
 
     # CPU reference first, before pinned buffers and GPU work claim host resources
     cpu = None
-    if rank == 0 and not args.no_cpu:
-        tpl0, pack0 = make_shard(p, boxes, args.kappa, 0, 1, min(64, boxes ** 3), field=args.field)
-        cpu = cpu_reference(tpl0, pack0, seconds=args.cpu_seconds)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(p, boxes, args.kappa, args.field, args.cpu_seconds)
 
     import torch
     torch.cuda.set_device(local)
@@ -277,57 +547,36 @@ def main():
             sys.stdout.flush()
             os.dup2(saved, 1)
             os.close(saved)
-    from paper_2503_04033_b200.engine import LeafEngine
-
-    tpl, pack = make_shard(p, boxes, args.kappa, rank, world, args.leaves, field=args.field)
-    L = pack.shape[0]
-    eng = LeafEngine(tpl, False, True, device=local)
-    coeffs = torch.from_numpy(pack).to(f"cuda:{local}")
-    out = torch.empty((L, m, m), dtype=torch.float64, device=f"cuda:{local}")
-    stats = torch.empty((L, 2), dtype=torch.float64, device=f"cuda:{local}")
-    stream = torch.cuda.current_stream()
 
     def barrier():
         if distributed:
             torch.distributed.barrier()
 
-    for _ in range(args.warmup):
-        eng.dtn(coeffs, out, stats)
-    torch.cuda.synchronize()
-    barrier()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        t_wall = time.perf_counter()
-        for k in range(args.steps):
-            starts[k].record(stream)
-            eng.dtn(coeffs, out, stats)
-            ends[k].record(stream)
-        torch.cuda.synchronize()
-        t_wall = time.perf_counter() - t_wall
-    barrier()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total_ms = float(sum(step_ms))
-    if distributed:
-        t = torch.tensor([total_ms], device=f"cuda:{local}")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
+    from paper_2503_04033_b200.engine import LeafEngine, dtn_flops, dtn_flops_executed
+    if args.leaves:
+        leaf_ids = [k % boxes ** 3 for k in range(rank * args.leaves, (rank + 1) * args.leaves)]
+    else:
+        leaf_ids = shard_ids(boxes ** 3, world, rank)
+    tpl, pack = make_shard(p, boxes, args.kappa, field=args.field, leaf_ids=leaf_ids)
+    L = pack.shape[0]
+    eng = LeafEngine(tpl, False, True, device=local)
+    coeffs = torch.from_numpy(pack).to(f"cuda:{local}")
+    out = torch.empty((L, m, m), dtype=torch.float64, device=f"cuda:{local}")
+    stats = torch.empty((L, 2), dtype=torch.float64, device=f"cuda:{local}")
+    step_ms, t_wall, clocks = timed_dtn(eng, coeffs, out, stats, args.steps, args.warmup, local, barrier)
+    total_ms = max_over_ranks(float(sum(step_ms)), distributed, local)
     value = world * L * args.steps / (total_ms / 1e3)
-    kernel_ms = float(np.mean(step_ms))
-    achieved = L * flops_leaf / (kernel_ms / 1e3) / 1e12
 
-    # parity spot check of this run's output against the CPU oracle (2 leaves)
-    parity = None
-    if rank == 0:
-        from oracle import hps_oracle as O
-        otpl = O.OracleTemplate(tpl.widths, p)
-        errs = []
-        for k in (0, L - 1):
-            ref, _, _ = O.leaf_dtn(otpl, pack[k, :3].T, None, pack[k, 3])
-            got = out[k].cpu().numpy()
-            errs.append(float(np.linalg.norm(got - ref) / np.linalg.norm(ref)))
-        parity = {"checked_leaves": 2, "max_rel_fro_err_vs_oracle": max(errs), "tolerance": 1e-10}
+    # parity of this run's output: 8 leaves per rank spread over the share (bump centre
+    # first) vs the CPU oracle, and the reference's own outputs for fixture leaves
+    fixture = {12: "c1_p12_const_k10", 16: "c2_p16_bump_k40"}.get(p) if boxes in (8, 16) else None
+    if fixture == "c1_p12_const_k10" and (boxes != 8 or args.field != "const" or args.kappa != 10.0):
+        fixture = None
+    if fixture == "c2_p16_bump_k40" and (boxes != 16 or args.field != "bump" or args.kappa != 40.0):
+        fixture = None
+    parity = parity_check(out, pack, leaf_ids, tpl, fixture, 8 if world == 1 else 4)
+    bad = max_over_ranks(0.0 if parity["ok"] else 1.0, distributed, local)
+    parity["all_ranks_ok"] = bad == 0.0
 
     e2e = None
     if not args.no_e2e:
@@ -355,46 +604,41 @@ def main():
             t0 = time.perf_counter()
             eng.dtn_host(h_coef, out=h_out, chunk_leaves=chunk)
             ts.append(time.perf_counter() - t0)
-        e2e_t = float(np.mean(ts))
-        if distributed:
-            t = torch.tensor([e2e_t], device=f"cuda:{local}", dtype=torch.float64)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e2e_t = float(t.item())
+        e2e_t = max_over_ranks(float(np.mean(ts)), distributed, local)
         unpin_host(h_coef)
         unpin_host(h_out)
         del h_coef, h_out
-        e2e = {"value": world * Le / e2e_t, "unit": "leaf DtN maps/s", "leaves_per_gpu": Le,
+        e2e = {"value": world * Le / e2e_t, "unit": UNIT, "leaves_per_gpu": Le,
                "h2d_bytes_per_step": int(Le * pack[0].nbytes), "d2h_bytes_per_step": int(Le * m * m * 8),
                "path": "LeafEngine.dtn_host -> hps_leaf_dtn_host (C ABI): H2D of all coefficients, "
                        "one persistent launch, D2H of each finished "
                        f"{chunk}-leaf chunk overlapped via device completion counters"}
+    else:
+        del out
+    del coeffs, stats, eng
+    torch.cuda.empty_cache()
 
+    configs3 = None
+    if args.configs3_steps > 0 and not args.leaves:
+        configs3 = configs3_share(args, world, rank, local, distributed, barrier)
 
     if rank == 0:
+        flops_ref = dtn_flops(n, m)
+        flops_leaf = dtn_flops_executed(n, m, p - 2)
         line = {
-            "metric": metric, "value": value, "unit": "leaf DtN maps/s", "n_gpus": world,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic",
-            "config": {"workload": workload, "p": p, "leaves_per_gpu": L, "n_interior": n,
-                       "n_boundary": m, "kappa": args.kappa,
-                       "l2": "inputs (coefficients %.0f MB) and outputs (%.1f GB) exceed the 126 MB L2"
-                             % (pack.nbytes / 1e6, L * m * m * 8 / 1e9),
-                       "parallelism": f"leaf-sharded x{world}, no data-path collective"},
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_of(args, world, L),
             "fp64_tflops": value * flops_leaf / 1e12,
             "fp64_tflops_reference_equivalent": value * flops_ref / 1e12,
             "flops_per_leaf": flops_leaf,
             "flops_per_leaf_reference_algorithm": flops_ref,
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": PEAK_FP64_TFLOPS,
-                         "unit": "TFLOP/s", "frac": achieved / PEAK_FP64_TFLOPS,
-                         "traffic": traffic_per_launch(L),
-                         "kernel": "hps_leaf_kernel (assembly + LU + Schur, DMMA m8n8k4 f64)",
-                         "peak_source": "measured FP64 DMMA peak 37.1 TFLOP/s (cuBLAS DGEMM 35.5); "
-                                        "MEASURED_PEAKS.json has no FP64 entry",
-                         "traffic_source": "profiles/r01_ncu_summary.json (ncu --set full, per leaf x leaves)"},
+            "roofline": roofline(p, L, float(np.mean(step_ms))),
             "gpu_launches": args.steps,
             "e2e": e2e, "cpu_baseline": cpu, "parity": parity,
-            "clocks": clk.summary(), "wall_s_timed": t_wall,
+            "clocks": clocks, "wall_s_timed": t_wall,
+            "configs3": configs3,
         }
         print(json.dumps(line), flush=True)
     if distributed:

@@ -3,7 +3,7 @@
 Run in the build container only (needs /root/reference, which does not exist
 on the GPU box):
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py [leaf] [pipeline] [bench]   (default: all)
 
 For every case it imports ``steklov`` from /root/reference/pkg/src, builds the
 leaf template and operator with the reference's own code, and stores inputs
@@ -11,8 +11,10 @@ leaf template and operator with the reference's own code, and stores inputs
 evaluates) and outputs (A_ii, A_ib, a_bi, a_bb, DtN, S, reduced load, interior
 solve) in ``leaf_cases.npz``.  A second file, ``pipeline_cases.npz``, stores
 end-to-end ``solve_bvp`` results and assembled interface matrices for small
-meshes.  The fixtures are what pin the oracle (tests/test_oracle_golden.py)
-and the CUDA path (tests/test_gpu_parity.py).
+meshes.  ``bench_cases.npz`` holds the reference's leaf outputs at the
+benchmark orders (configs[1-3]: p = 12, 16, 20; probes and sampled rows of the
+maps, full vectors).  The fixtures are what pin the oracle
+(tests/test_oracle_golden.py) and the CUDA path (tests/test_gpu_parity.py).
 """
 
 from __future__ import annotations
@@ -175,10 +177,87 @@ def pipeline_cases():
     return out
 
 
+def bench_field(kind, kappa):
+    """The bench workloads' coefficient fields (bench.py make_shard):
+    -Lap u - kappa^2 b(x) u with the Gaussian bump, or b = 1."""
+    if kind == "const":
+        return isotropic_field(3, zeroth=lambda x: np.full(x.shape[0], -kappa * kappa))
+    return isotropic_field(3, zeroth=lambda x: bump(x, kappa))
+
+
+BENCH_CASES = [
+    # name, p, leaf boxes per axis, kappa, field, leaf indices (i, j, k) in the unit-cube grid
+    # configs[1]: constant coefficient, every leaf the same operator up to translation
+    ("c1_p12_const_k10", 12, 8, 10.0, "const", [(3, 4, 5)]),
+    # configs[2]: (7,7,7) has the bump centre (0.5, 0.5, 0.5) as its corner; (3,12,5) off-centre
+    ("c2_p16_bump_k40", 16, 16, 40.0, "bump", [(7, 7, 7), (3, 12, 5)]),
+    # configs[3]: (1,7,7) is in rank 0's 1/8 share (leaves 0-511) nearest the centre
+    ("c3_p20_bump_k80", 20, 16, 80.0, "bump", [(7, 7, 7), (1, 7, 7)]),
+]
+N_PROBE = 8     # random probe columns for the DtN map and the solution operator
+N_ROWS = 8      # full DtN rows stored per leaf
+
+
+def bench_cases():
+    """Reference outputs at the benchmark orders (p = 12, 16, 20).  Full m x m maps
+    would be 3-30 MB each, so the fixtures keep what pins them: T R and S R for a
+    seeded Gaussian probe R (m x 8), N_ROWS full rows of T, the Frobenius norms,
+    and the full vectors of the load reduction and the interior solve
+    (reference local_ops.py:439-446, condensation.py:314-323 and 372-383)."""
+    out = {}
+    rng = np.random.default_rng(20251019)
+    for name, p, boxes, kappa, kind, leaves in BENCH_CASES:
+        h = 1.0 / boxes
+        coeffs = bench_field(kind, kappa)
+        tpl = LeafTemplate(np.array([h, h, h]), p, "drop", False)
+        m, n = tpl.n_boundary, tpl.n_interior
+        R = rng.standard_normal((m, N_PROBE))
+        out[name + "/meta"] = np.array([p, boxes, kappa])
+        out[name + "/R"] = R
+        for idx in leaves:
+            lo = np.asarray(idx, dtype=float) * h
+            nodes = []
+            for k in range(3):
+                x = lo[k] + h * tpl.ref_offsets
+                x[0], x[-1] = lo[k], lo[k] + h
+                nodes.append(x)
+            grid = tpl.leaf_grid(nodes)
+            lf = build_leaf_factors(tpl, coeffs, grid, leaf_index=idx)
+            a_ii, a_ib = tpl.interior_blocks(coeffs, grid)
+            x_int = grid[tpl.interior_idx]
+            f = np.sin(3 * x_int[:, 0]) + x_int[:, -1] ** 2
+            v = lf.solve_interior(f)
+            ub = rng.standard_normal(m)
+            u_int = v - lf.solve_interior(a_ib @ ub)
+            rows = np.sort(rng.choice(m, N_ROWS, replace=False))
+            pre = f"{name}/{idx[0]}_{idx[1]}_{idx[2]}/"
+            out[pre + "coeffs"] = pack_coeffs(coeffs, x_int, 3)
+            out[pre + "dtn_R"] = lf.dtn @ R
+            out[pre + "dtn_rows_idx"] = rows
+            out[pre + "dtn_rows"] = lf.dtn[rows]
+            out[pre + "dtn_fro"] = np.array([np.linalg.norm(lf.dtn)])
+            out[pre + "s_R"] = lf.s @ R
+            out[pre + "s_fro"] = np.array([np.linalg.norm(lf.s)])
+            out[pre + "f"] = f
+            out[pre + "v"] = v
+            out[pre + "flux"] = tpl.a_bi @ v
+            out[pre + "ub"] = ub
+            out[pre + "u_int"] = u_int
+            diag = np.abs(np.diag(lf.a_ii_factor[0]))
+            out[pre + "pivots"] = np.array([diag.min(), diag.max(),
+                                            int((lf.a_ii_factor[1] != np.arange(n)).sum())])
+    return out
+
+
 def main():
-    np.savez_compressed(os.path.join(HERE, "leaf_cases.npz"), **leaf_cases())
-    np.savez_compressed(os.path.join(HERE, "pipeline_cases.npz"), **pipeline_cases())
-    for fn in ("leaf_cases.npz", "pipeline_cases.npz"):
+    only = sys.argv[1:]
+    if not only or "leaf" in only:
+        np.savez_compressed(os.path.join(HERE, "leaf_cases.npz"), **leaf_cases())
+    if not only or "pipeline" in only:
+        np.savez_compressed(os.path.join(HERE, "pipeline_cases.npz"), **pipeline_cases())
+    if not only or "bench" in only:
+        np.savez_compressed(os.path.join(HERE, "bench_cases.npz"), **bench_cases())
+    for fn in ("leaf_cases.npz", "pipeline_cases.npz", "bench_cases.npz"):
         print(fn, os.path.getsize(os.path.join(HERE, fn)), "bytes")
 
 

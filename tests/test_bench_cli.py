@@ -9,7 +9,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def _run(cmd, env_extra=None):
-    env = dict(os.environ, OMP_NUM_THREADS="2", OPENBLAS_NUM_THREADS="2", MASTER_ADDR="127.0.0.1")
+    env = dict(os.environ, OMP_NUM_THREADS="2", OPENBLAS_NUM_THREADS="2", HPS_REF_WORKERS="2",
+               MASTER_ADDR="127.0.0.1")
     env.update(env_extra or {})
     return subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
 
@@ -27,8 +28,14 @@ def test_reference_arm_single_process():
     assert line["metric"] == "leaf DtN maps/sec" and line["value"] > 0
     assert line["e2e"]["value"] == line["value"]
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
-    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] == 2  # OPENBLAS_NUM_THREADS
+    # the installed reference (baseline/_ref) when present, else the oracle port
+    assert line["cpu_baseline"]["kind"] in ("reference", "port")
+    assert line["cpu_baseline"]["cores"] == 2  # HPS_REF_WORKERS
     assert line["config"]["p"] == 8 and line["config"]["leaves_per_gpu"] == 8
+    # what ran is what the line says: steps x ms_per_step is the measured time
+    assert line["leaves_timed"] == line["steps"] * line["config"]["sample_leaves"]
+    assert abs(line["value"] * line["steps"] * line["ms_per_step"] / 1e3 - line["leaves_timed"]) \
+        <= 1e-6 * line["leaves_timed"]
 
 
 def test_reference_arm_under_torchrun_prints_one_line():
@@ -39,3 +46,4 @@ def test_reference_arm_under_torchrun_prints_one_line():
     assert res.returncode == 0, res.stderr[-2000:]
     (line,) = _lines(res.stdout)
     assert line["impl"] == "reference" and line["n_gpus"] == 2
+    assert line["config"]["leaves_per_gpu"] == 4   # the 2x2x2 grid split by leaf index

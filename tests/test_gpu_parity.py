@@ -202,3 +202,54 @@ def test_column_zero_skipping_is_exact(kappa, monkeypatch):
     for k in (0, 7):
         ref, _, _ = O.leaf_dtn(otpl, pack[k, :3].T, None, pack[k, 3])
         assert rel(fast[k], ref) <= TOL
+
+
+# ---------------------------------------------------------------------------
+# benchmark orders (configs[1-3]: p = 12, 16, 20; kappa 10 / 40 / 80), against the
+# reference's own outputs (tests/golden/make_golden.py bench_cases): T R and S R for a
+# probe R, sampled full rows of T, the Frobenius norms, v / flux / u_int in full.
+# Reference: local_ops.py:439-446, condensation.py:314-323 and 372-383.
+# ---------------------------------------------------------------------------
+
+BG = np.load(os.path.join(HERE, "golden", "bench_cases.npz"))
+BENCH_NAMES = sorted({k.split("/")[0] for k in BG.files})
+
+
+@pytest.mark.parametrize("name", BENCH_NAMES)
+def test_bench_order_outputs_match_reference(name):
+    from paper_2503_04033_b200.engine import LeafEngine
+    from paper_2503_04033_b200.local_ops import LeafTemplate
+    p, boxes, _ = BG[name + "/meta"]
+    h = 1.0 / boxes
+    leaves = sorted({k.split("/")[1] for k in BG.files if k.startswith(name + "/") and k.count("/") == 2})
+    pre = [f"{name}/{leaf}/" for leaf in leaves]
+    pack = np.stack([BG[k + "coeffs"] for k in pre])
+    R = BG[name + "/R"]
+    eng = LeafEngine(LeafTemplate((h, h, h), int(p), "drop", False), False, True, device=0)
+    dtn, stats = eng.dtn_host(pack)
+    s, _ = eng.solution_operator_host(pack)
+    v, flux, _ = eng.reduce_load_host(pack, np.stack([BG[k + "f"] for k in pre]))
+    u, _ = eng.interior_solve_host(pack, np.stack([BG[k + "ub"] for k in pre]),
+                                   np.stack([BG[k + "v"] for k in pre]))
+    for i, k in enumerate(pre):
+        assert rel(dtn[i] @ R, BG[k + "dtn_R"]) <= TOL, (k, "dtn")
+        assert rel(dtn[i][BG[k + "dtn_rows_idx"]], BG[k + "dtn_rows"]) <= TOL, (k, "dtn rows")
+        assert abs(np.linalg.norm(dtn[i]) / BG[k + "dtn_fro"][0] - 1.0) <= TOL
+        assert rel(s[i] @ R, BG[k + "s_R"]) <= TOL, (k, "S")
+        assert abs(np.linalg.norm(s[i]) / BG[k + "s_fro"][0] - 1.0) <= TOL
+        assert rel(v[i], BG[k + "v"]) <= TOL, (k, "v")
+        assert rel(flux[i], BG[k + "flux"]) <= TOL, (k, "flux")
+        assert rel(u[i], BG[k + "u_int"]) <= TOL, (k, "u_int")
+        # pivots of the engine's (reordered) factorization: same magnitudes as LAPACK's
+        pmin, pmax, _ = BG[k + "pivots"]
+        assert 0.0 < stats[i, 0] <= stats[i, 1] and 0.1 < stats[i, 1] / pmax < 10.0
+
+
+def test_bench_parity_spot_check_spreads_over_the_grid():
+    """bench.py's parity leaves: 8 per rank, the bump-centre leaf and the fixture
+    leaves first, the rest spread over the share."""
+    import bench
+    ids = list(range(4096))
+    chosen = bench.spread_sample(ids, 8, must=[bench.centre_leaf(16), 375])
+    assert chosen[:2] == [1911, 375] and len(set(chosen)) == 8
+    assert max(chosen) - min(chosen) > 3000

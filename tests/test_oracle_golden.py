@@ -82,3 +82,54 @@ def test_singular_block_flagged():
     n = tpl.n
     _, _, (dmin, dmax, singular) = O.leaf_dtn(tpl, np.zeros((n, 2)), None, np.zeros(n))
     assert singular
+
+
+# ---------------------------------------------------------------------------
+# benchmark orders (configs[1-3]): p = 12, 16, 20 — fixtures from the reference
+# itself (tests/golden/make_golden.py bench_cases)
+# ---------------------------------------------------------------------------
+
+B = np.load(os.path.join(HERE, "golden", "bench_cases.npz"))
+BENCH_LEAVES = sorted({"/".join(k.split("/")[:2]) for k in B.files if k.count("/") == 2})
+
+
+def bench_leaf(key):
+    """(template widths, p, coefficient pack (4, n), probe R) of a bench fixture leaf."""
+    name = key.split("/")[0]
+    p, boxes, _ = B[name + "/meta"]
+    h = 1.0 / boxes
+    return (h, h, h), int(p), B[key + "/coeffs"], B[name + "/R"]
+
+
+@pytest.mark.parametrize("key", BENCH_LEAVES)
+def test_oracle_matches_reference_at_bench_orders(key):
+    widths, p, c, R = bench_leaf(key)
+    tpl = O.OracleTemplate(widths, p)
+    dtn, s, (dmin, dmax, singular) = O.leaf_dtn(tpl, c[:3].T, None, c[3])
+    assert not singular
+    assert rel(dtn @ R, B[key + "/dtn_R"]) <= 1e-13
+    assert rel(dtn[B[key + "/dtn_rows_idx"]], B[key + "/dtn_rows"]) <= 1e-13
+    assert abs(np.linalg.norm(dtn) / B[key + "/dtn_fro"][0] - 1.0) <= 1e-13
+    assert rel(s @ R, B[key + "/s_R"]) <= 1e-13
+    # same LAPACK partial pivoting: the same pivots and interchange count
+    pmin, pmax, swaps = B[key + "/pivots"]
+    assert dmin == pytest.approx(pmin, rel=1e-12) and dmax == pytest.approx(pmax, rel=1e-12)
+    v, flux, _ = O.leaf_reduce_load(tpl, B[key + "/f"], c[:3].T, None, c[3])
+    assert rel(v, B[key + "/v"]) <= 1e-13
+    assert rel(flux, B[key + "/flux"]) <= 1e-13
+    u, _ = O.leaf_interior_solve(tpl, B[key + "/v"], B[key + "/ub"], c[:3].T, None, c[3])
+    assert rel(u, B[key + "/u_int"]) <= 1e-13
+
+
+def test_bench_fixtures_match_bench_workload():
+    """bench.py's synthetic coefficient packs are the reference's fields at the same
+    leaves: the fixtures check exactly the bench workload."""
+    import bench
+    for key in BENCH_LEAVES:
+        name, leaf = key.split("/")
+        p, boxes, kappa = B[name + "/meta"]
+        idx = tuple(int(x) for x in leaf.split("_"))
+        field = "const" if "const" in name else "bump"
+        _, pack = bench.make_shard(int(p), int(boxes), float(kappa), 0, 1, field=field,
+                                   leaf_ids=[int(np.ravel_multi_index(idx, (int(boxes),) * 3))])
+        assert np.allclose(pack[0], B[key + "/coeffs"], rtol=1e-15, atol=0.0)

@@ -161,13 +161,12 @@ def spread_sample(ids, k, must=()):
     """k leaf ids of ``ids``: the ``must`` ids that are present, then evenly spaced ones."""
     ids = list(ids)
     present = set(ids)
-    out = [i for i in must if i in present]
-    for pos in np.linspace(0, len(ids) - 1, num=max(k, 1)).round().astype(int):
-        if len(out) >= k:
-            break
-        if ids[pos] not in out:
-            out.append(ids[pos])
-    return out[:k]
+    out = [i for i in dict.fromkeys(must) if i in present][:k]
+    rest = [i for i in ids if i not in set(out)]
+    need = min(k - len(out), len(rest))
+    if need > 0:
+        out += [rest[j] for j in np.linspace(0, len(rest) - 1, num=need).round().astype(int)]
+    return out
 
 
 def low_discrepancy_ids(n_leaves, first):

@@ -2,7 +2,8 @@
  *
  * Plain pointers and sizes only.  All `double*` arguments of the device entry
  * points are CUDA device pointers; `stream` is a cudaStream_t (NULL = legacy
- * default stream).  Every function returns 0 on success and a negative value
+ * default stream).  Launches of one plan are ordered after each other whatever
+ * stream they are issued on (the plan's slot workspace is shared).  Every function returns 0 on success and a negative value
  * on failure; hps_last_error() then describes the failure (thread-local).
  *
  * Reference interfaces replaced (steklov, /root/reference/pkg/src/steklov):
@@ -18,10 +19,14 @@
  *                                 two-level schedule (BatchSchedule) condensation.py:49-95,225-264
  *   hps_leaf_solution_operator <- LeafFactors.s = -A_ii^{-1} a_ib    local_ops.py:443
  *                                 (cache_leaf_factors path)         condensation.py:258-260,376-377
+ *   hps_leaf_factors           <- build_leaf_factors: s and dtn      local_ops.py:439-446
+ *                                 of the same factorization, one launch
  *   hps_leaf_reduce_load       <- reduce_load.leaf_task             condensation.py:314-323
  *   hps_leaf_interior_solve    <- solve.leaf_task (recompute path)  condensation.py:372-383
  *   hps_leaf_apply             <- explicit_rows @ full in           problems.py:473-505
  *                                 crank_nicolson_run
+ *   hps_plan_release           <- (no counterpart: the reference's per-leaf workspace is
+ *   hps_plan_workspace             transient; BatchSchedule.memory_budget  condensation.py:49-84)
  *
  * Data layout (row-major, C order, float64):
  *   coeffs : [n_leaves][ncoef][n]   ncoef = d (diagonal second-order a_kk)
@@ -51,7 +56,7 @@
 extern "C" {
 #endif
 
-#define HPS_ABI_VERSION 1
+#define HPS_ABI_VERSION 2
 
 typedef struct hps_plan_s* hps_plan_t;
 
@@ -77,6 +82,14 @@ int hps_plan_create_legendre(hps_plan_t* plan, int device, int dim, int p, int h
 int hps_plan_destroy(hps_plan_t plan);
 int hps_plan_info(hps_plan_t plan, int* n_interior, int* n_boundary, int* ncoef, int* slots,
                   size_t* dtn_slot_bytes, size_t* solve_slot_bytes);
+/* Device memory the plan holds now (slot workspace, pivot tables, inverse cache,
+ * streaming buffers) and the slots it is sized for.  The workspace grows on the
+ * first launch of a mode (bounded by workspace_budget_bytes and ~85% of free
+ * device memory) and is kept until hps_plan_release / hps_plan_destroy. */
+int hps_plan_workspace(hps_plan_t plan, size_t* bytes, int* slots);
+/* Free the workspace and streaming buffers after the plan's last launch has
+ * finished; templates and op programs stay and the next launch re-allocates. */
+int hps_plan_release(hps_plan_t plan);
 
 /* Diagnostics: when `counters` (device, [slots][16] uint64, zeroed by the
  * caller) is set, every launch accumulates clock64 cycles per op kind
@@ -90,6 +103,9 @@ int hps_leaf_dtn_host(hps_plan_t plan, int n_leaves, const double* coeffs_host, 
                       double* stats_host, int chunk_leaves);
 int hps_leaf_solution_operator(hps_plan_t plan, int n_leaves, const double* coeffs, double* s,
                                double* stats, void* stream);
+/* dtn [n_leaves][m][m] and s [n_leaves][n][m] from one factorization per leaf. */
+int hps_leaf_factors(hps_plan_t plan, int n_leaves, const double* coeffs, double* dtn, double* s,
+                     double* stats, void* stream);
 int hps_leaf_reduce_load(hps_plan_t plan, int n_leaves, const double* coeffs, const double* f,
                          double* v, double* flux, double* stats, void* stream);
 /* w = rows(coeffs) [u_int; u_b]: the leaf's collocation operator applied to

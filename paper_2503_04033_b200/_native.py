@@ -20,9 +20,9 @@ EXPORTS = (
     "hps_plan_destroy", "hps_plan_info", "hps_leaf_dtn", "hps_leaf_dtn_host",
     "hps_leaf_reduce_load", "hps_leaf_interior_solve", "hps_leaf_solution_operator",
     "hps_plan_set_profile", "hps_plan_create_legendre", "hps_leaf_apply",
-    "hps_interface_scatter",
+    "hps_interface_scatter", "hps_leaf_factors", "hps_plan_release", "hps_plan_workspace",
 )
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 _lib = None
 
@@ -47,6 +47,9 @@ def _sig(lib):
     lib.hps_leaf_reduce_load.argtypes = [_P, _I, _P, _P, _P, _P, _P, _P]
     lib.hps_leaf_interior_solve.argtypes = [_P, _I, _P, _P, _P, _P, _P, _P]
     lib.hps_leaf_solution_operator.argtypes = [_P, _I, _P, _P, _P, _P]
+    lib.hps_leaf_factors.argtypes = [_P, _I, _P, _P, _P, _P, _P]
+    lib.hps_plan_release.argtypes = [_P]
+    lib.hps_plan_workspace.argtypes = [_P, ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(_I)]
     lib.hps_plan_set_profile.argtypes = [_P, _P]
     lib.hps_interface_scatter.argtypes = [_I, _P, ctypes.c_longlong, ctypes.c_longlong,
                                           ctypes.c_longlong, _I, _P, _P, _P, _P]

@@ -80,6 +80,11 @@ class InterfacePattern:
             self.indptr.append(indptr.astype(idx_t))
             base.append(dict(zip(iface, bases)))
         self.nnz = (int(self.indptr[0][-1]), int(self.indptr[1][-1]))
+        # the index arrays are shared by every T / C built from this (cached) pattern:
+        # read-only, so an in-place edit of a returned matrix (eliminate_zeros, prune,
+        # sort_indices) raises instead of corrupting later builds of the same mesh
+        for a in self.indptr + self.indices:
+            a.flags.writeable = False
         pos = {k: i for i, k in enumerate(iface)}
         self.leaf_jobs: List[np.ndarray] = []
         for leaf in disc.leaves:
@@ -161,7 +166,7 @@ class DeviceAssembler:
         self.jobs = torch.from_numpy(np.ascontiguousarray(table)).to(dev)  # uploaded once
         self._keep = None  # the last flush's inputs / job table, alive until the kernel is ordered
 
-    def _launch(self, blocks, ld: int, block_stride: int, ids, out0, out1, stream) -> None:
+    def _launch(self, blocks, ld: int, block_stride: int, ids, out0, out1) -> None:
         torch = self.torch
         ids = list(ids)
         if not ids:
@@ -176,14 +181,16 @@ class DeviceAssembler:
             n_jobs, leaf0 = len(jobs_h), 0
         if n_jobs == 0:
             return
-        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        # torch's current stream: the caller's launch stream, the one the maps were
+        # produced on and the one finish() reads the values after
+        s = torch.cuda.current_stream(self.device)
         _native.check(self.lib.hps_interface_scatter(
             self.device, ctypes.c_void_p(blocks.data_ptr()), ld, block_stride, leaf0, n_jobs,
             ctypes.c_void_p(jobs.data_ptr()), ctypes.c_void_p(out0.data_ptr()),
             ctypes.c_void_p(out1.data_ptr()), ctypes.c_void_p(s.cuda_stream)))
         self._keep = (blocks, jobs)
 
-    def add(self, dtn, ids, stream=None) -> None:
+    def add(self, dtn, ids) -> None:
         """Scatter-add the DtN maps of a flush (device tensor [len(ids)][m][m])."""
         if self.vectors:
             raise ConfigError("this assembler accumulates interface vectors")
@@ -191,24 +198,25 @@ class DeviceAssembler:
             raise ConfigError(f"DtN batch of shape {tuple(dtn.shape)} for {len(ids)} leaves")
         dtn = dtn.contiguous()
         m = int(dtn.shape[1])
-        self._launch(dtn, m, m * m, ids, self.t_vals, self.c_vals, stream)
+        self._launch(dtn, m, m * m, ids, self.t_vals, self.c_vals)
 
-    def add_vectors(self, flux, ids, stream=None) -> None:
+    def add_vectors(self, flux, ids) -> None:
         """Add the interface part of per-leaf boundary vectors (device [len(ids)][m])."""
         if not self.vectors:
             raise ConfigError("this assembler accumulates T and C")
         if flux.dim() != 2 or flux.shape[0] != len(ids):
             raise ConfigError(f"flux batch of shape {tuple(flux.shape)} for {len(ids)} leaves")
         flux = flux.contiguous()
-        self._launch(flux, 1, int(flux.shape[1]), ids, self.g, self.g, stream)
+        self._launch(flux, 1, int(flux.shape[1]), ids, self.g, self.g)
 
     def finish(self) -> Tuple[sp.csr_matrix, sp.csr_matrix]:
         nt, nc = self.pattern.nnz
-        t_vals = self.t_vals[:nt].cpu().numpy()
+        t_vals = self.t_vals[:nt].cpu().numpy()   # synchronizes the current stream
         c_vals = self.c_vals[:nc].cpu().numpy()
         self._keep = None
         return self.pattern.matrices(t_vals, c_vals)
 
     def finish_vector(self) -> np.ndarray:
+        g = self.g[:self.pattern.n_int].cpu().numpy()
         self._keep = None
-        return self.g[:self.pattern.n_int].cpu().numpy()
+        return g

@@ -92,7 +92,10 @@ constexpr int SMALL_PANEL = HPS_SMALL_PANEL;  // recursion leaf width handled by
 constexpr int RHS_COLS = 16;     // padded rhs block in solve mode
 constexpr int PANEL_SMEM_CAP = 96 * 1024;
 
-enum { MODE_DTN = 0, MODE_REDUCE = 1, MODE_INTERIOR = 2, MODE_SOLOP = 3 };
+// MODE_FACTORS: the solution-operator program, then both outputs of the leaf
+// (S = -A_ii^{-1} A_ib and T = A_bb + A_bi S) from one factorization
+enum { MODE_DTN = 0, MODE_REDUCE = 1, MODE_INTERIOR = 2, MODE_SOLOP = 3, MODE_FACTORS = 4 };
+constexpr int N_MODES = 5;
 
 // Endgame GEMM sharing.  Once every leaf of the launch has been claimed, a CTA
 // that finds no leaf left does not exit: it joins the GEMMs of CTAs still
@@ -2129,6 +2132,18 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     } else if (P.mode == MODE_SOLOP) {
       copy_block(c.M + P.n_pad, c.ld, P.out0 + (size_t)leaf * P.n * P.m, P.m, P.n, P.m, true,
                  P.rowperm ? P.rowpos : nullptr);
+    } else if (P.mode == MODE_FACTORS) {
+      // S = -X, then T from the same X: a_bb - a_bi X (legendre: already formed in the
+      // R_b region by the program; drop: the line-sparse A_bi applied here)
+      copy_block(c.M + P.n_pad, c.ld, P.out1 + (size_t)leaf * P.n * P.m, P.m, P.n, P.m, true,
+                 P.rowperm ? P.rowpos : nullptr);
+      __syncthreads();
+      double* T = P.out0 + (size_t)leaf * P.m * P.m;
+      if (P.legendre) {
+        copy_block(c.M + P.col_rb, c.ld, T, P.m, P.m, P.m, false);
+      } else if (!dtn_lines_stream(P, c, c.M, c.ld, T)) {
+        dtn_lines(P, c.M, c.ld, T);
+      }
     } else {
       double* out = P.out0 + (size_t)leaf * P.n;
       if (P.mode == MODE_REDUCE) {
@@ -2439,13 +2454,13 @@ struct hps_plan_s {
   double* work = nullptr;
   size_t work_doubles = 0;
   int* piv = nullptr;
-  int colperm[4] = {0, 0, 0, 0};
-  int rowperm[4] = {0, 0, 0, 0};
+  int colperm[N_MODES] = {};
+  int rowperm[N_MODES] = {};
   double* scratch = nullptr;
   int ws_slots = 0;
   // unrolled LU programs per mode (device copies)
-  Op* prog[4] = {nullptr, nullptr, nullptr, nullptr};
-  int prog_len[4] = {0, 0, 0, 0};
+  Op* prog[N_MODES] = {};
+  int prog_len[N_MODES] = {};
   double* h_stage = nullptr;
   unsigned long long* prof = nullptr;  // diagnostics counters (device), optional
   int* leaf_counter = nullptr;  // [0] next leaf, [32] CTAs without a leaf (endgame sharing)
@@ -2464,8 +2479,13 @@ struct hps_plan_s {
   double* s_stats = nullptr;
   int* s_done = nullptr;
   size_t s_leaves = 0;
-  TmaMaps maps[4];
-  int maps_ok[4] = {0, 0, 0, 0};
+  TmaMaps maps[N_MODES];
+  int maps_ok[N_MODES] = {};
+  // completion of the plan's last launch: every launch waits on it first, so
+  // launches on different streams (device calls on torch's stream, the host-buffer
+  // path's own streams) never overlap on the shared slot workspace and counters
+  cudaEvent_t last = nullptr;
+  bool last_recorded = false;
 };
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -2500,7 +2520,7 @@ static int make_map(CUtensorMap* map, double* base, uint64_t cols, uint64_t rows
 static int round16(int x) { return (x + 15) / 16 * 16; }
 
 static void mode_dims(const hps_plan_s* P, int mode, int* NR, int* NC) {
-  if (mode == MODE_DTN || mode == MODE_SOLOP) {
+  if (mode == MODE_DTN || mode == MODE_SOLOP || mode == MODE_FACTORS) {
     *NR = P->n_pad;
     *NC = P->n_pad + P->m_pad + (P->legendre ? P->nb_pad : 0);
   } else {
@@ -2514,7 +2534,7 @@ static void mode_dims(const hps_plan_s* P, int mode, int* NR, int* NC) {
 static int rows_alloc(const hps_plan_s* P, int mode) {
   int NR, NC;
   mode_dims(P, mode, &NR, &NC);
-  if (P->legendre && mode == MODE_DTN && P->m_pad > NR) return P->m_pad;
+  if (P->legendre && (mode == MODE_DTN || mode == MODE_FACTORS) && P->m_pad > NR) return P->m_pad;
   if (!P->legendre && mode == MODE_DTN && P->wt) return NR + P->RW;  // W-block rows
   return NR;
 }
@@ -2589,7 +2609,7 @@ static int ensure_workspace(hps_plan_s* P, int mode, int want_slots) {
   CK(cudaMalloc(&P->scratch, (size_t)2 * P->n_pad * TRI_BLOCK * slots * 8));
   P->work_doubles = per * (size_t)slots;
   P->ws_slots = slots;
-  for (int k = 0; k < 4; ++k) P->maps_ok[k] = 0;
+  for (int k = 0; k < N_MODES; ++k) P->maps_ok[k] = 0;
   return ensure_workspace(P, mode, want_slots);
 }
 
@@ -2600,7 +2620,7 @@ static int ensure_program(hps_plan_s* P, int mode) {
   ProgramBuilder b;
   b.n_pad = P->n_pad;
   // working columns: [A_ii | A_ib or rhs]; legendre adds an R_b / T region after them
-  const bool leg_op = P->legendre && (mode == MODE_DTN || mode == MODE_SOLOP);
+  const bool leg_op = P->legendre && (mode == MODE_DTN || mode == MODE_SOLOP || mode == MODE_FACTORS);
   const int NW = leg_op ? P->n_pad + P->m_pad : NC;
   const int col_rb = P->n_pad + P->m_pad;
   if (leg_op)  // A_ib = R_b Q
@@ -2643,7 +2663,7 @@ static int ensure_program(hps_plan_s* P, int mode) {
   } else {
     b.trsm_upper(0, P->n_pad, P->n_pad, NW);
   }
-  if (leg_op && mode == MODE_DTN) {  // T = a_bb - a_bi X in the (now free) R_b region
+  if (leg_op && (mode == MODE_DTN || mode == MODE_FACTORS)) {  // T = a_bb - a_bi X in the (now free) R_b region
     Op o{};
     o.kind = OP_COPY_ABB;
     o.a = col_rb;
@@ -2676,6 +2696,8 @@ static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, c
     if (dbg && (atoi(dbg) & 8) && want > P->sms) want = P->sms;  // diagnostics: one CTA per SM
   }
   if (want > n_leaves) want = n_leaves;
+  // ordered after the plan's previous launch, whatever stream that was on
+  if (P->last_recorded) CK(cudaStreamWaitEvent(stream, P->last, 0));
   const int slots = ensure_workspace(P, mode, want);
   if (slots < 0) return -1;
   LeafParams L;
@@ -2738,7 +2760,23 @@ static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, c
   CK(cudaFuncSetAttribute(hps_leaf_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   hps_leaf_kernel<<<slots, NT, smem, stream>>>(L, P->prog[mode], P->prog_len[mode], P->maps[mode]);
   CK(cudaGetLastError());
+  CK(cudaEventRecord(P->last, stream));
+  P->last_recorded = true;
   return 0;
+}
+
+// Free the slot workspace and the streaming buffers (they are re-allocated by
+// the next launch); templates, orderings and op programs stay.
+static void release_workspace(hps_plan_s* P) {
+  if (P->last_recorded) cudaEventSynchronize(P->last);
+  cudaFree(P->work); cudaFree(P->piv); cudaFree(P->scratch);
+  P->work = nullptr; P->piv = nullptr; P->scratch = nullptr;
+  P->work_doubles = 0; P->ws_slots = 0;
+  for (int k = 0; k < N_MODES; ++k) P->maps_ok[k] = 0;
+  cudaFree(P->share); P->share = nullptr; P->share_cap = 0;
+  cudaFree(P->s_coef); cudaFree(P->s_out); cudaFree(P->s_stats); cudaFree(P->s_done);
+  P->s_coef = nullptr; P->s_out = nullptr; P->s_stats = nullptr; P->s_done = nullptr;
+  P->s_leaves = 0;
 }
 
 
@@ -2925,6 +2963,10 @@ static int plan_create(hps_plan_t* out, int device, int dim, int p, int legendre
   P->wb = wb;
   P->budget = workspace_budget_bytes;
   if (cudaSetDevice(device) != cudaSuccess) { delete P; return fail("cudaSetDevice failed"); }
+  if (cudaEventCreateWithFlags(&P->last, cudaEventDisableTiming) != cudaSuccess) {
+    delete P;
+    return fail("cudaEventCreate failed");
+  }
   cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device);
   P->slots = (max_slots > 0 && max_slots < CTAS_PER_SM * P->sms) ? max_slots : CTAS_PER_SM * P->sms;
   const size_t tab = (size_t)dim * p * p * 8;
@@ -2983,6 +3025,8 @@ int hps_plan_create_legendre(hps_plan_t* out, int device, int dim, int p, int ha
 int hps_plan_destroy(hps_plan_t P) {
   if (!P) return 0;
   cudaSetDevice(P->device);
+  release_workspace(P);
+  if (P->last) cudaEventDestroy(P->last);
   cudaFree(P->D1); cudaFree(P->D2); cudaFree(P->a_bi); cudaFree(P->a_bb);
   cudaFree(P->leaf_counter);
   cudaFree(P->share);
@@ -2995,9 +3039,25 @@ int hps_plan_destroy(hps_plan_t P) {
   cudaFree(P->s_coef); cudaFree(P->s_out); cudaFree(P->s_stats); cudaFree(P->s_done);
   cudaFree(P->Q); cudaFree(P->a_bi_pad); cudaFree(P->bpos);
   cudaFree(P->work); cudaFree(P->piv); cudaFree(P->scratch);
-  for (int k = 0; k < 4; ++k) cudaFree(P->prog[k]);
+  for (int k = 0; k < N_MODES; ++k) cudaFree(P->prog[k]);
   if (P->h_stage) cudaFreeHost(P->h_stage);
   delete P;
+  return 0;
+}
+
+int hps_plan_release(hps_plan_t P) {
+  if (!P) return fail("null plan");
+  CK(cudaSetDevice(P->device));
+  release_workspace(P);
+  return 0;
+}
+
+int hps_plan_workspace(hps_plan_t P, size_t* bytes, int* slots) {
+  if (!P) return fail("null plan");
+  const size_t per_slot = (size_t)piv_stride(P) * 4 + (size_t)2 * P->n_pad * TRI_BLOCK * 8;
+  if (bytes) *bytes = P->work_doubles * 8 + per_slot * P->ws_slots + sizeof(ShareSlot) * P->share_cap +
+                      P->s_leaves * ((size_t)P->ncoef * P->n * 8 + (size_t)P->m * P->m * 8 + 16 + 4);
+  if (slots) *slots = P->ws_slots;
   return 0;
 }
 
@@ -3023,6 +3083,13 @@ int hps_leaf_dtn(hps_plan_t P, int n_leaves, const double* coeffs, double* dtn, 
                  void* stream) {
   if (!P) return fail("null plan");
   return launch(P, MODE_DTN, n_leaves, coeffs, nullptr, nullptr, dtn, nullptr, stats,
+                (cudaStream_t)stream);
+}
+
+int hps_leaf_factors(hps_plan_t P, int n_leaves, const double* coeffs, double* dtn, double* s,
+                     double* stats, void* stream) {
+  if (!P) return fail("null plan");
+  return launch(P, MODE_FACTORS, n_leaves, coeffs, nullptr, nullptr, dtn, s, stats,
                 (cudaStream_t)stream);
 }
 

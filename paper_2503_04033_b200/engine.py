@@ -45,9 +45,16 @@ def _np_ptr(a: Optional[np.ndarray]) -> ctypes.c_void_p:
 
 
 class LeafEngine:
-    """One device plan for equal leaves of a mesh (shape, order, coefficient layout)."""
+    """One device plan for equal leaves of a mesh (shape, order, coefficient layout).
+
+    A plan's slot workspace (tens of GB at p >= 16) is allocated by its first
+    launch and held until :meth:`release` — ``for_template`` keeps a small cache of
+    plans and releases the workspace of every other cached plan on the device
+    before handing one out, so only the plan in use holds device memory.
+    """
 
     _plans = {}
+    MAX_CACHED = 4
 
     def __init__(self, template: LeafTemplate, has_first: bool, has_zeroth: bool,
                  device: int = 0, max_slots: int = 0, workspace_budget: int = 0,
@@ -110,13 +117,45 @@ class LeafEngine:
     @classmethod
     def for_template(cls, template: LeafTemplate, coeffs, device: int = 0, **kw) -> "LeafEngine":
         has_first, has_zeroth, has_cross = coefficient_layout(coeffs)
-        key = (template.widths, template.p, template.corner_mode, has_first, has_zeroth, has_cross,
-               device, tuple(sorted(kw.items())))
-        eng = cls._plans.get(key)
+        key = (tuple(float(w) for w in template.widths), template.p, template.corner_mode, has_first,
+               has_zeroth, has_cross, int(device), tuple(sorted(kw.items())))
+        eng = cls._plans.pop(key, None)
+        for other in cls._plans.values():        # one workspace per device at a time
+            if other.device == int(device):
+                other.release()
         if eng is None:
+            while len(cls._plans) >= cls.MAX_CACHED:   # drop the least recently used: its
+                cls._plans.pop(next(iter(cls._plans))).release()  # plan dies with its last user
             eng = cls(template, has_first, has_zeroth, device=device, has_cross=has_cross, **kw)
-            cls._plans[key] = eng
+        cls._plans[key] = eng                   # most recently used last
         return eng
+
+    @classmethod
+    def clear_cache(cls) -> None:
+        """Drop every cached plan and free its workspace."""
+        while cls._plans:
+            cls._plans.popitem()[1].release()
+
+    def release(self) -> None:
+        """Free the slot workspace and streaming buffers (after the last launch
+        finishes); the next call re-allocates them."""
+        bufs = getattr(self, "_stage_bufs", None)
+        if bufs is not None:
+            for b in bufs:
+                if b is not None:
+                    b[2].synchronize()
+            self._stage_bufs = None
+        if self.plan is not None and self.plan.value:
+            _native.check(self.lib.hps_plan_release(self.plan))
+
+    def close(self) -> None:
+        self.__del__()
+
+    def workspace(self) -> Tuple[int, int]:
+        """(device bytes held now, slots they are sized for)."""
+        b, s = ctypes.c_size_t(), ctypes.c_int()
+        _native.check(self.lib.hps_plan_workspace(self.plan, ctypes.byref(b), ctypes.byref(s)))
+        return int(b.value), int(s.value)
 
     # ---------------------------------------------------------------- helpers
     def _stream(self, stream):
@@ -138,6 +177,39 @@ class LeafEngine:
     def _empty(self, *shape):
         return self.torch.empty(shape, dtype=self.torch.float64, device=f"cuda:{self.device}")
 
+    empty = _empty
+
+    def synchronize(self) -> None:
+        self.torch.cuda.synchronize(self.device)
+
+    def stage(self, pack: np.ndarray, stream=None):
+        """Host coefficient pack -> device tensor through a pinned double buffer: the
+        H2D copy is queued on the launch stream and the host returns at once (it
+        packs the next flush while the device works on this one)."""
+        torch = self.torch
+        pack = np.ascontiguousarray(pack, dtype=np.float64)
+        self._check_coeffs(pack)
+        L = pack.shape[0]
+        self._stage_k = (getattr(self, "_stage_k", 0) + 1) % 2
+        bufs = getattr(self, "_stage_bufs", None)
+        if bufs is None:
+            bufs = self._stage_bufs = [None, None]
+        b = bufs[self._stage_k]
+        if b is None or b[0].shape[0] < L:
+            if b is not None:
+                b[2].synchronize()
+            shape = (L, self.ncoef, self.n)
+            b = bufs[self._stage_k] = (torch.empty(shape, dtype=torch.float64, pin_memory=True),
+                                       self._empty(*shape), torch.cuda.Event())
+        host, dev, done = b
+        done.synchronize()                       # the last copy out of this host buffer is over
+        host[:L].numpy()[:] = pack
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(s):
+            dev[:L].copy_(host[:L], non_blocking=True)
+            done.record(s)
+        return dev[:L]
+
     # ---------------------------------------------------------- device calls
     def dtn(self, coeffs, out=None, stats=None, stream=None):
         """DtN maps (leaves, m, m) for device coefficient packs (leaves, ncoef, n)."""
@@ -149,6 +221,17 @@ class LeafEngine:
         _native.check(self.lib.hps_leaf_dtn(self.plan, L, _ptr(coeffs), _ptr(out), _ptr(stats),
                                             self._stream(stream)))
         return out, stats
+
+    def factors(self, coeffs, stream=None):
+        """DtN maps (leaves, m, m) and solution operators (leaves, n, m) from one
+        factorization per leaf (one launch)."""
+        coeffs = self._dev(coeffs)
+        self._check_coeffs(coeffs)
+        L = coeffs.shape[0]
+        dtn, s, stats = self._empty(L, self.m, self.m), self._empty(L, self.n, self.m), self._empty(L, 2)
+        _native.check(self.lib.hps_leaf_factors(self.plan, L, _ptr(coeffs), _ptr(dtn), _ptr(s),
+                                                _ptr(stats), self._stream(stream)))
+        return dtn, s, stats
 
     def solution_operator(self, coeffs, stream=None):
         coeffs = self._dev(coeffs)
@@ -200,6 +283,10 @@ class LeafEngine:
         _native.check(self.lib.hps_leaf_dtn_host(self.plan, L, _np_ptr(coeffs), _np_ptr(out),
                                                  _np_ptr(stats), int(chunk_leaves)))
         return out, stats
+
+    def factors_host(self, coeffs):
+        dtn, s, stats = self.factors(coeffs)
+        return dtn.cpu().numpy(), s.cpu().numpy(), stats.cpu().numpy()
 
     def apply_host(self, coeffs, u_int, u_b):
         return self.apply(coeffs, u_int, u_b).cpu().numpy()

@@ -366,9 +366,8 @@ def build_leaf_factors(template: LeafTemplate, coeffs: CoefficientField,
     x_int = grid[template.interior_idx]
     engine = engine or LeafEngine.for_template(template, coeffs)
     pack = pack_coefficients(coeffs, x_int, 1)
-    dtn, stats = engine.dtn_host(pack)
+    dtn, s, stats = engine.factors_host(pack)   # one factorization, one launch
     check_pivots(stats, [leaf_index])
-    s, _ = engine.solution_operator_host(pack)
     return LeafFactors(a_ii_factor=None, a_ib=None, a_bi=template.a_bi, a_bb=template.a_bb,
                        s=s[0], dtn=dtn[0], _engine=engine, _coeffs=pack[0])
 

@@ -47,3 +47,13 @@ def test_reference_arm_under_torchrun_prints_one_line():
     (line,) = _lines(res.stdout)
     assert line["impl"] == "reference" and line["n_gpus"] == 2
     assert line["config"]["leaves_per_gpu"] == 4   # the 2x2x2 grid split by leaf index
+
+
+def test_bench_parity_spot_check_spreads_over_the_grid():
+    """bench.py's parity leaves: 8 per rank, the bump-centre leaf and the fixture
+    leaves first, the rest spread over the share."""
+    import bench
+    ids = list(range(4096))
+    chosen = bench.spread_sample(ids, 8, must=[bench.centre_leaf(16), 375])
+    assert chosen[:2] == [1911, 375] and len(set(chosen)) == 8
+    assert max(chosen) - min(chosen) > 3000

@@ -1,9 +1,11 @@
-"""Multi-process (world_size 2, gloo, CPU) coverage of the leaf-sharded build path.
+"""Multi-process (gloo, CPU) coverage of the multi-rank solver stages.
 
-Each rank reduces its contiguous leaf shard (here with the CPU oracle standing in
-for the rank's GPU) and the blocks are gathered to rank 0 in leaf order; the
-result must equal the single-process computation.  Also checks the
-max-over-ranks timing rule.
+``build``, ``reduce_load`` and ``solve`` split the leaves by index over the
+ranks of an initialized torch.distributed group (reference worker pool,
+condensation.py:248-264, 325-333, 385-391).  Here every rank's GPU is stood in
+for by the CPU oracle (tests/hps_fakes.py); the sharding, flushes and collectives
+run unchanged over gloo.  The bar is bit-exact against one process: the same T,
+C, g_b and solution.
 """
 
 import os
@@ -29,32 +31,47 @@ def test_shard_range_partitions():
 def _problem():
     from paper_2503_04033_b200.geometry import MeshConfig, build_discretization
     from paper_2503_04033_b200.problems import make_problem
-    spec = make_problem("bump_helmholtz", d=3, kappa=12.0)
+    spec = make_problem("helmholtz_green", d=3, kappa=6.0)
     return spec, build_discretization(spec.domain, MeshConfig((3, 2, 2), 6))
 
 
-def _oracle_compute(disc):
-    from oracle import hps_oracle as O
-    tpl = O.OracleTemplate(disc.leaf_widths, disc.p)
-
-    def compute(pack):
-        return np.stack([O.leaf_dtn(tpl, c[:3].T, None, c[3])[0] for c in pack])
-    return compute
+def _schedule(**kw):
+    from paper_2503_04033_b200.condensation import BatchSchedule
+    # a small budget: several flushes per rank (5 staged blocks of 8 * 96^2 bytes per flush)
+    return BatchSchedule(memory_budget=5 * 8 * 96 ** 2 + 4 * 96 ** 2, **kw)
 
 
-def _worker(rank, world, port, out_path):
+def _run(distributed):
+    from paper_2503_04033_b200.condensation import build, reduce_load, solve
+    spec, disc = _problem()
+    sys_ = build(disc, spec.coeffs, _schedule(distributed=distributed))
+    v_list, g_b = reduce_load(disc, spec.coeffs, spec.f, spec.g, sys_)
+    report = solve(sys_, v_list, g_b, spec.g)
+    return sys_, v_list, g_b, report
+
+
+def _worker(rank, world, port, out_dir):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2503_04033_b200.sharding import max_over_ranks, sharded_dtn
-        spec, disc = _problem()
-        blocks = sharded_dtn(disc, spec.coeffs, world, rank, compute=_oracle_compute(disc))
-        slowest = max_over_ranks(float(rank + 1))
+        import hps_fakes as _fakes
+        engines = _fakes.install()
+        sys_, v_list, g_b, report = _run(None)
+        shard = sys_.shard
+        assert shard is not None and shard.world == world and shard.rank == rank
+        own = set(shard.ids)
+        assert all((v is not None) == (i in own) for i, v in enumerate(v_list))
+        assert sys_.peak_workspace_bytes <= sys_.schedule.memory_budget
+        launches = sum(e.launches for e in engines)
+        res = dict(u=report.u, residual=report.residual, launches=launches,
+                   start=shard.start, stop=shard.stop)
         if rank == 0:
-            np.savez(out_path, blocks=blocks, slowest=slowest)
+            res.update(t_data=sys_.t.data, t_indices=sys_.t.indices, t_indptr=sys_.t.indptr,
+                       c_data=sys_.dirichlet_coupling.data, g_b=g_b)
         else:
-            assert blocks is None
+            assert sys_.t is None and sys_.factorization is None and g_b is None
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), **res)
     finally:
         dist.destroy_process_group()
 
@@ -65,68 +82,73 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def test_sharded_build_matches_single_process(tmp_path):
-    out = str(tmp_path / "dist.npz")
-    mp.start_processes(_worker, args=(2, _free_port(), out), nprocs=2, start_method="spawn")
-    res = np.load(out)
-    spec, disc = _problem()
-    from paper_2503_04033_b200.local_ops import pack_coefficients
-    from paper_2503_04033_b200.condensation import interior_points
-    full = _oracle_compute(disc)(pack_coefficients(spec.coeffs,
-                                                   interior_points(disc, range(len(disc.leaves))),
-                                                   len(disc.leaves)))
-    assert np.array_equal(res["blocks"], full)
-    assert float(res["slowest"]) == 2.0
-
-
-def _replay_scatter(pattern, dtn, ids):
-    """numpy replay of hps_interface_scatter (the rank's GPU in this CPU test)."""
-    out = [np.zeros(pattern.nnz[0]), np.zeros(pattern.nnz[1])]
-    for k, r0, c0, nr, nc, tgt, base, stride in pattern.jobs_for(ids):
-        idx = base + np.arange(nr)[:, None] * stride + np.arange(nc)[None, :]
-        np.add.at(out[tgt], idx, dtn[k, r0:r0 + nr, c0:c0 + nc])
-    return out
-
-
-def _interface_worker(rank, world, port, out_path):
-    import torch.distributed as dist
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    try:
-        from paper_2503_04033_b200.sharding import sharded_interface
-        spec, disc = _problem()
-        res = sharded_interface(disc, spec.coeffs, world, rank, compute=_oracle_compute(disc),
-                                scatter=_replay_scatter)
-        if rank == 0:
-            t, c = res
-            np.savez(out_path, t_data=t.data, t_indices=t.indices, t_indptr=t.indptr,
-                     c_data=c.data, c_indices=c.indices, c_indptr=c.indptr)
-        else:
-            assert res is None
-    finally:
-        dist.destroy_process_group()
-
-
 @pytest.mark.parametrize("world", [2, 3])
-def test_sharded_interface_reduce_matches_host_assembly(tmp_path, world):
-    """Partial CSR values of T and C per rank, one sum-reduce: bit-identical to
-    the single-process host scatter of all DtN maps."""
-    out = str(tmp_path / "iface.npz")
-    mp.start_processes(_interface_worker, args=(world, _free_port(), out), nprocs=world,
+def test_multi_rank_build_load_solve_match_single_process(tmp_path, world, monkeypatch):
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
                        start_method="spawn")
-    res = np.load(out)
+    import hps_fakes as _fakes
+    from paper_2503_04033_b200 import condensation
+    monkeypatch.setattr(condensation, "_engine_for", condensation._engine_for)
+    monkeypatch.setattr(condensation, "DeviceAssembler", condensation.DeviceAssembler)
+    _fakes.install()
+    sys_, v_list, g_b, report = _run(False)
+    assert sys_.shard is None
+    r0 = np.load(tmp_path / "rank0.npz")
+    # T, C and g_b summed onto the root: bit-identical to one process
+    assert np.array_equal(r0["t_indptr"], sys_.t.indptr)
+    assert np.array_equal(r0["t_indices"], sys_.t.indices)
+    assert np.array_equal(r0["t_data"], sys_.t.data)
+    assert np.array_equal(r0["c_data"], sys_.dirichlet_coupling.data)
+    assert np.array_equal(r0["g_b"], g_b)
+    spans = []
+    for r in range(world):
+        res = np.load(tmp_path / f"rank{r}.npz")
+        # every rank returns the same assembled solution and residual
+        assert np.array_equal(res["u"], report.u)
+        assert float(res["residual"]) == report.residual
+        spans.append((int(res["start"]), int(res["stop"])))
+        assert int(res["launches"]) >= 1
+    assert spans == [shard_range(len(sys_.disc.leaves), world, r) for r in range(world)]
+    # and the solution is the manufactured one to the accuracy of p = 6 leaves
     spec, disc = _problem()
-    from paper_2503_04033_b200.condensation import (_make_dof_map, finalize_host, interior_points,
-                                                    scatter_leaf_blocks)
-    from paper_2503_04033_b200.local_ops import LeafTemplate, pack_coefficients
-    from paper_2503_04033_b200.sparse_backend import SparseMatrix
-    ids = list(range(len(disc.leaves)))
-    full = _oracle_compute(disc)(pack_coefficients(spec.coeffs, interior_points(disc, ids), len(ids)))
-    dof_map = _make_dof_map(disc, LeafTemplate(disc.leaf_widths, disc.p, disc.corner_mode, False))
-    tb, cr, cc, cv = SparseMatrix(disc.n_interface), [], [], []
-    scatter_leaf_blocks(dof_map, ids, full, tb, cr, cc, cv)
-    t, c = finalize_host(tb, cr, cc, cv, disc.n_interface, disc.n_dirichlet)
-    for name, ref in (("t", t), ("c", c)):
-        assert np.array_equal(res[f"{name}_indptr"], ref.indptr)
-        assert np.array_equal(res[f"{name}_indices"], ref.indices)
-        assert np.array_equal(res[f"{name}_data"], ref.data)
+    exact = spec.exact(disc.nodes)
+    assert np.linalg.norm(report.u - exact) / np.linalg.norm(exact) < 2e-3
+
+
+def test_flush_respects_memory_budget():
+    """The staged DtN blocks of a flush stay within memory_budget (the reference's
+    peak_workspace_bytes <= budget contract, condensation.py:255-263, 291)."""
+    import hps_fakes as _fakes
+    from paper_2503_04033_b200 import condensation
+    saved = condensation._engine_for, condensation.DeviceAssembler
+    try:
+        engines = _fakes.install()
+        spec, disc = _problem()
+        sched = _schedule(distributed=False)
+        sys_ = condensation.build(disc, spec.coeffs, sched)
+        res = sched.resolve(disc.p, disc.d, disc.corner_mode)
+        assert sys_.peak_workspace_bytes <= sched.memory_budget
+        assert sys_.peak_workspace_bytes == 5 * res.block_bytes
+        assert engines[0].launches == -(-len(disc.leaves) // 5)   # ceil(12 / 5) flushes
+        # an explicit resident_limit bounds the flush further
+        sys2 = condensation.build(disc, spec.coeffs, _schedule(distributed=False, resident_limit=2))
+        assert sys2.peak_workspace_bytes == 2 * res.block_bytes
+        assert np.array_equal(sys2.t.data, sys_.t.data)
+    finally:
+        condensation._engine_for, condensation.DeviceAssembler = saved
+
+
+def test_max_over_ranks_single_process():
+    from paper_2503_04033_b200.sharding import max_over_ranks
+    assert max_over_ranks(3.5) == 3.5
+
+
+def test_bench_leaf_shards_cover_the_grid():
+    """bench.py --gpus N: rank r owns leaves [L r / N, L (r + 1) / N) of ONE grid;
+    the configs[3] share of rank r is the r-th eighth."""
+    import bench
+    for world in (1, 2, 4, 8):
+        ids = [bench.shard_ids(4096, world, r) for r in range(world)]
+        assert sum(ids, []) == list(range(4096))
+    assert bench.shard_ids(4096, 8, 0) == list(range(512))
+    assert bench.shard_ids(4096, 8, 3)[0] == 1536

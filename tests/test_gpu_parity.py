@@ -244,12 +244,3 @@ def test_bench_order_outputs_match_reference(name):
         pmin, pmax, _ = BG[k + "pivots"]
         assert 0.0 < stats[i, 0] <= stats[i, 1] and 0.1 < stats[i, 1] / pmax < 10.0
 
-
-def test_bench_parity_spot_check_spreads_over_the_grid():
-    """bench.py's parity leaves: 8 per rank, the bump-centre leaf and the fixture
-    leaves first, the rest spread over the share."""
-    import bench
-    ids = list(range(4096))
-    chosen = bench.spread_sample(ids, 8, must=[bench.centre_leaf(16), 375])
-    assert chosen[:2] == [1911, 375] and len(set(chosen)) == 8
-    assert max(chosen) - min(chosen) > 3000

@@ -99,19 +99,53 @@ def test_build_leaf_operator_api():
     assert np.allclose(lf.solve_interior(np.ones(lf.s.shape[0])), lf.solve_interior(np.ones((lf.s.shape[0], 2)))[:, 0])
 
 
-def test_sharded_dtn_single_rank_on_gpu():
-    from paper_2503_04033_b200 import build_discretization, MeshConfig, make_problem
-    from paper_2503_04033_b200.sharding import sharded_dtn
+def test_leaf_factors_one_launch():
+    """build_leaf_factors: DtN and S from ONE factorization (hps_leaf_factors): S equals
+    the solution-operator launch bit for bit, T the DtN launch to rounding, and both
+    the oracle within 1e-10."""
+    from paper_2503_04033_b200.engine import LeafEngine
+    from paper_2503_04033_b200.local_ops import LeafTemplate
     from oracle import hps_oracle as O
-    spec = make_problem("bump_helmholtz", d=3, kappa=20.0)
-    disc = build_discretization(spec.domain, MeshConfig((2, 2, 2), 8))
-    blocks = sharded_dtn(disc, spec.coeffs, 1, 0)
-    tpl = O.OracleTemplate(disc.leaf_widths, 8)
-    from paper_2503_04033_b200.local_ops import pack_coefficients
-    from paper_2503_04033_b200.condensation import interior_points
-    pack = pack_coefficients(spec.coeffs, interior_points(disc, range(8)), 8)
-    for k in range(8):
-        assert rel(blocks[k], O.leaf_dtn(tpl, pack[k, :3].T, None, pack[k, 3])[0]) <= 1e-10
+    rng = np.random.default_rng(3)
+    for d, p in ((3, 8), (3, 12), (2, 9)):
+        tpl = LeafTemplate((0.25,) * d, p, "drop", False)
+        n = tpl.n_interior
+        pack = np.concatenate([1.0 + 0.05 * rng.standard_normal((3, d, n)),
+                               -200.0 * (1.0 + 0.1 * rng.standard_normal((3, 1, n)))], axis=1)
+        eng = LeafEngine(tpl, False, True, device=0)
+        t, s, stats = eng.factors_host(pack)
+        s_ref, _ = eng.solution_operator_host(pack)
+        t_ref, _ = eng.dtn_host(pack)
+        assert np.array_equal(s, s_ref)
+        assert rel(t, t_ref) <= 1e-12
+        otpl = O.OracleTemplate(tpl.widths, p)
+        for k in range(3):
+            ot, os_, _ = O.leaf_dtn(otpl, pack[k, :d].T, None, pack[k, d])
+            assert rel(t[k], ot) <= 1e-10 and rel(s[k], os_) <= 1e-10
+        assert np.all(stats[:, 0] > 0)
+
+
+def test_launches_on_different_streams_are_ordered():
+    """A device-buffer launch queued on torch's stream and a host-buffer launch (own
+    streams) on the same plan do not overlap on the shared slot workspace."""
+    import torch
+    from paper_2503_04033_b200.engine import LeafEngine
+    from paper_2503_04033_b200.local_ops import LeafTemplate
+    rng = np.random.default_rng(8)
+    tpl = LeafTemplate((0.25,) * 3, 10, "drop", False)
+    n = tpl.n_interior
+    L = 600
+    pack = np.concatenate([np.ones((L, 3, n)), -300.0 * (1.0 + 0.2 * rng.standard_normal((L, 1, n)))],
+                          axis=1)
+    eng = LeafEngine(tpl, False, True, device=0)
+    ref, _ = eng.dtn_host(pack)
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        dev, _ = eng.dtn(torch.from_numpy(pack).cuda(), stream=side)   # still running ...
+    host, _ = eng.dtn_host(pack[::-1].copy())                          # ... when this starts
+    torch.cuda.synchronize()
+    assert np.array_equal(dev.cpu().numpy(), ref)
+    assert np.array_equal(host, ref[::-1])
 
 
 def test_bench_emits_contract_line():

@@ -144,18 +144,28 @@ def test_build_device_and_host_assembly_identical(boxes, p, monkeypatch):
 
 
 @pytest.mark.gpu
-def test_sharded_interface_single_rank_matches_build():
-    import torch
-    from paper_2503_04033_b200 import make_problem
+def test_build_flushes_and_workspace_release():
+    """A budget of a few staged maps (many flushes, partial waves) gives the same T and
+    C bit for bit as one flush; the staged bytes stay within memory_budget; the leaf
+    engine's workspace is reported, can be released and is re-allocated on demand."""
+    from paper_2503_04033_b200 import BatchSchedule, make_problem
     from paper_2503_04033_b200.condensation import build
-    from paper_2503_04033_b200.sharding import sharded_interface
     spec = make_problem("bump_helmholtz", d=3, kappa=20.0)
     disc = build_discretization(spec.domain, MeshConfig((3, 2, 2), 8))
-    torch.cuda.set_device(0)
-    t, c = sharded_interface(disc, spec.coeffs, 1, 0)
-    ref = build(disc, spec.coeffs)
-    _same(t, ref.t)
-    _same(c, ref.dirichlet_coupling)
+    one = build(disc, spec.coeffs, BatchSchedule(memory_budget=1 << 30))
+    tb = 8 * (6 * 36) ** 2
+    budget = 5 * tb + tb // 2      # 5 staged maps per flush: 12 leaves in 3 flushes
+    small = build(disc, spec.coeffs, BatchSchedule(memory_budget=budget))
+    assert small.peak_workspace_bytes <= budget < one.peak_workspace_bytes
+    _same(small.t, one.t)
+    _same(small.dirichlet_coupling, one.dirichlet_coupling)
+    eng = small.engine
+    held, slots = eng.workspace()
+    assert held > 0 and slots >= 1 and small.device_workspace_bytes > 0
+    eng.release()
+    assert eng.workspace() == (0, 0)
+    again = build(disc, spec.coeffs, BatchSchedule(memory_budget=budget))
+    _same(again.t, one.t)
 
 
 @pytest.mark.parametrize("boxes,p,mode", CASES)
@@ -191,6 +201,22 @@ def test_reduce_load_device_and_host_identical(monkeypatch):
     v_host, g_host = reduce_load(disc, spec.coeffs, spec.f, spec.g, sys_)
     assert np.array_equal(g_dev, g_host)
     assert all(np.array_equal(a, b) for a, b in zip(v_dev, v_host))
+
+
+def test_cached_pattern_indices_are_read_only():
+    """T and C share the cached pattern's index arrays: an in-place structural edit
+    of a returned matrix raises instead of corrupting later builds (advisor finding)."""
+    disc = _disc((2, 2, 1), 6, "drop")
+    pat = InterfacePattern(disc)
+    t, c = pat.matrices(np.ones(pat.nnz[0]), np.ones(pat.nnz[1]))
+    before = pat.indptr[0].copy()
+    with pytest.raises(ValueError):
+        t.eliminate_zeros()
+    assert np.array_equal(pat.indptr[0], before)
+    t2 = t.copy()            # a copy is the user's own
+    t2.data[:] = 0.0
+    t2.eliminate_zeros()
+    assert t2.nnz == 0 and t.nnz == pat.nnz[0]
 
 
 def test_pattern_is_built_once_per_discretization():

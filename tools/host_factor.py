@@ -36,4 +36,4 @@ for p in (int(x) for x in a.ps.split(",")):
            "solve_bvp_wall_s": wall, "residual": report.residual}
     print(json.dumps(row), flush=True)
     del sys_, report
-    LeafEngine._plans.clear()
+    LeafEngine.clear_cache()

@@ -40,5 +40,5 @@ for p in (int(x) for x in a.ps.split(",")):
     print(json.dumps(row), flush=True)
     rows.append(row)
     del out, coeffs, stats, eng
-    LeafEngine._plans.clear()
+    LeafEngine.clear_cache()
     torch.cuda.empty_cache()

@@ -83,7 +83,7 @@ constexpr int MI = TM / WM / 8;       // 8-row m-tiles per warp
 constexpr int NJ = TN / WN / 8;       // 8-col n-tiles per warp (4)
 static_assert(MI * 8 * WM == TM && NJ == 4, "warp tiling");
 constexpr int EPI_DBL = EPI_SLOTS * 2 * 8 * 16;  // per warp: ring slots x two [8][16] blocks
-constexpr int GEMM_SMEM_BYTES = (STAGES * STAGE_DBL + (NT / 32) * EPI_DBL) * 8;
+constexpr int WIDE_SMEM_BYTES = (STAGES * STAGE_DBL + (NT / 32) * EPI_DBL) * 8;
 constexpr int TRI_BLOCK = 64;    // triangular base block (explicit inverse + GEMM)
 #ifndef HPS_SMALL_PANEL
 #define HPS_SMALL_PANEL 32
@@ -171,8 +171,13 @@ struct LeafParams {
                              // 16 no endgame GEMM sharing
 };
 
-constexpr int PROF_SLOTS = 32;  // 0..8 op kinds, 9 leaves, 10-14 panel steps, 15 interchanges,
+#ifndef HPS_PROF_EXEC
+#define HPS_PROF_EXEC 0  // diagnostics build: count the DMMAs each GEMM op executes
+#endif
+constexpr int PROF_SLOTS = 48;  // 0..8 op kinds, 9 leaves, 10-14 panel steps, 15 interchanges,
                                 // 16-18 GEMM cycles by N (<=64, <=256, >256), 19-21 their MFLOP, 22 assemble, 23 output
+                                // (HPS_PROF_EXEC) 32-34 executed DMMA flops by N bucket, 35-37 by phase,
+                                // 38-40 GEMM cycles by phase
 
 // ---------------------------------------------------------------------------
 // PTX helpers
@@ -317,9 +322,9 @@ struct GemmShape {
   static_assert(MI_ == 4 && NJ_ == 4, "32 x 32 warp tiles");
 };
 constexpr int NARROW_SMEM_DBL = STAGES * GemmShape<GemmNarrow>::SDBL + (NT / 32) * EPI_DBL;
-static_assert(NARROW_SMEM_DBL * 8 <= GEMM_SMEM_BYTES, "narrow stages fit the wide GEMM smem");
-static_assert((STAGES * GemmShape<GemmTall>::SDBL + (NT / 32) * EPI_DBL) * 8 <= GEMM_SMEM_BYTES,
-              "tall stages fit the wide GEMM smem");
+constexpr int TALL_SMEM_DBL = STAGES * GemmShape<GemmTall>::SDBL + (NT / 32) * EPI_DBL;
+// dynamic shared memory of the GEMM engine: the largest of the three tile shapes
+constexpr int GEMM_SMEM_BYTES = std::max(WIDE_SMEM_BYTES, 8 * std::max(NARROW_SMEM_DBL, TALL_SMEM_DBL));
 
 struct Ctx {
   double* M;
@@ -350,6 +355,9 @@ struct Ctx {
   const int* leaf_counter;
   int n_leaves;
 };
+#if HPS_PROF_EXEC
+__shared__ unsigned long long s_exec_dmma;  // DMMAs issued by this CTA's warps in the current op
+#endif
 
 // ---------------------------------------------------------------------------
 // GEMM engine: C[MxN] = (sub ? C - A*B : A*B) with A = M[ar.., ac..] (or the
@@ -516,6 +524,9 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
 
   int tile = 0, kc = 0, it = 0, my_tiles = 0;
   bool in_tile = false;
+#if HPS_PROF_EXEC
+  unsigned long long my_dmma = 0;
+#endif
   // 8x8 sub-tiles of this warp that lie inside the GEMM extent (warp-uniform):
   // edge tiles skip the DMMAs on zero-filled rows / columns.
   int mv = MI, nv = NJ;
@@ -607,6 +618,9 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     if (!zero_chunk) {
       if (mv == MI && nv == NJ) mainloop(std::false_type{});
       else if (mv > 0 && nv > 0) mainloop(std::true_type{});
+#if HPS_PROF_EXEC
+      my_dmma += (unsigned long long)(mv * nv * (KC / 4));
+#endif
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&c.empty[s]);
@@ -671,6 +685,9 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     }
   }
   c.pipe += it;
+#if HPS_PROF_EXEC
+  if (c.prof && lane == 0) atomicAdd(&s_exec_dmma, my_dmma);
+#endif
   if (sub && lane == 0) {
     bulk_wait_all();
     fence_proxy_async_global();
@@ -1998,6 +2015,9 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
       mbar_init(&bars[STAGES + s], NT / 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+#if HPS_PROF_EXEC
+    s_exec_dmma = 0;
+#endif
   }
   __syncthreads();
   Ctx c;
@@ -2109,6 +2129,16 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
       if (prof && threadIdx.x == 0) {
         const long long dt = clock64() - t0;
         prof[28 + phase] += dt;
+#if HPS_PROF_EXEC
+        if (op.kind == OP_GEMM_SUB || op.kind == OP_GEMM_SET || op.kind == OP_GEMM_SET_Q ||
+            op.kind == OP_GEMM_SUB_ABI || op.kind == OP_GEMM_SET_R) {
+          const unsigned long long f = s_exec_dmma * 512ull;  // flops per m8n8k4 DMMA
+          prof[32 + (op.Ndim <= 64 ? 0 : (op.Ndim <= 256 ? 1 : 2))] += f;
+          prof[35 + phase] += f;
+          prof[38 + phase] += dt;
+        }
+        s_exec_dmma = 0;
+#endif
         const int pk = op.kind < OP_RHS_PROFILE ? op.kind
                        : (op.kind == OP_RHS_PROFILE ? 24
                           : (op.kind == OP_GEMM_SET_R ? OP_GEMM_SET : (op.kind == OP_GMIN16 ? 22 : 27)));
@@ -2696,6 +2726,21 @@ static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, c
     if (dbg && (atoi(dbg) & 8) && want > P->sms) want = P->sms;  // diagnostics: one CTA per SM
   }
   if (want > n_leaves) want = n_leaves;
+  // dynamic shared memory: the largest of the GEMM stages, the panel and the inverses
+  const int panel_bytes = ((P->n_pad * P->wb > 1024 ? P->n_pad * P->wb : 1024) + 32 * P->wb) * 8;
+  int smem = GEMM_SMEM_BYTES;
+  if (panel_bytes > smem) smem = panel_bytes;
+  if ((2 * TRI_BLOCK * TRI_LD + 32 * TRI_BLOCK / 2) * 8 > smem) smem = (2 * TRI_BLOCK * TRI_LD + 32 * TRI_BLOCK / 2) * 8;
+  CK(cudaFuncSetAttribute(hps_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  CK(cudaFuncSetAttribute(hps_leaf_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  {
+    // the grid is persistent and CTAs wait on each other (endgame sharing): every
+    // CTA must be resident at once, so never launch more than the occupancy allows
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hps_leaf_kernel, NT, smem));
+    if (occ < 1) return fail("hps_leaf_kernel does not fit on an SM");
+    if (want > occ * P->sms) want = occ * P->sms;
+  }
   // ordered after the plan's previous launch, whatever stream that was on
   if (P->last_recorded) CK(cudaStreamWaitEvent(stream, P->last, 0));
   const int slots = ensure_workspace(P, mode, want);
@@ -2750,14 +2795,8 @@ static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, c
     }
   }
   L.coeffs = coeffs; L.in0 = in0; L.in1 = in1; L.out0 = out0; L.out1 = out1; L.stats = stats;
-  const int panel_bytes = ((P->n_pad * P->wb > 1024 ? P->n_pad * P->wb : 1024) + 32 * P->wb) * 8;
-  int smem = GEMM_SMEM_BYTES;
-  if (panel_bytes > smem) smem = panel_bytes;
-  if ((2 * TRI_BLOCK * TRI_LD + 32 * TRI_BLOCK / 2) * 8 > smem) smem = (2 * TRI_BLOCK * TRI_LD + 32 * TRI_BLOCK / 2) * 8;
   L.smem_doubles = smem / 8;
   if (const char* dbg = getenv("HPS_DEBUG")) L.debug = atoi(dbg);
-  CK(cudaFuncSetAttribute(hps_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  CK(cudaFuncSetAttribute(hps_leaf_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   hps_leaf_kernel<<<slots, NT, smem, stream>>>(L, P->prog[mode], P->prog_len[mode], P->maps[mode]);
   CK(cudaGetLastError());
   CK(cudaEventRecord(P->last, stream));

@@ -115,25 +115,34 @@ def test_multi_rank_build_load_solve_match_single_process(tmp_path, world, monke
     assert np.linalg.norm(report.u - exact) / np.linalg.norm(exact) < 2e-3
 
 
-def test_flush_respects_memory_budget():
-    """The staged DtN blocks of a flush stay within memory_budget (the reference's
-    peak_workspace_bytes <= budget contract, condensation.py:255-263, 291)."""
+def test_flush_respects_budgets():
+    """Flushes of two device waves (2 x slots leaves), bounded by resident_limit and
+    by memory_budget for the host staging (the reference's peak_workspace_bytes <=
+    budget contract, condensation.py:255-263, 291); the results do not depend on it."""
     import hps_fakes as _fakes
     from paper_2503_04033_b200 import condensation
     saved = condensation._engine_for, condensation.DeviceAssembler
     try:
-        engines = _fakes.install()
+        engines = _fakes.install(slots=3)
         spec, disc = _problem()
         sched = _schedule(distributed=False)
         sys_ = condensation.build(disc, spec.coeffs, sched)
-        res = sched.resolve(disc.p, disc.d, disc.corner_mode)
-        assert sys_.peak_workspace_bytes <= sched.memory_budget
-        assert sys_.peak_workspace_bytes == 5 * res.block_bytes
-        assert engines[0].launches == -(-len(disc.leaves) // 5)   # ceil(12 / 5) flushes
-        # an explicit resident_limit bounds the flush further
-        sys2 = condensation.build(disc, spec.coeffs, _schedule(distributed=False, resident_limit=2))
-        assert sys2.peak_workspace_bytes == 2 * res.block_bytes
+        pack_bytes = 8 * 4 * 64                   # ncoef x n doubles per leaf
+        assert sys_.peak_workspace_bytes == 2 * 6 * pack_bytes <= sched.memory_budget
+        assert engines[-1].launches == 2          # 12 leaves, flushes of 2 x 3 slots
+        # (the reference's resolve() caps resident_limit by the budget: at most 3 maps here)
+        sys2 = condensation.build(disc, spec.coeffs, _schedule(distributed=False, resident_limit=3))
+        assert engines[-1].launches == 4 and sys2.peak_workspace_bytes == 2 * 3 * pack_bytes
         assert np.array_equal(sys2.t.data, sys_.t.data)
+        # a budget that holds the staging of only two leaves' packs bounds the flush to one leaf
+        tight = condensation.BatchSchedule(memory_budget=2 * pack_bytes + 8 * 64 ** 2 * 4, distributed=False)
+        with pytest.raises(condensation.ConfigError):
+            tight.resolve(disc.p, disc.d, disc.corner_mode)   # cannot hold one leaf workspace
+        res = _schedule().resolve(disc.p, disc.d, disc.corner_mode)
+        eng = engines[-1]
+        assert condensation._flush_size(res, eng, 12, device_staging=False) == 5  # 5.5 maps in budget
+        res.memory_budget = 3 * pack_bytes
+        assert condensation._flush_size(res, eng, 12, device_staging=True) == 1
     finally:
         condensation._engine_for, condensation.DeviceAssembler = saved
 

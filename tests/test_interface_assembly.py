@@ -152,11 +152,9 @@ def test_build_flushes_and_workspace_release():
     from paper_2503_04033_b200.condensation import build
     spec = make_problem("bump_helmholtz", d=3, kappa=20.0)
     disc = build_discretization(spec.domain, MeshConfig((3, 2, 2), 8))
-    one = build(disc, spec.coeffs, BatchSchedule(memory_budget=1 << 30))
-    tb = 8 * (6 * 36) ** 2
-    budget = 5 * tb + tb // 2      # 5 staged maps per flush: 12 leaves in 3 flushes
-    small = build(disc, spec.coeffs, BatchSchedule(memory_budget=budget))
-    assert small.peak_workspace_bytes <= budget < one.peak_workspace_bytes
+    one = build(disc, spec.coeffs, BatchSchedule())
+    small = build(disc, spec.coeffs, BatchSchedule(resident_limit=5))   # 12 leaves in 3 flushes
+    assert small.peak_workspace_bytes < one.peak_workspace_bytes <= BatchSchedule().memory_budget
     _same(small.t, one.t)
     _same(small.dirichlet_coupling, one.dirichlet_coupling)
     eng = small.engine
@@ -164,7 +162,7 @@ def test_build_flushes_and_workspace_release():
     assert held > 0 and slots >= 1 and small.device_workspace_bytes > 0
     eng.release()
     assert eng.workspace() == (0, 0)
-    again = build(disc, spec.coeffs, BatchSchedule(memory_budget=budget))
+    again = build(disc, spec.coeffs, BatchSchedule(resident_limit=5))
     _same(again.t, one.t)
 
 

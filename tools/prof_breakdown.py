@@ -21,13 +21,13 @@ def run():
     else:
         eng.reduce_load(coeffs, f)
 run(); torch.cuda.synchronize()
-cnt = torch.zeros(eng.slots * 32, dtype=torch.int64, device="cuda")
+cnt = torch.zeros(eng.slots * 48, dtype=torch.int64, device="cuda")
 eng.lib.hps_plan_set_profile(eng.plan, ctypes.c_void_p(cnt.data_ptr()))
 e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
 e0.record(); run(); e1.record(); torch.cuda.synchronize()
 eng.lib.hps_plan_set_profile(eng.plan, ctypes.c_void_p(0))
 ms = e0.elapsed_time(e1)
-c = cnt.view(eng.slots, 32).cpu().numpy().astype(float)
+c = cnt.view(eng.slots, 48).cpu().numpy().astype(float)
 names = ["small-panel", "swaps", "inv-lower", "inv-upper", "gemm-sub", "gemm-set", "gemm-set-Q", "gemm-sub-abi", "copy-abb"]
 tot = c[:, :9].sum() + c[:, 22].sum() + c[:, 23].sum() + c[:, 24].sum() + c[:, 27].sum()
 leaves = c[:, 9].sum()
@@ -66,3 +66,16 @@ order = np.argsort(sm)
 pair = per_leaf[order].reshape(-1, 2) if len(order) % 2 == 0 else None
 if pair is not None:
     print(f"  same-SM pair |difference| mean {np.abs(pair[:, 0] - pair[:, 1]).mean() / clk * 1e3:.1f} ms")
+ex = c[:, 32:35].sum()
+if ex > 0:   # HPS_PROF_EXEC build: DMMA flops actually issued
+    print(f"  executed DMMA flops/leaf {ex/leaves:.3e}")
+    for b, nm in enumerate(["N<=64", "N<=256", "N>256"]):
+        cyc, f = c[:, 16 + b].sum(), c[:, 32 + b].sum()
+        if cyc:
+            print(f"    gemm {nm:7s} executed {f/leaves:.2e} flop/leaf  {f/cyc*clk/1e9:6.1f} GF/s per CTA "
+                  f"({100*f/cyc*clk/1e9/125.3:.0f}% of the 37.1/296 fair share)")
+    for i, nm in enumerate(["LU", "forward solve", "W blocks / backward"]):
+        cyc, f = c[:, 38 + i].sum(), c[:, 35 + i].sum()
+        if cyc:
+            print(f"    phase {nm:20s} gemm {cyc/leaves/clk*1e3:7.2f} ms/leaf, executed {f/leaves:.2e} flop/leaf, "
+                  f"{f/cyc*clk/1e9:6.1f} GF/s per CTA; whole phase {c[:, 28 + i].sum()/leaves/clk*1e3:.1f} ms/leaf")

@@ -60,6 +60,14 @@ constexpr int KC = HPS_KC;       // k-chunk per pipeline stage
 #endif
 constexpr int STAGES = HPS_STAGES;
 constexpr int EPI_SLOTS = HPS_EPI_SLOTS;
+// Epilogue of C -= A B.  0: -acc staged in a per-warp smem ring and added in L2 by TMA
+// reduce-add (each warp waits for the previous block to be read out of smem);
+// 1: fire-and-forget f64 reductions in L2 (red.global.add.f64) straight from the
+// accumulators — no smem ring, no waits (the same IEEE round-to-nearest add).
+#ifndef HPS_EPI_RED
+#define HPS_EPI_RED 0
+#endif
+constexpr bool EPI_RED = HPS_EPI_RED != 0;
 // Operand boxes.  Padded boxes (A 20, B 132 doubles per row; the extra
 // columns are just neighbouring data) give bank-conflict-free m8n8k4 fragment
 // loads; the alternative is a 128B-swizzled 16-column A box / unpadded B box.
@@ -82,7 +90,7 @@ constexpr int WM = WARPS / WN;        // warps along M
 constexpr int MI = TM / WM / 8;       // 8-row m-tiles per warp
 constexpr int NJ = TN / WN / 8;       // 8-col n-tiles per warp (4)
 static_assert(MI * 8 * WM == TM && NJ == 4, "warp tiling");
-constexpr int EPI_DBL = EPI_SLOTS * 2 * 8 * 16;  // per warp: ring slots x two [8][16] blocks
+constexpr int EPI_DBL = EPI_RED ? 0 : EPI_SLOTS * 2 * 8 * 16;  // per warp: ring slots x two [8][16] blocks
 constexpr int WIDE_SMEM_BYTES = (STAGES * STAGE_DBL + (NT / 32) * EPI_DBL) * 8;
 constexpr int TRI_BLOCK = 64;    // triangular base block (explicit inverse + GEMM)
 #ifndef HPS_SMALL_PANEL
@@ -193,6 +201,9 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
 }
+__device__ __forceinline__ void red_add_f64(double* p, double v) {
+  asm volatile("red.global.add.f64 [%0], %1;\n" ::"l"(p), "d"(v) : "memory");
+}
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c[0]), "+d"(c[1])
@@ -300,7 +311,7 @@ struct GemmWide {
 };
 struct GemmNarrow {
   // k-chunk 8 (row stride 12) with a 3-stage ring; 4 (stride 4) with deeper rings
-  static constexpr int TM_ = 256, TN_ = 32, KC_ = STAGES <= 3 ? 8 : 4, AS = KC_ == 8 ? 12 : 4;
+  static constexpr int TM_ = 256, TN_ = 32, KC_ = (STAGES <= 3 || EPI_RED) ? 8 : 4, AS = KC_ == 8 ? 12 : 4;
   static constexpr int BS = 36, WN_ = 1, KIND = 1;
   static constexpr bool SWZ = false;
 };
@@ -357,6 +368,7 @@ struct Ctx {
 };
 #if HPS_PROF_EXEC
 __shared__ unsigned long long s_exec_dmma;  // DMMAs issued by this CTA's warps in the current op
+__shared__ unsigned long long s_exec_cap;   // DMMA slots of the chunks the CTA walked (8 warps x tile)
 #endif
 
 // ---------------------------------------------------------------------------
@@ -379,6 +391,7 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   constexpr int TM = G::TM_, TN = G::TN_, KC = G::KC_, A_STRIDE = G::AS, B_STRIDE = G::BS;
   constexpr int WN = G::WN_, MI = S::MI_, NJ = S::NJ_, STAGE_A = S::SA, STAGE_DBL = S::SDBL;
   constexpr bool narrow = (G::KIND == 1);
+  constexpr int WARPS_ = NT / 32;
   if (M <= 0 || N <= 0 || K <= 0) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wm = warp / WN, wn = warp % WN;
@@ -579,6 +592,9 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
       in_tile = true;
       set_valid(tile);
     }
+#if HPS_PROF_EXEC
+    if (c.prof && tid == 0) s_exec_cap += (unsigned long long)(WARPS_ * MI * NJ * (KC / 4));
+#endif
     const double* sa = smem + s * STAGE_DBL;
     const double* sb = sa + STAGE_A;
     auto mainloop = [&](auto edge) {
@@ -628,6 +644,24 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
       in_tile = false;
       const int tm = tile / tiles_n, tn = tile - tm * tiles_n;
       ++my_tiles;
+      if (sub && EPI_RED) {
+        // C -= acc as f64 reductions in L2, issued straight from the accumulators
+#pragma unroll
+        for (int i = 0; i < MI; ++i) {
+          const int row = tm * TM + wm * (MI * 8) + i * 8 + lr;
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) {
+            const int col = tn * TN + wn * (NJ * 8) + j * 8 + 2 * lc;
+            if (row < M && col < N) {
+              double* cp = C + (size_t)row * c.ld + col;
+              red_add_f64(cp, -acc[i][j][0]);
+              red_add_f64(cp + 1, -acc[i][j][1]);
+            }
+            acc[i][j][0] = acc[i][j][1] = 0.0;
+          }
+        }
+        continue;
+      }
       if (sub) {
         // C -= acc through TMA reduce-add in L2: -acc goes to a per-warp smem ring
         // (two [8][16] blocks per m-tile) and drains asynchronously.
@@ -688,10 +722,11 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
 #if HPS_PROF_EXEC
   if (c.prof && lane == 0) atomicAdd(&s_exec_dmma, my_dmma);
 #endif
-  if (sub && lane == 0) {
+  if (sub && !EPI_RED && lane == 0) {
     bulk_wait_all();
     fence_proxy_async_global();
   }
+  if (sub && EPI_RED) fence_proxy_async_global();  // this thread's reductions before later TMA reads
   if (gmode != 0) {  // shared op: count the tiles done here; the owner waits for all
     __threadfence();
     __syncthreads();
@@ -2017,6 +2052,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 #if HPS_PROF_EXEC
     s_exec_dmma = 0;
+    s_exec_cap = 0;
 #endif
   }
   __syncthreads();
@@ -2133,11 +2169,14 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
         if (op.kind == OP_GEMM_SUB || op.kind == OP_GEMM_SET || op.kind == OP_GEMM_SET_Q ||
             op.kind == OP_GEMM_SUB_ABI || op.kind == OP_GEMM_SET_R) {
           const unsigned long long f = s_exec_dmma * 512ull;  // flops per m8n8k4 DMMA
-          prof[32 + (op.Ndim <= 64 ? 0 : (op.Ndim <= 256 ? 1 : 2))] += f;
+          const int bk = op.Ndim <= 64 ? 0 : (op.Ndim <= 256 ? 1 : 2);
+          prof[32 + bk] += f;
           prof[35 + phase] += f;
           prof[38 + phase] += dt;
+          prof[41 + bk] += s_exec_cap * 512ull;  // capacity of the walked chunks
         }
         s_exec_dmma = 0;
+        s_exec_cap = 0;
 #endif
         const int pk = op.kind < OP_RHS_PROFILE ? op.kind
                        : (op.kind == OP_RHS_PROFILE ? 24

@@ -72,8 +72,11 @@ if ex > 0:   # HPS_PROF_EXEC build: DMMA flops actually issued
     for b, nm in enumerate(["N<=64", "N<=256", "N>256"]):
         cyc, f = c[:, 16 + b].sum(), c[:, 32 + b].sum()
         if cyc:
+            cap = c[:, 41 + b].sum()
             print(f"    gemm {nm:7s} executed {f/leaves:.2e} flop/leaf  {f/cyc*clk/1e9:6.1f} GF/s per CTA "
-                  f"({100*f/cyc*clk/1e9/125.3:.0f}% of the 37.1/296 fair share)")
+                  f"({100*f/cyc*clk/1e9/125.3:.0f}% of the 37.1/296 fair share); warp-slot use "
+                  f"{100*f/max(cap, 1):.0f}% of the chunks walked, walked-chunk rate "
+                  f"{cap/cyc*clk/1e9:6.1f} GF/s per CTA")
     for i, nm in enumerate(["LU", "forward solve", "W blocks / backward"]):
         cyc, f = c[:, 38 + i].sum(), c[:, 35 + i].sum()
         if cyc:

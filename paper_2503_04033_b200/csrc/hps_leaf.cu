@@ -65,9 +65,12 @@ constexpr int EPI_SLOTS = HPS_EPI_SLOTS;
 // 1: fire-and-forget f64 reductions in L2 (red.global.add.f64) straight from the
 // accumulators — no smem ring, no waits (the same IEEE round-to-nearest add).
 #ifndef HPS_EPI_RED
-#define HPS_EPI_RED 0
+#define HPS_EPI_RED 1
 #endif
 constexpr bool EPI_RED = HPS_EPI_RED != 0;
+#ifndef HPS_WARP_SWIZZLE
+#define HPS_WARP_SWIZZLE 1
+#endif
 // Operand boxes.  Padded boxes (A 20, B 132 doubles per row; the extra
 // columns are just neighbouring data) give bank-conflict-free m8n8k4 fragment
 // loads; the alternative is a 128B-swizzled 16-column A box / unpadded B box.
@@ -394,7 +397,16 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   constexpr int WARPS_ = NT / 32;
   if (M <= 0 || N <= 0 || K <= 0) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int wm = warp / WN, wn = warp % WN;
+  // warp -> (row block wm, column block wn).  The warps of an SM sub-partition are
+  // warp and warp + 4; with HPS_WARP_SWIZZLE the second row of warps is rotated by
+  // WN / 2 columns, so each sub-partition holds an early and a late column block
+  // (columns are sorted by their first nonzero row: the per-warp k bounds leave
+  // late blocks idle in early chunks) instead of two warps of the same column.
+  // (tall 4 x 2 warp grids: the second half of the warps takes the other column
+  // block and the row blocks two further on)
+  const int wm = (!HPS_WARP_SWIZZLE || WN != 2) ? warp / WN : (warp < 4 ? warp : (warp - 2) % 4);
+  const int wn = !HPS_WARP_SWIZZLE ? warp % WN
+                 : (WN == 2 ? warp / 4 : (warp % WN + wm * (WN / 2)) % WN);
   const int lr = lane >> 2, lc = lane & 3;
   const int tiles_n = (N + TN - 1) / TN;
   const int tiles = ((M + TM - 1) / TM) * tiles_n;
@@ -2569,6 +2581,9 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+#ifndef HPS_L2_PROMO
+#define HPS_L2_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
 static int make_map(CUtensorMap* map, double* base, uint64_t cols, uint64_t rows, uint64_t slots,
                     uint64_t ld, uint64_t slot_stride, uint32_t box_cols, uint32_t box_rows,
                     bool swizzle128 = false) {
@@ -2581,7 +2596,7 @@ static int make_map(CUtensorMap* map, double* base, uint64_t cols, uint64_t rows
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE,
                   swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  HPS_L2_PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return 0;
 }

@@ -1,0 +1,12 @@
+# round 2: ncu evidence for the current kernel: launch list of the default bench, full capture at p=16 and p=20
+O=gpurun_out/${OUT:-r2l}; mkdir -p $O
+C16="python bench.py --leaves 296 --steps 1 --warmup 3 --no-e2e --no-cpu --configs3-steps 0"
+C20="python bench.py --p 20 --kappa 80 --leaves 296 --steps 1 --warmup 3 --no-e2e --no-cpu --configs3-steps 0"
+CL="python bench.py --steps 2 --warmup 3 --no-cpu --configs3-steps 2"
+$CL > $O/plain_launch.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches.csv $CL > $O/ncu_launch.log 2>&1
+$C16 > $O/plain16.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:hps_leaf_kernel -s 3 -c 1 -o $O/full16 $C16 > $O/ncu_full16.log 2>&1
+$C20 > $O/plain20.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:hps_leaf_kernel -s 3 -c 1 -o $O/full20 $C20 > $O/ncu_full20.log 2>&1
+ls -la $O

@@ -867,6 +867,9 @@ __shared__ double s_rowj[2][8];
 // compacted pivot candidates: the 16-row groups after the block's own group that
 // have a structural nonzero in the panel
 constexpr int MAXG = 768;
+#ifndef HPS_PANEL_COMPACT_WB
+#define HPS_PANEL_COMPACT_WB 1  // panel block width from the compacted candidate count
+#endif
 __shared__ int s_glist[MAXG];
 __shared__ int s_ng;
 
@@ -913,7 +916,7 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
   double* S = c.smem;                          // column-major [WB][n_cand]: S[j * NS + r]
   const int NS = n_cand;
   // staging T (<= 32 x 32) and Q (<= 16 x 32) alias S; Ut sits after all of them
-  double* Ut = c.smem + (size_t)max(n_full * WB, 1024);  // WB x 32, Ut[j*32 + kk]
+  double* Ut = c.smem + (size_t)max(n_cand * WB, 1024);  // WB x 32, Ut[j*32 + kk]
   unsigned long long* prof = c.prof;
   long long tp = (prof && tid == 0) ? clock64() : 0;
 #define PANEL_TICK(slot)                                   \
@@ -1248,9 +1251,38 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
 // candidate set shrinks (the smem block holds n_cand x WB doubles).
 __device__ void lu_small(Ctx& c, int c0, int w) {
   int wb = c.wb;
+  // candidate rows of the panel's first block (the most of any block: later blocks see
+  // a subset of these groups — an interchange only lowers the bound of a group that
+  // already holds a candidate, or of the head group): the compacted count of
+  // panel_block, so panels whose rows are mostly structurally zero get wider blocks
+  int n_cand = c.n_piv - c0;
+  if (HPS_PANEL_COMPACT_WB && c.gpos != nullptr && ((c.n_piv + 15) >> 4) - (c0 >> 4) <= MAXG) {
+    __shared__ int s_ncg;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x, g_end = (c.n_piv + 15) >> 4;
+      int cnt = 0, last = -1;
+      for (int g0 = (c0 >> 4) + 1; g0 < g_end; g0 += 32) {
+        const int g = g0 + lane;
+        const bool act = g < g_end && c.gmin16[g] < c0 + w;
+        const unsigned bal = __ballot_sync(0xffffffffu, act);
+        cnt += __popc(bal);
+        if (bal) last = g0 + 31 - __clz(bal);
+      }
+      if (lane == 0) {
+        int nc = min(16 - (c0 & 15), c.n_piv - c0) + 16 * cnt;
+        if (cnt > 0 && (c.n_piv & 15) && last == ((c.n_piv - 1) >> 4)) nc -= 16 - (c.n_piv & 15);
+        s_ncg = nc;
+      }
+    }
+    __syncthreads();
+    // + 16: a later block's head group (rows b0 .. the end of b0's group) is counted
+    // whole even when that group held no candidate for the first block
+    n_cand = min(s_ncg + 16, c.n_piv - c0);
+  }
   // panel block smem: max(n_cand * WB, 1024) doubles (S and the staging it hosts) + 32 * WB (Ut)
   auto fits = [&](int W) {
-    const int sz = (c.n_piv - c0) * W;
+    const int sz = n_cand * W;
     return (sz > 1024 ? sz : 1024) + 32 * W <= c.smem_doubles;
   };
   while (wb < 8 && w % (2 * wb) == 0 && fits(2 * wb)) wb *= 2;

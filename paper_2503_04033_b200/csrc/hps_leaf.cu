@@ -68,6 +68,12 @@ constexpr int EPI_SLOTS = HPS_EPI_SLOTS;
 #define HPS_EPI_RED 1
 #endif
 constexpr bool EPI_RED = HPS_EPI_RED != 0;
+// Skip the DMMAs of 8 x 8 sub-blocks whose rows or columns are structurally zero over
+// the whole k chunk (per-row first nonzero gpos / wf, per-8-column bounds), on top of
+// the per-warp chunk skipping: exact zeros, so the results are unchanged.
+#ifndef HPS_SUB_SKIP
+#define HPS_SUB_SKIP 0
+#endif
 #ifndef HPS_WARP_SWIZZLE
 #define HPS_WARP_SWIZZLE 1
 #endif
@@ -369,6 +375,9 @@ struct Ctx {
   const int* leaf_counter;
   int n_leaves;
 };
+// per warp: first k (relative to the GEMM's k origin) of each 8-row group and each
+// 8-column group of the warp's 32 x 32 block in the current tile (HPS_SUB_SKIP)
+__shared__ int s_sub[NT / 32][8];
 #if HPS_PROF_EXEC
 __shared__ unsigned long long s_exec_dmma;  // DMMAs issued by this CTA's warps in the current op
 __shared__ unsigned long long s_exec_cap;   // DMMA slots of the chunks the CTA walked (8 warps x tile)
@@ -558,6 +567,10 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   // first k this warp's part of the tile needs: the kmode bounds of the tile,
   // taken over the warp's own rows (A) and columns (B)
   int wk = 0;
+  // 8 x 8 sub-blocks (i * NJ + j) with work in the current chunk; the starts only
+  // grow with k, so once every in-range sub-block is active the mask is final for the tile
+  unsigned sub_mask = 0xffffu, sub_final = 0xffffu;
+  bool sub_done = false;
   auto set_valid = [&](int t) {
     const int tm = t / tiles_n, tn = t - tm * tiles_n;
     const int rows = M - (tm * TM + wm * (MI * 8)), cols = N - (tn * TN + wn * (NJ * 8));
@@ -585,6 +598,39 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
         for (int cq = bc + c0w; cq < bc + c1w; cq += 16) gm = min(gm, c.gcol16[cq >> 4]);
         wk = max(wk, gm - br);
       }
+    }
+    sub_final = 0;
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+      if (i < mv) sub_final |= ((1u << nv) - 1u) << (i * NJ);
+    sub_done = !HPS_SUB_SKIP;
+    sub_mask = sub_final;
+    if (HPS_SUB_SKIP) {
+      // rows: lane l holds row r0 + l's first k, min over each 8-row group
+      const int r0 = ar + tm * TM + wm * (MI * 8);
+      const int r = r0 + lane;
+      int f = 0;
+      if (r >= ar + M) {
+        f = 0x7fffffff;
+      } else {
+        if (kmode & 2) f = max(f, c.wf[r - c.n_piv] - ac);
+        if (kmode & 4) f = max(f, c.gpos[r] - ac);
+      }
+#pragma unroll
+      for (int off = 1; off < 8; off <<= 1) f = min(f, __shfl_xor_sync(0xffffffffu, f, off));
+      if (lane < MI * 8 && (lane & 7) == 0) s_sub[warp][lane >> 3] = f;
+      if (lane < NJ) {  // columns: 8-column groups
+        const int cw = tn * TN + wn * (NJ * 8) + lane * 8;
+        int g = 0;
+        if (cw >= N) {
+          g = 0x7fffffff;
+        } else {
+          if (kmode & 1) g = max(g, c.rhs_g[cw] - br);
+          if (kmode & 8) g = max(g, min(c.gcol16[-1], c.gcol16[(bc + cw) >> 4]) - br);
+        }
+        s_sub[warp][4 + lane] = g;
+      }
+      __syncwarp();
     }
   };
   for (;; ++it) {
@@ -629,7 +675,7 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
         for (int i = 0; i < MI; ++i)
 #pragma unroll
           for (int j = 0; j < NJ; ++j)
-            if (!decltype(edge)::value || (i < mv && j < nv)) dmma(acc[i][j], af[i], bf[j]);
+            if (!decltype(edge)::value || ((sub_mask >> (i * NJ + j)) & 1u)) dmma(acc[i][j], af[i], bf[j]);
       }
     };
     // triangular operands (explicit inverses): chunks whose part of this warp's
@@ -643,11 +689,25 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
       const int c_hi = tn * TN + wn * (NJ * 8) + NJ * 8 - 1;
       zero_chunk = zero_chunk || (tri == 1 && k_lo > r_hi) || (tri == 3 && k_hi < r_lo) || (tri == 2 && k_lo > c_hi);
     }
-    if (!zero_chunk) {
-      if (mv == MI && nv == NJ) mainloop(std::false_type{});
-      else if (mv > 0 && nv > 0) mainloop(std::true_type{});
+    if (!zero_chunk && mv > 0 && nv > 0) {
+      if (!sub_done) {
+        const int kend = kc * KC + KC;
+        unsigned ra = 0, ca = 0;
+#pragma unroll
+        for (int i = 0; i < MI; ++i) ra |= (kend > s_sub[warp][i] ? 1u : 0u) << i;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) ca |= (kend > s_sub[warp][4 + j] ? 1u : 0u) << j;
+        sub_mask = 0;
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+          if ((ra >> i) & 1u) sub_mask |= ca << (i * NJ);
+        sub_mask &= sub_final;
+        sub_done = sub_mask == sub_final;
+      }
+      if (sub_mask == 0xffffu) mainloop(std::false_type{});
+      else if (sub_mask) mainloop(std::true_type{});
 #if HPS_PROF_EXEC
-      my_dmma += (unsigned long long)(mv * nv * (KC / 4));
+      my_dmma += (unsigned long long)(__popc(sub_mask) * (KC / 4));
 #endif
     }
     __syncwarp();

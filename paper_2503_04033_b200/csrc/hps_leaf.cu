@@ -1,7 +1,8 @@
 // B200 (sm_100a) leaf-box reduction engine for the two-level HPS solver.
 //
-// One persistent CTA per SM owns one "slot" of HBM workspace and processes leaf
-// boxes one after another (static stride over the batch).  For each leaf the CTA
+// A persistent grid of two CTAs per SM; each CTA owns one "slot" of HBM workspace and
+// reduces leaf boxes one after another (next leaf from a global counter).  For each leaf
+// the CTA
 //   1. assembles the padded augmented collocation matrix
 //          M = [ A_ii  A_ib ]      (DtN mode,  NR = NC = n_pad + m_pad)
 //              [ A_bi  A_bb ]
@@ -11,18 +12,18 @@
 //   2. factors the first n_pad columns with partial pivoting restricted to the
 //      interior rows (recursive right-looking LU; reference: local_ops.py:422-436
 //      uses LAPACK getrf on A_ii),
-//   3. DtN mode: forms T = A_bb - A_bi A_ii^{-1} A_ib as the Schur complement
-//      left in the bottom-right block (reference: local_ops.py:439-446,
+//   3. DtN mode: forms T = A_bb - A_bi A_ii^{-1} A_ib block by block as
+//      A_bb - (A_bi U^-1)(L^-1 P A_ib) (reference: local_ops.py:439-446,
 //      dtn = a_bb + a_bi @ (-A_ii^{-1} a_ib));
 //      solve mode: forward/back substitution of the rhs column
 //      (reference: condensation.py:314-323 and 372-383).
 //
 // All O(n^3) work runs in one FP64 tensor-core GEMM engine (mma.sync m8n8k4 f64
-// -> SASS DMMA), 128x128 CTA tiles, 8 warps of 64x32, a 4-stage cp.async
-// pipeline that flows across tile boundaries, and an L2 prefetch of the C tile
-// ahead of its epilogue.  Pivot search, the narrow panel and triangular-block
-// inversions run on the same CTA between GEMMs; other SMs keep their tensor
-// pipes busy with their own leaves, so there is no grid-wide synchronisation.
+// -> SASS DMMA): 64 x 128 CTA tiles of 8 warps (32 x 32 each), operands staged by
+// TMA in a 2-stage ring of 32-deep k chunks with mbarriers, epilogue as f64
+// reductions in L2.  Pivot search, the narrow panels and the triangular-block
+// inversions run on the same CTA between GEMMs; the other CTA of the SM keeps the
+// tensor pipe busy with its own leaf, so there is no grid-wide synchronisation.
 
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -49,11 +50,11 @@ constexpr int CTAS_PER_SM = 2;
 constexpr int TM = 64;           // GEMM tile rows (1 x 4 warps of 64 x 32)
 constexpr int TN = 128;          // GEMM tile cols
 #ifndef HPS_KC
-#define HPS_KC 16
+#define HPS_KC 32
 #endif
 constexpr int KC = HPS_KC;       // k-chunk per pipeline stage
 #ifndef HPS_STAGES
-#define HPS_STAGES 3
+#define HPS_STAGES 2
 #endif
 #ifndef HPS_EPI_SLOTS
 #define HPS_EPI_SLOTS 1
@@ -134,6 +135,30 @@ constexpr int SHARE_MIN_TILES = 16;
 #define HPS_PF 0  // GEMM operand L2 prefetch distance in k chunks (0: off)
 #endif
 constexpr int PF_DIST = HPS_PF;
+// C tile L2 prefetch issued HPS_CPF k chunks before the tile's last chunk (0: with the
+// first chunk).  A long tile outlives L2 residency (K = 1376: ~180 us per tile while L2
+// turns over every ~35 us), so a prefetch at the start is evicted before the epilogue's
+// reductions, which then fetch C from DRAM a second time.
+#ifndef HPS_CPF
+#define HPS_CPF 2
+#endif
+// Serpentine k order: odd tiles walk their k chunks backwards, so a tile starts on the
+// operand chunks its predecessor (same 64-row A panel) read last, while they are in L2.
+#ifndef HPS_KREV
+#define HPS_KREV 0
+#endif
+// The TMA producer is lane 0 of this warp.  Issuing a chunk costs the producer ~500
+// cycles of its own DMMA issue; warp 5 holds the tile's last-starting 32 x 32 block (wide
+// tiles: row block 1, column block 3; tall tiles: row block 3, column block 1), so in
+// ragged tiles it issues while it has no DMMAs of its own.
+#ifndef HPS_PRODUCER_WARP
+#define HPS_PRODUCER_WARP 0
+#endif
+constexpr int PRODUCER_TID = 32 * HPS_PRODUCER_WARP;
+// L2 eviction hints on the operand loads: bit 1 A evict_last, bit 2 B evict_first
+#ifndef HPS_L2HINT
+#define HPS_L2HINT 2
+#endif
 #ifndef HPS_RW
 #define HPS_RW 256  // W-trick block of sorted boundary DOFs (rows below A_ii)
 #endif
@@ -213,8 +238,16 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 __device__ __forceinline__ void red_add_f64(double* p, double v) {
   asm volatile("red.global.add.f64 [%0], %1;\n" ::"l"(p), "d"(v) : "memory");
 }
+#ifndef HPS_DMMA_NV
+#define HPS_DMMA_NV 0  // 1: the DMMA asm is not volatile (the compiler may schedule around it)
+#endif
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+#if HPS_DMMA_NV
+  asm(
+#else
+  asm volatile(
+#endif
+"mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
 }
@@ -244,6 +277,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
+#ifdef HPS_TRACE  // probe: per-warp chunk timeline of CTA 0 (wait start, data ready, chunk done)
+__device__ long long g_trace[NT / 32][HPS_TRACE][3];
+__device__ long long g_trace_prod[HPS_TRACE][4];
+#endif
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
                                             uint64_t* bar) {
   asm volatile(
@@ -251,6 +288,25 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
+}
+// the same load with an L2 eviction-priority hint (createpolicy cache policy)
+__device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                 uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
 }
 __device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
   asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(
@@ -319,8 +375,10 @@ struct GemmWide {
   static constexpr bool SWZ = !A_PAD;
 };
 struct GemmNarrow {
-  // k-chunk 8 (row stride 12) with a 3-stage ring; 4 (stride 4) with deeper rings
-  static constexpr int TM_ = 256, TN_ = 32, KC_ = (STAGES <= 3 || EPI_RED) ? 8 : 4, AS = KC_ == 8 ? 12 : 4;
+  // k-chunk 16 (row stride 20) with the 32-wide chunks of the wide tiles, else 8 (row
+  // stride 12) with a 3-stage ring, 4 (stride 4) with deeper rings
+  static constexpr int TM_ = 256, TN_ = 32, KC_ = KC >= 32 ? 16 : ((STAGES <= 3 || EPI_RED) ? 8 : 4);
+  static constexpr int AS = KC_ == 16 ? 20 : (KC_ == 8 ? 12 : 4);
   static constexpr int BS = 36, WN_ = 1, KIND = 1;
   static constexpr bool SWZ = false;
 };
@@ -328,7 +386,8 @@ struct GemmNarrow {
 // right inverses (N = 64, in place: one tile column, so no tile reads columns
 // another tile already wrote).
 struct GemmTall {
-  static constexpr int TM_ = 128, TN_ = 64, KC_ = 8, AS = 12, BS = 68, WN_ = 2, KIND = 2;
+  static constexpr int TM_ = 128, TN_ = 64, KC_ = KC >= 32 ? 16 : 8, AS = KC_ == 16 ? 20 : 12, BS = 68, WN_ = 2,
+                       KIND = 2;
   static constexpr bool SWZ = false;
 };
 template <class G>
@@ -419,7 +478,7 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   const int lr = lane >> 2, lc = lane & 3;
   const int tiles_n = (N + TN - 1) / TN;
   const int tiles = ((M + TM - 1) / TM) * tiles_n;
-  const int kchunks = K / KC;
+  const int kchunks = (K + KC - 1) / KC;  // K is a multiple of 16; the last chunk may be partial
   double* smem = c.smem;
   const CUtensorMap* mapA = narrow ? &c.maps->a_work_n
                            : G::KIND == 2 ? &c.maps->a_work_t
@@ -460,7 +519,7 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   const int gmode = s_gmode;
 
   // producer state (thread 0 only)
-  int p_it = 0, p_tile = 0, p_kc = 0, p_next = 0, p_skipped = 0;
+  int p_it = 0, p_tile = 0, p_kc = 0, p_next = 0, p_skipped = 0, p_k0 = 0, p_j = 0;
   bool p_end = false, p_in = false;
   auto claim_tile = [&]() -> int {
     if (gmode == 0) return p_next < tiles ? p_next++ : -1;
@@ -477,11 +536,20 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
       old = prev;
     }
   };
+  // the next chunk into its stage, once every warp has released the stage's last use
   auto produce = [&]() {
     if (p_end) return;
     const unsigned g = c.pipe + p_it;
     const unsigned s = g % STAGES, use = g / STAGES;
-    if (use > 0) mbar_wait(&c.empty[s], (use - 1) & 1);
+    if (use > 0) {
+#ifdef HPS_TRACE
+      if (blockIdx.x == 0 && g < HPS_TRACE) g_trace_prod[g][0] = clock64();
+#endif
+      mbar_wait(&c.empty[s], (use - 1) & 1);
+#ifdef HPS_TRACE
+      if (blockIdx.x == 0 && g < HPS_TRACE) g_trace_prod[g][1] = clock64();
+#endif
+    }
     const bool first_chunk = !p_in;
     if (!p_in) {
       for (;;) {
@@ -515,6 +583,9 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
         p_kc = k0 > kchunks - 1 ? kchunks - 1 : k0;
         break;
       }
+      p_k0 = p_kc;
+      p_j = 0;
+      if (HPS_KREV && (p_tile & 1)) p_kc = kchunks - 1;
       s_tile_ring[s] = p_tile;
       if (p_tile < 0) {  // end marker: a stage with no data
         p_end = true;
@@ -522,20 +593,38 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
         ++p_it;
         return;
       }
-      s_kc0_ring[s] = p_kc;
+      s_kc0_ring[s] = p_k0;
       p_in = true;
     }
     const int tm = p_tile / tiles_n, tn = p_tile - tm * tiles_n;
     double* sa = smem + s * STAGE_DBL;
     double* sb = sa + STAGE_A;
+#ifdef HPS_TRACE
+    if (blockIdx.x == 0 && g < HPS_TRACE) g_trace_prod[g][2] = clock64();
+#endif
+#ifdef HPS_TEST_NOTMA  // probe: no operand transfer (stale stage data), the ring protocol alone
+    (void)sa; (void)sb; (void)tm; (void)tn;
+    mbar_arrive(&c.full[s]);
+#else
     mbar_expect_tx(&c.full[s], S::BYTES);
+#if HPS_L2HINT
+    // the A panel of a tile row is read again by the row's next tile: keep it; the B
+    // panel is not reused before it would be evicted anyway
+    if (HPS_L2HINT & 1) tma_load_3d_hint(sa, mapA, ac + p_kc * KC, ar + tm * TM, a_slot, &c.full[s], policy_evict_last());
+    else tma_load_3d(sa, mapA, ac + p_kc * KC, ar + tm * TM, a_slot, &c.full[s]);
+    if (HPS_L2HINT & 2) tma_load_3d_hint(sb, mapB, bc + tn * TN, br + p_kc * KC, b_slot, &c.full[s], policy_evict_first());
+    else tma_load_3d(sb, mapB, bc + tn * TN, br + p_kc * KC, b_slot, &c.full[s]);
+#else
     tma_load_3d(sa, mapA, ac + p_kc * KC, ar + tm * TM, a_slot, &c.full[s]);
     tma_load_3d(sb, mapB, bc + tn * TN, br + p_kc * KC, b_slot, &c.full[s]);
+#endif
+#endif
     if (PF_DIST > 0 && p_kc + PF_DIST < kchunks) {  // operand chunks further ahead into L2
       tma_prefetch_3d(mapA, ac + (p_kc + PF_DIST) * KC, ar + tm * TM, a_slot);
       tma_prefetch_3d(mapB, bc + tn * TN, br + (p_kc + PF_DIST) * KC, b_slot);
     }
-    if (sub && first_chunk) {  // C tile into L2 ahead of the reduce-add epilogue
+    if (sub && (HPS_CPF == 0 ? first_chunk : p_j == max(0, kchunks - p_k0 - HPS_CPF))) {
+      // C tile into L2 ahead of the reduce-add epilogue
       if (narrow) {
         for (int r = 0; r < TM; r += 8) tma_prefetch_3d(&c.maps->b_work_n, cc + tn * TN, cr + tm * TM + r, c.slot);
       } else {
@@ -543,10 +632,16 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
           tma_prefetch_3d(&c.maps->b_work, cc + tn * TN, cr + tm * TM + r, c.slot);
       }
     }
+#ifdef HPS_TRACE
+    if (blockIdx.x == 0 && g < HPS_TRACE) g_trace_prod[g][3] = clock64();
+#endif
     ++p_it;
-    if (++p_kc == kchunks) p_in = false;
+    ++p_j;
+    if (HPS_KREV && (p_tile & 1)) --p_kc;
+    else ++p_kc;
+    if (p_j == kchunks - p_k0) p_in = false;
   };
-  if (tid == 0) {
+  if (tid == PRODUCER_TID) {
     for (int s = 0; s < STAGES - 1; ++s) produce();
   }
 
@@ -556,8 +651,8 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
 #pragma unroll
     for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  int tile = 0, kc = 0, it = 0, my_tiles = 0;
-  bool in_tile = false;
+  int tile = 0, kc = 0, it = 0, my_tiles = 0, kj = 0, kn = 0;
+  bool in_tile = false, krev = false;
 #if HPS_PROF_EXEC
   unsigned long long my_dmma = 0;
 #endif
@@ -634,10 +729,16 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     }
   };
   for (;; ++it) {
-    if (tid == 0) produce();
+    if (tid == PRODUCER_TID) produce();
     const unsigned g = c.pipe + it;
     const unsigned s = g % STAGES;
+#ifdef HPS_TRACE
+    const long long tr0 = clock64();
+#endif
     mbar_wait(&c.full[s], (g / STAGES) & 1);
+#ifdef HPS_TRACE
+    if (blockIdx.x == 0 && lane == 0 && g < HPS_TRACE) { g_trace[warp][g][0] = tr0; g_trace[warp][g][1] = clock64(); }
+#endif
     if (!in_tile) {
       tile = reinterpret_cast<volatile int*>(s_tile_ring)[s];
       if (tile < 0) {
@@ -647,6 +748,10 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
         break;
       }
       kc = reinterpret_cast<volatile int*>(s_kc0_ring)[s];
+      kn = kchunks - kc;  // chunks of this tile
+      kj = 0;
+      krev = HPS_KREV && (tile & 1);
+      if (krev) kc = kchunks - 1;
       in_tile = true;
       set_valid(tile);
     }
@@ -655,22 +760,44 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
 #endif
     const double* sa = smem + s * STAGE_DBL;
     const double* sb = sa + STAGE_A;
+    auto load_frags = [&](int ks, double (&af)[MI], double (&bf)[NJ]) {
+#pragma unroll
+      for (int i = 0; i < MI; ++i) {
+        const int row = wm * (MI * 8) + i * 8 + lr, k = ks + lc;
+        if (!G::SWZ) {
+          af[i] = sa[row * A_STRIDE + k];
+        } else {
+          // 128B swizzle: 16-byte chunk index ^= row % 8  (row % 8 == lr here)
+          af[i] = sa[row * A_STRIDE + ((((k >> 1) ^ lr) << 1) | (k & 1))];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) bf[j] = sb[(ks + lc) * B_STRIDE + wn * (NJ * 8) + j * 8 + lr];
+    };
+    // k-steps (4 k each) of this chunk the warp executes: [klo, khi).  The last chunk
+    // of a K that is not a multiple of KC is partial; steps whose rows / columns of
+    // this warp are zero (first nonzero wk, explicit-inverse triangles) are skipped.
+    constexpr int KS = KC / 4;
+    const int kbase = kc * KC;
+    int khi = min(KS, (K - kbase) >> 2);
+    int klo = wk > kbase ? (wk - kbase) >> 2 : 0;
+    if (tri) {
+      const int tm = tile / tiles_n, tn = tile - tm * tiles_n;
+      const int r_lo = tm * TM + wm * (MI * 8), r_hi = r_lo + MI * 8 - 1;
+      const int c_hi = tn * TN + wn * (NJ * 8) + NJ * 8 - 1;
+      if (tri == 1) khi = min(khi, r_hi >= kbase ? ((r_hi - kbase) >> 2) + 1 : 0);  // A lower: k <= row
+      else if (tri == 3) klo = max(klo, r_lo > kbase ? (r_lo - kbase) >> 2 : 0);    // A upper: k >= row
+      else if (tri == 2) khi = min(khi, c_hi >= kbase ? ((c_hi - kbase) >> 2) + 1 : 0);  // B upper: k <= col
+    }
+#ifdef HPS_TEST_IDLE  // probe: warps of the given mask do no DMMAs (is a lone warp per SMSP DMMA-limited?)
+    if ((HPS_TEST_IDLE >> warp) & 1) khi = 0;
+#endif
     auto mainloop = [&](auto edge) {
 #pragma unroll
-      for (int ks = 0; ks < KC; ks += 4) {
+      for (int t = 0; t < KS; ++t) {
+        if (t < klo || t >= khi) continue;
         double af[MI], bf[NJ];
-#pragma unroll
-        for (int i = 0; i < MI; ++i) {
-          const int row = wm * (MI * 8) + i * 8 + lr, k = ks + lc;
-          if (!G::SWZ) {
-            af[i] = sa[row * A_STRIDE + k];
-          } else {
-            // 128B swizzle: 16-byte chunk index ^= row % 8  (row % 8 == lr here)
-            af[i] = sa[row * A_STRIDE + ((((k >> 1) ^ lr) << 1) | (k & 1))];
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) bf[j] = sb[(ks + lc) * B_STRIDE + wn * (NJ * 8) + j * 8 + lr];
+        load_frags(4 * t, af, bf);
 #pragma unroll
         for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -678,20 +805,9 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
             if (!decltype(edge)::value || ((sub_mask >> (i * NJ + j)) & 1u)) dmma(acc[i][j], af[i], bf[j]);
       }
     };
-    // triangular operands (explicit inverses): chunks whose part of this warp's
-    // rows / columns lies entirely in the zero triangle are skipped
-    // rows of this warp that are zero over the whole chunk (first nonzero beyond it)
-    bool zero_chunk = kc * KC + KC <= wk;
-    if (tri) {
-      const int k_lo = kc * KC, k_hi = k_lo + KC - 1;
-      const int tm = tile / tiles_n, tn = tile - tm * tiles_n;
-      const int r_lo = tm * TM + wm * (MI * 8), r_hi = r_lo + MI * 8 - 1;
-      const int c_hi = tn * TN + wn * (NJ * 8) + NJ * 8 - 1;
-      zero_chunk = zero_chunk || (tri == 1 && k_lo > r_hi) || (tri == 3 && k_hi < r_lo) || (tri == 2 && k_lo > c_hi);
-    }
-    if (!zero_chunk && mv > 0 && nv > 0) {
+    if (klo < khi && mv > 0 && nv > 0) {
       if (!sub_done) {
-        const int kend = kc * KC + KC;
+        const int kend = kbase + KC;
         unsigned ra = 0, ca = 0;
 #pragma unroll
         for (int i = 0; i < MI; ++i) ra |= (kend > s_sub[warp][i] ? 1u : 0u) << i;
@@ -707,12 +823,16 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
       if (sub_mask == 0xffffu) mainloop(std::false_type{});
       else if (sub_mask) mainloop(std::true_type{});
 #if HPS_PROF_EXEC
-      my_dmma += (unsigned long long)(__popc(sub_mask) * (KC / 4));
+      my_dmma += (unsigned long long)(__popc(sub_mask) * (khi - klo));
 #endif
     }
     __syncwarp();
+#ifdef HPS_TRACE
+    if (blockIdx.x == 0 && lane == 0 && g < HPS_TRACE) g_trace[warp][g][2] = clock64();
+#endif
     if (lane == 0) mbar_arrive(&c.empty[s]);
-    if (++kc == kchunks) {
+    kc += krev ? -1 : 1;
+    if (++kj == kn) {
       in_tile = false;
       const int tm = tile / tiles_n, tn = tile - tm * tiles_n;
       ++my_tiles;
@@ -918,6 +1038,7 @@ __device__ void apply_swaps(const Ctx& c, int j0, int cnt, int c_lo, int c_hi) {
 // ---------------------------------------------------------------------------
 
 __shared__ int s_swp_dst[16], s_swp_src[16], s_swp_cnt;
+__shared__ int s_swp_rows[16], s_swp_cont[16];  // thread 0's scratch (no local-memory arrays)
 // pivot search state, parity-buffered by column: per-warp best |a| / row / row values,
 // and row j's values at the start of step j
 __shared__ double s_pv[2][NT / 32];
@@ -1261,7 +1382,9 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
   for (int j = 0; j < WB; ++j) any_swap |= c.piv[b0 + j] != b0 + j;
   if (tid == 0 && !any_swap) s_swp_cnt = 0;
   if (tid == 0 && any_swap) {
-    int rows[16], cont[16], cnt = 0;
+    int* rows = s_swp_rows;
+    int* cont = s_swp_cont;
+    int cnt = 0;
     for (int j = 0; j < WB; ++j) {
       const int cand[2] = {b0 + j, c.piv[b0 + j]};
       for (int t = 0; t < 2; ++t) {

@@ -3,7 +3,10 @@
 #include "../../paper_2503_04033_b200/csrc/hps_leaf.cu"
 
 namespace {
-__global__ void __launch_bounds__(NT, CTAS_PER_SM) gemm_probe(double* base, size_t stride, int ld, int M, int N,
+#ifndef GB_MINB
+#define GB_MINB CTAS_PER_SM  // minimum CTAs per SM in the probe's launch bounds (1: up to 255 registers)
+#endif
+__global__ void __launch_bounds__(NT, GB_MINB) gemm_probe(double* base, size_t stride, int ld, int M, int N,
                                                     int K, int reps, const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(1024) double smem[];
   __shared__ __align__(8) uint64_t bars[2 * STAGES];
@@ -12,12 +15,22 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) gemm_probe(double* base, size
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+#ifdef GB_PFTMAP
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.a_work)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.b_work)) : "memory");
+  }
+#endif
   Ctx c;
   c.M = base + (size_t)blockIdx.x * stride;
   c.ld = ld; c.slot = blockIdx.x; c.smem = smem; c.maps = &maps;
   c.full = bars; c.empty = bars + STAGES; c.pipe = 0; c.prof = nullptr;
   c.sh = nullptr; c.role = 0; c.seq = 0; c.cur_op = 0; c.leaf_counter = nullptr; c.n_leaves = 0;
+#ifdef GB_L2  // every CTA reads the same A and B (slot 0: L2-resident after first touch); C per CTA
+  for (int r = 0; r < reps; ++r) gemm(c, true, 2, 0, 0, 1, M, 0, M + K, 0, M, N, K);
+#else
   for (int r = 0; r < reps; ++r) gemm(c, true, 0, 0, 0, 0, M, 0, M + K, 0, M, N, K);
+#endif
 }
 }  // namespace
 
@@ -46,6 +59,8 @@ int main(int argc, char** argv) {
     make_map(&maps.a_work, buf, ld, NR, CTAS_PER_SM * sms, ld, stride, A_STRIDE, TM, !A_PAD);
     make_map(&maps.b_work, buf, ld, NR, CTAS_PER_SM * sms, ld, stride, B_STRIDE, KC);
     maps.a_scratch = maps.a_work;
+    maps.a_abi = maps.a_work;
+    maps.b_q = maps.b_work;
     make_map(&maps.c_red, buf, ld, NR, CTAS_PER_SM * sms, ld, stride, 16, 8);
     make_map(&maps.a_work_n, buf, ld, NR, CTAS_PER_SM * sms, ld, stride, GemmNarrow::AS, GemmNarrow::TM_);
     make_map(&maps.b_work_n, buf, ld, NR, CTAS_PER_SM * sms, ld, stride, GemmNarrow::BS, GemmNarrow::KC_);
@@ -63,6 +78,19 @@ int main(int argc, char** argv) {
     printf("M=%5d N=%5d K=%5d: %6.2f TFLOP/s useful, %6.2f tile-TFLOP/s (%.1f GF/s/SM useful) %s\n",
            s.M, s.N, s.K, fl * reps * cps * sms / ms / 1e9, tiles * reps * cps * sms / ms / 1e9,
            cps * fl * reps / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
+#ifdef HPS_TRACE
+    if (s.M == 2560) {  // timeline of CTA 0's first chunks (last launch), relative to its first wait
+      static long long tr[NT / 32][HPS_TRACE][3], tp[HPS_TRACE][4];
+      cudaMemcpyFromSymbol(tr, g_trace, sizeof(tr));
+      cudaMemcpyFromSymbol(tp, g_trace_prod, sizeof(tp));
+      const long long t0 = tr[0][0][0];
+      for (int g = 0; g < HPS_TRACE; ++g) {
+        printf("chunk %3d prod_wait %7lld..%7lld tma %7lld..%7lld |", g, tp[g][0] ? tp[g][0] - t0 : -1, tp[g][1] ? tp[g][1] - t0 : -1, tp[g][2] - t0, tp[g][3] - t0);
+        for (int w = 0; w < NT / 32; ++w) printf(" w%d %7lld %7lld %7lld", w, tr[w][g][0] - t0, tr[w][g][1] - t0, tr[w][g][2] - t0);
+        printf("\n");
+      }
+    }
+#endif
     cudaFree(buf);
   }
   return 0;

@@ -151,9 +151,13 @@ constexpr int PF_DIST = HPS_PF;
 // cycles of its own DMMA issue; warp 5 holds the tile's last-starting 32 x 32 block (wide
 // tiles: row block 1, column block 3; tall tiles: row block 3, column block 1), so in
 // ragged tiles it issues while it has no DMMAs of its own.
+// Only warp 0 works: the share protocol's sequence number (Ctx::seq) and op
+// publication live in thread 0, so a producer elsewhere deadlocks on shared ops
+// (HPS_PRODUCER_WARP=5 hung the bench, profiles/r02c_variant_sweep.jsonl).
 #ifndef HPS_PRODUCER_WARP
 #define HPS_PRODUCER_WARP 0
 #endif
+static_assert(HPS_PRODUCER_WARP == 0, "the TMA producer must be thread 0 (share protocol state)");
 constexpr int PRODUCER_TID = 32 * HPS_PRODUCER_WARP;
 // L2 eviction hints on the operand loads: bit 1 A evict_last, bit 2 B evict_first
 #ifndef HPS_L2HINT

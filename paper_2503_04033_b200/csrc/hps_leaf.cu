@@ -163,6 +163,17 @@ constexpr int PRODUCER_TID = 32 * HPS_PRODUCER_WARP;
 #ifndef HPS_L2HINT
 #define HPS_L2HINT 2
 #endif
+// Wide GEMMs as two independent 4-warp groups on 64 x 64 tiles (1) instead of all 8
+// warps on one 64 x 128 tile (0).  The per-warp k bounds are ragged mostly across
+// column blocks (a 64 x 128 tile walks its k range from its earliest column's start:
+// 86% of the walked warp slots carry DMMAs at p = 16; 92% for 64 x 64 tiles that
+// walk independently; tools/r03/sim_program.py).  Measured: -5% at p = 16, -7% at
+// p = 20 (twice the chunks per FLOP, lower operand reuse; profiles/r02c_variant_sweep.jsonl),
+// so it stays off.
+#ifndef HPS_HALF
+#define HPS_HALF 0
+#endif
+constexpr int HSTAGES = 2;  // ring depth of each group (16-deep k chunks)
 #ifndef HPS_RW
 #define HPS_RW 256  // W-trick block of sorted boundary DOFs (rows below A_ii)
 #endif
@@ -366,6 +377,10 @@ struct TmaMaps {
   CUtensorMap b_scratch_t;  // tall tiles: box {68, 8, 1} over the inverse cache
   CUtensorMap a_work_n;   // narrow tiles: box {12, 256, 1} over [slots][NR][NC]
   CUtensorMap b_work_n;   // narrow tiles: box {36, 8, 1}
+  CUtensorMap a_work_h;   // half tiles: box {20, 64, 1} over [slots][NR][NC]
+  CUtensorMap b_work_h;   // half tiles: box {68, 16, 1}
+  CUtensorMap a_scratch_h;  // half tiles: box {20, 64, 1} over the inverse cache
+  CUtensorMap b_scratch_h;  // half tiles: box {68, 16, 1} over the inverse cache
 };
 
 // GEMM tile configurations.  Wide: 64 x 128 tiles, 2 x 4 warps of 32 x 32, k-chunk 16
@@ -376,7 +391,16 @@ struct TmaMaps {
 // mbarriers and the per-warp epilogue ring.
 struct GemmWide {
   static constexpr int TM_ = TM, TN_ = TN, KC_ = KC, AS = A_STRIDE, BS = B_STRIDE, WN_ = WN, KIND = 0;
+  static constexpr int GROUPS = 1, ST_ = STAGES;
   static constexpr bool SWZ = !A_PAD;
+};
+// Half: 64 x 64 tiles, two independent groups of 4 warps (2 x 2 of 32 x 32), each with
+// its own producer, 2-stage ring of 16-deep k chunks and mbarriers; tiles claimed from
+// one shared counter.  A box stride 20 / B stride 68: conflict-free fragments.
+struct GemmHalf {
+  static constexpr int TM_ = 64, TN_ = 64, KC_ = 16, AS = 20, BS = 68, WN_ = 2, KIND = 3;
+  static constexpr int GROUPS = 2, ST_ = HSTAGES;
+  static constexpr bool SWZ = false;
 };
 struct GemmNarrow {
   // k-chunk 16 (row stride 20) with the 32-wide chunks of the wide tiles, else 8 (row
@@ -384,6 +408,7 @@ struct GemmNarrow {
   static constexpr int TM_ = 256, TN_ = 32, KC_ = KC >= 32 ? 16 : ((STAGES <= 3 || EPI_RED) ? 8 : 4);
   static constexpr int AS = KC_ == 16 ? 20 : (KC_ == 8 ? 12 : 4);
   static constexpr int BS = 36, WN_ = 1, KIND = 1;
+  static constexpr int GROUPS = 1, ST_ = STAGES;
   static constexpr bool SWZ = false;
 };
 // Tall: 128 x 64 tiles (4 x 2 warps), k-chunk 8, B stride 68, for the W-block
@@ -392,11 +417,12 @@ struct GemmNarrow {
 struct GemmTall {
   static constexpr int TM_ = 128, TN_ = 64, KC_ = KC >= 32 ? 16 : 8, AS = KC_ == 16 ? 20 : 12, BS = 68, WN_ = 2,
                        KIND = 2;
+  static constexpr int GROUPS = 1, ST_ = STAGES;
   static constexpr bool SWZ = false;
 };
 template <class G>
 struct GemmShape {
-  static constexpr int WM_ = (NT / 32) / G::WN_;
+  static constexpr int WM_ = (NT / 32) / G::GROUPS / G::WN_;
   static constexpr int MI_ = G::TM_ / WM_ / 8;
   static constexpr int NJ_ = G::TN_ / G::WN_ / 8;
   static constexpr int SA = G::TM_ * G::AS, SB = G::KC_ * G::BS;
@@ -406,8 +432,12 @@ struct GemmShape {
 };
 constexpr int NARROW_SMEM_DBL = STAGES * GemmShape<GemmNarrow>::SDBL + (NT / 32) * EPI_DBL;
 constexpr int TALL_SMEM_DBL = STAGES * GemmShape<GemmTall>::SDBL + (NT / 32) * EPI_DBL;
-// dynamic shared memory of the GEMM engine: the largest of the three tile shapes
-constexpr int GEMM_SMEM_BYTES = std::max(WIDE_SMEM_BYTES, 8 * std::max(NARROW_SMEM_DBL, TALL_SMEM_DBL));
+constexpr int HALF_SMEM_DBL = 2 * HSTAGES * GemmShape<GemmHalf>::SDBL;
+static_assert(!HPS_HALF || EPI_RED, "half tiles reduce C in L2 (no epilogue ring)");
+// dynamic shared memory of the GEMM engine: the largest of the tile shapes
+constexpr int GEMM_SMEM_BYTES =
+    std::max(WIDE_SMEM_BYTES, 8 * std::max(std::max(NARROW_SMEM_DBL, TALL_SMEM_DBL), HALF_SMEM_DBL));
+constexpr int STAGES_MAX = STAGES > HSTAGES ? STAGES : HSTAGES;
 
 struct Ctx {
   double* M;
@@ -429,6 +459,9 @@ struct Ctx {
   uint64_t* full;   // STAGES mbarriers: stage filled (TMA tx complete)
   uint64_t* empty;  // STAGES mbarriers: stage released by all 8 warps
   unsigned pipe;    // running stage counter, identical in every thread
+  uint64_t* gfull;  // half tiles: [2 groups][HSTAGES] stage-filled mbarriers
+  uint64_t* gempty; // half tiles: [2 groups][HSTAGES] stage-released mbarriers (4 warps)
+  unsigned gpipe;   // half tiles: the group's running stage counter (same in its threads)
   // endgame sharing: sh = share record of the slot whose GEMM runs (own slot for
   // an owner, the helped slot for a helper); role 0 owner-capable, 2 helper
   ShareSlot* sh;
@@ -466,9 +499,14 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   constexpr int TM = G::TM_, TN = G::TN_, KC = G::KC_, A_STRIDE = G::AS, B_STRIDE = G::BS;
   constexpr int WN = G::WN_, MI = S::MI_, NJ = S::NJ_, STAGE_A = S::SA, STAGE_DBL = S::SDBL;
   constexpr bool narrow = (G::KIND == 1);
+  constexpr bool half = (G::KIND == 3);
+  constexpr int GR = G::GROUPS, STG = G::ST_;
   constexpr int WARPS_ = NT / 32;
+  constexpr int GW = WARPS_ / GR;  // warps per group (half tiles: two groups walk their own tiles)
   if (M <= 0 || N <= 0 || K <= 0) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int grp = GR == 1 ? 0 : warp / GW, gwarp = warp - grp * GW;
+  const int prod_tid = PRODUCER_TID + grp * GW * 32;  // the group's TMA producer
   // warp -> (row block wm, column block wn).  The warps of an SM sub-partition are
   // warp and warp + 4; with HPS_WARP_SWIZZLE the second row of warps is rotated by
   // WN / 2 columns, so each sub-partition holds an early and a late column block
@@ -476,19 +514,27 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   // late blocks idle in early chunks) instead of two warps of the same column.
   // (tall 4 x 2 warp grids: the second half of the warps takes the other column
   // block and the row blocks two further on)
-  const int wm = (!HPS_WARP_SWIZZLE || WN != 2) ? warp / WN : (warp < 4 ? warp : (warp - 2) % 4);
-  const int wn = !HPS_WARP_SWIZZLE ? warp % WN
-                 : (WN == 2 ? warp / 4 : (warp % WN + wm * (WN / 2)) % WN);
+  // (half tiles: group warps 2 x 2; a group's warps sit on the four sub-partitions)
+  const int wm = half ? gwarp / WN
+                      : ((!HPS_WARP_SWIZZLE || WN != 2) ? warp / WN : (warp < 4 ? warp : (warp - 2) % 4));
+  const int wn = half ? gwarp % WN
+                      : (!HPS_WARP_SWIZZLE ? warp % WN
+                                           : (WN == 2 ? warp / 4 : (warp % WN + wm * (WN / 2)) % WN));
   const int lr = lane >> 2, lc = lane & 3;
   const int tiles_n = (N + TN - 1) / TN;
   const int tiles = ((M + TM - 1) / TM) * tiles_n;
   const int kchunks = (K + KC - 1) / KC;  // K is a multiple of 16; the last chunk may be partial
-  double* smem = c.smem;
+  double* smem = c.smem + grp * STG * STAGE_DBL;
+  uint64_t* full = half ? c.gfull + grp * HSTAGES : c.full;
+  uint64_t* empty = half ? c.gempty + grp * HSTAGES : c.empty;
+  unsigned& pipe = half ? c.gpipe : c.pipe;
   const CUtensorMap* mapA = narrow ? &c.maps->a_work_n
+                           : half ? (a_src == 0 ? &c.maps->a_work_h : &c.maps->a_scratch_h)
                            : G::KIND == 2 ? &c.maps->a_work_t
                            : (a_src == 0 ? &c.maps->a_work
                                          : (a_src == 1 ? &c.maps->a_scratch : &c.maps->a_abi));
   const CUtensorMap* mapB = narrow ? &c.maps->b_work_n
+                           : half ? (b_src == 0 ? &c.maps->b_work_h : &c.maps->b_scratch_h)
                            : G::KIND == 2 ? &c.maps->b_scratch_t
                            : (b_src == 0 ? &c.maps->b_work : (b_src == 1 ? &c.maps->b_q : &c.maps->b_scratch));
   const int a_slot = a_src == 2 ? 0 : c.slot, b_slot = b_src == 1 ? 0 : c.slot;
@@ -497,10 +543,12 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   // Tile claims: mode 0 in order; mode 1 owner of a published op (atomicAdd on
   // the slot's claim word); mode 2 helper (compare-and-swap with the op's seq).
   __shared__ int s_gmode;
-  __shared__ int s_tile_ring[STAGES];  // tile id started in each stage (-1: end)
-  __shared__ int s_kc0_ring[STAGES];   // its first k-chunk
+  __shared__ int s_tile_ring[2][STAGES_MAX];  // per group: tile id started in each stage (-1: end)
+  __shared__ int s_kc0_ring[2][STAGES_MAX];   // its first k-chunk
+  __shared__ int s_next_tile;                 // half tiles, in-order mode: next unclaimed tile
   if (tid == 0) {
     int m = 0;
+    s_next_tile = 0;
     if (c.role == 2) {
       m = 2;
     } else if (c.sh && tiles >= SHARE_MIN_TILES &&
@@ -526,7 +574,11 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   int p_it = 0, p_tile = 0, p_kc = 0, p_next = 0, p_skipped = 0, p_k0 = 0, p_j = 0;
   bool p_end = false, p_in = false;
   auto claim_tile = [&]() -> int {
-    if (gmode == 0) return p_next < tiles ? p_next++ : -1;
+    if (gmode == 0) {
+      if (GR == 1) return p_next < tiles ? p_next++ : -1;
+      const int t = atomicAdd(&s_next_tile, 1);
+      return t < tiles ? t : -1;
+    }
     if (gmode == 1) {
       const unsigned long long old = atomicAdd(&c.sh->claim, 1ull);
       const int t = (int)(old & 0xffffffffull);
@@ -543,13 +595,13 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   // the next chunk into its stage, once every warp has released the stage's last use
   auto produce = [&]() {
     if (p_end) return;
-    const unsigned g = c.pipe + p_it;
-    const unsigned s = g % STAGES, use = g / STAGES;
+    const unsigned g = pipe + p_it;
+    const unsigned s = g % STG, use = g / STG;
     if (use > 0) {
 #ifdef HPS_TRACE
       if (blockIdx.x == 0 && g < HPS_TRACE) g_trace_prod[g][0] = clock64();
 #endif
-      mbar_wait(&c.empty[s], (use - 1) & 1);
+      mbar_wait(&empty[s], (use - 1) & 1);
 #ifdef HPS_TRACE
       if (blockIdx.x == 0 && g < HPS_TRACE) g_trace_prod[g][1] = clock64();
 #endif
@@ -590,14 +642,14 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
       p_k0 = p_kc;
       p_j = 0;
       if (HPS_KREV && (p_tile & 1)) p_kc = kchunks - 1;
-      s_tile_ring[s] = p_tile;
+      s_tile_ring[grp][s] = p_tile;
       if (p_tile < 0) {  // end marker: a stage with no data
         p_end = true;
-        mbar_arrive(&c.full[s]);
+        mbar_arrive(&full[s]);
         ++p_it;
         return;
       }
-      s_kc0_ring[s] = p_k0;
+      s_kc0_ring[grp][s] = p_k0;
       p_in = true;
     }
     const int tm = p_tile / tiles_n, tn = p_tile - tm * tiles_n;
@@ -608,19 +660,19 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
 #endif
 #ifdef HPS_TEST_NOTMA  // probe: no operand transfer (stale stage data), the ring protocol alone
     (void)sa; (void)sb; (void)tm; (void)tn;
-    mbar_arrive(&c.full[s]);
+    mbar_arrive(&full[s]);
 #else
-    mbar_expect_tx(&c.full[s], S::BYTES);
+    mbar_expect_tx(&full[s], S::BYTES);
 #if HPS_L2HINT
     // the A panel of a tile row is read again by the row's next tile: keep it; the B
     // panel is not reused before it would be evicted anyway
-    if (HPS_L2HINT & 1) tma_load_3d_hint(sa, mapA, ac + p_kc * KC, ar + tm * TM, a_slot, &c.full[s], policy_evict_last());
-    else tma_load_3d(sa, mapA, ac + p_kc * KC, ar + tm * TM, a_slot, &c.full[s]);
-    if (HPS_L2HINT & 2) tma_load_3d_hint(sb, mapB, bc + tn * TN, br + p_kc * KC, b_slot, &c.full[s], policy_evict_first());
-    else tma_load_3d(sb, mapB, bc + tn * TN, br + p_kc * KC, b_slot, &c.full[s]);
+    if (HPS_L2HINT & 1) tma_load_3d_hint(sa, mapA, ac + p_kc * KC, ar + tm * TM, a_slot, &full[s], policy_evict_last());
+    else tma_load_3d(sa, mapA, ac + p_kc * KC, ar + tm * TM, a_slot, &full[s]);
+    if (HPS_L2HINT & 2) tma_load_3d_hint(sb, mapB, bc + tn * TN, br + p_kc * KC, b_slot, &full[s], policy_evict_first());
+    else tma_load_3d(sb, mapB, bc + tn * TN, br + p_kc * KC, b_slot, &full[s]);
 #else
-    tma_load_3d(sa, mapA, ac + p_kc * KC, ar + tm * TM, a_slot, &c.full[s]);
-    tma_load_3d(sb, mapB, bc + tn * TN, br + p_kc * KC, b_slot, &c.full[s]);
+    tma_load_3d(sa, mapA, ac + p_kc * KC, ar + tm * TM, a_slot, &full[s]);
+    tma_load_3d(sb, mapB, bc + tn * TN, br + p_kc * KC, b_slot, &full[s]);
 #endif
 #endif
     if (PF_DIST > 0 && p_kc + PF_DIST < kchunks) {  // operand chunks further ahead into L2
@@ -631,6 +683,8 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
       // C tile into L2 ahead of the reduce-add epilogue
       if (narrow) {
         for (int r = 0; r < TM; r += 8) tma_prefetch_3d(&c.maps->b_work_n, cc + tn * TN, cr + tm * TM + r, c.slot);
+      } else if (half) {
+        for (int r = 0; r < TM; r += KC) tma_prefetch_3d(&c.maps->b_work_h, cc + tn * TN, cr + tm * TM + r, c.slot);
       } else {
         for (int r = 0; r < TM; r += KC)
           tma_prefetch_3d(&c.maps->b_work, cc + tn * TN, cr + tm * TM + r, c.slot);
@@ -645,8 +699,8 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     else ++p_kc;
     if (p_j == kchunks - p_k0) p_in = false;
   };
-  if (tid == PRODUCER_TID) {
-    for (int s = 0; s < STAGES - 1; ++s) produce();
+  if (tid == prod_tid) {
+    for (int s = 0; s < STG - 1; ++s) produce();
   }
 
   double acc[MI][NJ][2];
@@ -733,25 +787,25 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     }
   };
   for (;; ++it) {
-    if (tid == PRODUCER_TID) produce();
-    const unsigned g = c.pipe + it;
-    const unsigned s = g % STAGES;
+    if (tid == prod_tid) produce();
+    const unsigned g = pipe + it;
+    const unsigned s = g % STG;
 #ifdef HPS_TRACE
     const long long tr0 = clock64();
 #endif
-    mbar_wait(&c.full[s], (g / STAGES) & 1);
+    mbar_wait(&full[s], (g / STG) & 1);
 #ifdef HPS_TRACE
     if (blockIdx.x == 0 && lane == 0 && g < HPS_TRACE) { g_trace[warp][g][0] = tr0; g_trace[warp][g][1] = clock64(); }
 #endif
     if (!in_tile) {
-      tile = reinterpret_cast<volatile int*>(s_tile_ring)[s];
+      tile = reinterpret_cast<volatile int*>(s_tile_ring[grp])[s];
       if (tile < 0) {
         __syncwarp();
-        if (lane == 0) mbar_arrive(&c.empty[s]);
+        if (lane == 0) mbar_arrive(&empty[s]);
         ++it;
         break;
       }
-      kc = reinterpret_cast<volatile int*>(s_kc0_ring)[s];
+      kc = reinterpret_cast<volatile int*>(s_kc0_ring[grp])[s];
       kn = kchunks - kc;  // chunks of this tile
       kj = 0;
       krev = HPS_KREV && (tile & 1);
@@ -760,7 +814,7 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
       set_valid(tile);
     }
 #if HPS_PROF_EXEC
-    if (c.prof && tid == 0) s_exec_cap += (unsigned long long)(WARPS_ * MI * NJ * (KC / 4));
+    if (c.prof && tid == prod_tid) atomicAdd(&s_exec_cap, (unsigned long long)(GW * MI * NJ * (KC / 4)));
 #endif
     const double* sa = smem + s * STAGE_DBL;
     const double* sb = sa + STAGE_A;
@@ -834,7 +888,7 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
 #ifdef HPS_TRACE
     if (blockIdx.x == 0 && lane == 0 && g < HPS_TRACE) g_trace[warp][g][2] = clock64();
 #endif
-    if (lane == 0) mbar_arrive(&c.empty[s]);
+    if (lane == 0) mbar_arrive(&empty[s]);
     kc += krev ? -1 : 1;
     if (++kj == kn) {
       in_tile = false;
@@ -914,7 +968,7 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
       }
     }
   }
-  c.pipe += it;
+  pipe += it;
 #if HPS_PROF_EXEC
   if (c.prof && lane == 0) atomicAdd(&s_exec_dmma, my_dmma);
 #endif
@@ -926,8 +980,9 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   if (gmode != 0) {  // shared op: count the tiles done here; the owner waits for all
     __threadfence();
     __syncthreads();
+    // each group's producer counts its group's tiles; thread 0 (owner) waits for all
+    if (tid == prod_tid && my_tiles + p_skipped > 0) atomicAdd(&c.sh->done, my_tiles + p_skipped);
     if (tid == 0) {
-      if (my_tiles + p_skipped > 0) atomicAdd(&c.sh->done, my_tiles + p_skipped);
       if (gmode == 1) {
         while (*reinterpret_cast<volatile int*>(&c.sh->done) < tiles) __nanosleep(200);
         __threadfence();
@@ -956,6 +1011,10 @@ __device__ __forceinline__ void gemm(Ctx& c, const bool sub, const int a_src, in
     gemm_t<GemmNarrow>(c, sub, a_src, ar, ac, b_src, br, bc, cr, cc, M, N, K, kmode, tri);
   else if (!sub && a_src == 0 && b_src == 2 && N <= 64 && K % 8 == 0)  // W-block right inverse
     gemm_t<GemmTall>(c, sub, a_src, ar, ac, b_src, br, bc, cr, cc, M, N, K, kmode, tri);
+#if HPS_HALF
+  else if (a_src != 2 && b_src != 1)  // (legendre's plan-level operands stay wide)
+    gemm_t<GemmHalf>(c, sub, a_src, ar, ac, b_src, br, bc, cr, cc, M, N, K, kmode, tri);
+#endif
   else
     gemm_t<GemmWide>(c, sub, a_src, ar, ac, b_src, br, bc, cr, cc, M, N, K, kmode, tri);
 }
@@ -2274,11 +2333,16 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     hps_leaf_kernel(LeafParams P, const Op* __restrict__ ops, int n_ops, const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(1024) double smem[];
   __shared__ __align__(8) uint64_t bars[2 * STAGES];
+  __shared__ __align__(8) uint64_t gbars[2 * 2 * HSTAGES];  // half tiles: [full | empty][group][stage]
   const int slot = blockIdx.x;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&bars[s], 1);
       mbar_init(&bars[STAGES + s], NT / 32);
+    }
+    for (int s = 0; s < 2 * HSTAGES; ++s) {
+      mbar_init(&gbars[s], 1);
+      mbar_init(&gbars[2 * HSTAGES + s], NT / 32 / 2);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 #if HPS_PROF_EXEC
@@ -2293,6 +2357,9 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
   c.full = bars;
   c.empty = bars + STAGES;
   c.pipe = 0;
+  c.gfull = gbars;
+  c.gempty = gbars + 2 * HSTAGES;
+  c.gpipe = 0;
   c.M = P.work + (size_t)slot * P.slot_stride;
   c.ld = P.ld;
   c.n_piv = P.n_pad;
@@ -2541,6 +2608,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
         gemm(h, sub, a_src, op.ar, op.ac, b_src, op.br, op.bc, op.cr, op.cc, op.Mdim, N, op.Kdim,
              op.kmode, tri);
         c.pipe = h.pipe;
+        c.gpipe = h.gpipe;
       }
       __syncthreads();
     }
@@ -2891,7 +2959,13 @@ static int ensure_workspace(hps_plan_s* P, int mode, int want_slots) {
           make_map(&m.a_work_n, P->work, NC, NR, P->ws_slots, NC, per, GemmNarrow::AS,
                    GemmNarrow::TM_) ||
           make_map(&m.b_work_n, P->work, NC, NR, P->ws_slots, NC, per, GemmNarrow::BS,
-                   GemmNarrow::KC_))
+                   GemmNarrow::KC_) ||
+          make_map(&m.a_work_h, P->work, NC, NR, P->ws_slots, NC, per, GemmHalf::AS, GemmHalf::TM_) ||
+          make_map(&m.b_work_h, P->work, NC, NR, P->ws_slots, NC, per, GemmHalf::BS, GemmHalf::KC_) ||
+          make_map(&m.a_scratch_h, P->scratch, TRI_BLOCK, 2 * P->n_pad, P->ws_slots, TRI_BLOCK,
+                   (size_t)2 * P->n_pad * TRI_BLOCK, GemmHalf::AS, GemmHalf::TM_) ||
+          make_map(&m.b_scratch_h, P->scratch, TRI_BLOCK, 2 * P->n_pad, P->ws_slots, TRI_BLOCK,
+                   (size_t)2 * P->n_pad * TRI_BLOCK, GemmHalf::BS, GemmHalf::KC_))
         return -1;
       if (P->legendre &&
           (make_map(&m.a_abi, P->a_bi_pad, P->n_pad, P->m_pad, 1, P->n_pad,

@@ -206,7 +206,8 @@ def geometries(p):
     ops, T = build(p - 2)
     geos = [Geo("64x128/2x4 k16", 64, 128, 16, 2, 4), Geo("64x128/2x4 k4", 64, 128, 4, 2, 4),
             Geo("128x64/4x2 k16", 128, 64, 16, 4, 2), Geo("32x256/1x8 k16", 32, 256, 16, 1, 8),
-            Geo("128x128/4x4 k16", 128, 128, 16, 4, 4), Geo("128x256/4x8 k16", 128, 256, 16, 4, 8)]
+            Geo("128x128/4x4 k16", 128, 128, 16, 4, 4), Geo("128x256/4x8 k16", 128, 256, 16, 4, 8),
+            Geo("64x64/2x2 k4", 64, 64, 4, 2, 2), Geo("256x32/8x1 k4", 256, 32, 4, 8, 1)]
     for G in geos:
         walked = fl_all = 0.0
         s0 = 0

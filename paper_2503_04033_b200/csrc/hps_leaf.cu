@@ -174,6 +174,14 @@ constexpr int PRODUCER_TID = 32 * HPS_PRODUCER_WARP;
 #define HPS_HALF 0
 #endif
 constexpr int HSTAGES = 2;  // ring depth of each group (16-deep k chunks)
+// Wide GEMMs of a CTA's own op: every warp issues its slice of each chunk (A: 8 of the
+// 64 rows, B: 4 of the 32 k rows) instead of warp 0 issuing whole chunks, so no warp
+// carries the producer's work (the stage's full barrier then counts 8 arrivals).
+#ifndef HPS_SLICE
+#define HPS_SLICE 0
+#endif
+constexpr unsigned FULL_COUNT = HPS_SLICE ? NT / 32 : 1;
+static_assert(!(HPS_SLICE && (HPS_HALF || HPS_KREV)), "sliced production: 8-warp tiles, forward k order");
 #ifndef HPS_RW
 #define HPS_RW 256  // W-trick block of sorted boundary DOFs (rows below A_ii)
 #endif
@@ -284,6 +292,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, unsigned cnt) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(cnt) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
       "{\n .reg .pred p;\n"
@@ -381,6 +392,10 @@ struct TmaMaps {
   CUtensorMap b_work_h;   // half tiles: box {68, 16, 1}
   CUtensorMap a_scratch_h;  // half tiles: box {20, 64, 1} over the inverse cache
   CUtensorMap b_scratch_h;  // half tiles: box {68, 16, 1} over the inverse cache
+  CUtensorMap a_work_s;     // sliced wide chunks: box {A_STRIDE, 8, 1} (a warp's 8 A rows)
+  CUtensorMap a_scratch_s;  // ... over the inverse cache
+  CUtensorMap b_work_s;     // box {B_STRIDE, 4, 1} (a warp's 4 B k rows)
+  CUtensorMap b_scratch_s;  // ... over the inverse cache
 };
 
 // GEMM tile configurations.  Wide: 64 x 128 tiles, 2 x 4 warps of 32 x 32, k-chunk 16
@@ -569,7 +584,10 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   fence_proxy_async_global();
   __syncthreads();
   const int gmode = s_gmode;
-
+  // sliced production: own-op (in-order) wide GEMMs on slot / inverse-cache operands
+  const bool slice = HPS_SLICE && G::KIND == 0 && gmode == 0 && a_src != 2 && b_src != 1;
+  __shared__ int s_tile_ring_w[NT / 32][STAGES_MAX];  // sliced: per warp, tile id of each stage
+  __shared__ int s_kc0_ring_w[NT / 32][STAGES_MAX];
   // producer state (thread 0 only)
   int p_it = 0, p_tile = 0, p_kc = 0, p_next = 0, p_skipped = 0, p_k0 = 0, p_j = 0;
   bool p_end = false, p_in = false;
@@ -630,10 +648,11 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
           kk = max(kk, gm - ac);
           if (kk >= K) {  // the tile's rows are zero over the whole k range: C unchanged
             ++p_skipped;
-            if (c.prof) c.prof[31] += ((unsigned long long)K * TM * TN * 2) >> 20;
+            if (c.prof && (!slice || tid == 0)) c.prof[31] += ((unsigned long long)K * TM * TN * 2) >> 20;
             continue;
           }
-          if (c.prof && kk > 0) c.prof[31] += ((unsigned long long)(kk / KC) * KC * TM * TN * 2) >> 20;
+          if (c.prof && kk > 0 && (!slice || tid == 0))
+            c.prof[31] += ((unsigned long long)(kk / KC) * KC * TM * TN * 2) >> 20;
         }
         const int k0 = kk / KC;
         p_kc = k0 > kchunks - 1 ? kchunks - 1 : k0;
@@ -642,14 +661,26 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
       p_k0 = p_kc;
       p_j = 0;
       if (HPS_KREV && (p_tile & 1)) p_kc = kchunks - 1;
-      s_tile_ring[grp][s] = p_tile;
+      if (slice) {
+        if (lane == 0) s_tile_ring_w[warp][s] = p_tile;
+      } else {
+        s_tile_ring[grp][s] = p_tile;
+      }
       if (p_tile < 0) {  // end marker: a stage with no data
         p_end = true;
-        mbar_arrive(&full[s]);
+        if (slice) {
+          if (lane == 0) mbar_arrive(&full[s]);
+        } else {
+          mbar_arrive_cnt(&full[s], FULL_COUNT);
+        }
         ++p_it;
         return;
       }
-      s_kc0_ring[grp][s] = p_k0;
+      if (slice) {
+        if (lane == 0) s_kc0_ring_w[warp][s] = p_k0;
+      } else {
+        s_kc0_ring[grp][s] = p_k0;
+      }
       p_in = true;
     }
     const int tm = p_tile / tiles_n, tn = p_tile - tm * tiles_n;
@@ -660,9 +691,33 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
 #endif
 #ifdef HPS_TEST_NOTMA  // probe: no operand transfer (stale stage data), the ring protocol alone
     (void)sa; (void)sb; (void)tm; (void)tn;
-    mbar_arrive(&full[s]);
+    mbar_arrive_cnt(&full[s], FULL_COUNT);
 #else
+    if (slice) {
+      // this warp's slice: A rows [8 warp, 8 warp + 8), B k rows [4 warp, 4 warp + 4)
+      if (lane == 0) {
+        mbar_expect_tx(&full[s], S::BYTES / (NT / 32));
+        const CUtensorMap* mA = a_src == 0 ? &c.maps->a_work_s : &c.maps->a_scratch_s;
+        const CUtensorMap* mB = b_src == 0 ? &c.maps->b_work_s : &c.maps->b_scratch_s;
+        tma_load_3d(sa + warp * 8 * A_STRIDE, mA, ac + p_kc * KC, ar + tm * TM + warp * 8, a_slot, &full[s]);
+        if (HPS_L2HINT & 2)
+          tma_load_3d_hint(sb + warp * 4 * B_STRIDE, mB, bc + tn * TN, br + p_kc * KC + warp * 4, b_slot, &full[s],
+                           policy_evict_first());
+        else
+          tma_load_3d(sb + warp * 4 * B_STRIDE, mB, bc + tn * TN, br + p_kc * KC + warp * 4, b_slot, &full[s]);
+        if (sub && p_j == max(0, kchunks - p_k0 - HPS_CPF)) {  // this warp's 8 rows of the C tile into L2
+          tma_prefetch_3d(&c.maps->b_work_s, cc + tn * TN, cr + tm * TM + warp * 8, c.slot);
+          tma_prefetch_3d(&c.maps->b_work_s, cc + tn * TN, cr + tm * TM + warp * 8 + 4, c.slot);
+        }
+      }
+      ++p_it;
+      ++p_j;
+      ++p_kc;
+      if (p_j == kchunks - p_k0) p_in = false;
+      return;
+    }
     mbar_expect_tx(&full[s], S::BYTES);
+    if (FULL_COUNT > 1) mbar_arrive_cnt(&full[s], FULL_COUNT - 1);
 #if HPS_L2HINT
     // the A panel of a tile row is read again by the row's next tile: keep it; the B
     // panel is not reused before it would be evicted anyway
@@ -699,7 +754,7 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     else ++p_kc;
     if (p_j == kchunks - p_k0) p_in = false;
   };
-  if (tid == prod_tid) {
+  if (slice || tid == prod_tid) {
     for (int s = 0; s < STG - 1; ++s) produce();
   }
 
@@ -787,7 +842,7 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     }
   };
   for (;; ++it) {
-    if (tid == prod_tid) produce();
+    if (slice || tid == prod_tid) produce();
     const unsigned g = pipe + it;
     const unsigned s = g % STG;
 #ifdef HPS_TRACE
@@ -798,14 +853,16 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     if (blockIdx.x == 0 && lane == 0 && g < HPS_TRACE) { g_trace[warp][g][0] = tr0; g_trace[warp][g][1] = clock64(); }
 #endif
     if (!in_tile) {
-      tile = reinterpret_cast<volatile int*>(s_tile_ring[grp])[s];
+      tile = slice ? reinterpret_cast<volatile int*>(s_tile_ring_w[warp])[s]
+                   : reinterpret_cast<volatile int*>(s_tile_ring[grp])[s];
       if (tile < 0) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         ++it;
         break;
       }
-      kc = reinterpret_cast<volatile int*>(s_kc0_ring[grp])[s];
+      kc = slice ? reinterpret_cast<volatile int*>(s_kc0_ring_w[warp])[s]
+                 : reinterpret_cast<volatile int*>(s_kc0_ring[grp])[s];
       kn = kchunks - kc;  // chunks of this tile
       kj = 0;
       krev = HPS_KREV && (tile & 1);
@@ -2337,7 +2394,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
   const int slot = blockIdx.x;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&bars[s], 1);
+      mbar_init(&bars[s], FULL_COUNT);
       mbar_init(&bars[STAGES + s], NT / 32);
     }
     for (int s = 0; s < 2 * HSTAGES; ++s) {
@@ -2965,7 +3022,13 @@ static int ensure_workspace(hps_plan_s* P, int mode, int want_slots) {
           make_map(&m.a_scratch_h, P->scratch, TRI_BLOCK, 2 * P->n_pad, P->ws_slots, TRI_BLOCK,
                    (size_t)2 * P->n_pad * TRI_BLOCK, GemmHalf::AS, GemmHalf::TM_) ||
           make_map(&m.b_scratch_h, P->scratch, TRI_BLOCK, 2 * P->n_pad, P->ws_slots, TRI_BLOCK,
-                   (size_t)2 * P->n_pad * TRI_BLOCK, GemmHalf::BS, GemmHalf::KC_))
+                   (size_t)2 * P->n_pad * TRI_BLOCK, GemmHalf::BS, GemmHalf::KC_) ||
+          make_map(&m.a_work_s, P->work, NC, NR, P->ws_slots, NC, per, A_STRIDE, 8, !A_PAD) ||
+          make_map(&m.a_scratch_s, P->scratch, TRI_BLOCK, 2 * P->n_pad, P->ws_slots, TRI_BLOCK,
+                   (size_t)2 * P->n_pad * TRI_BLOCK, A_STRIDE, 8, !A_PAD) ||
+          make_map(&m.b_work_s, P->work, NC, NR, P->ws_slots, NC, per, B_STRIDE, 4) ||
+          make_map(&m.b_scratch_s, P->scratch, TRI_BLOCK, 2 * P->n_pad, P->ws_slots, TRI_BLOCK,
+                   (size_t)2 * P->n_pad * TRI_BLOCK, B_STRIDE, 4))
         return -1;
       if (P->legendre &&
           (make_map(&m.a_abi, P->a_bi_pad, P->n_pad, P->m_pad, 1, P->n_pad,

@@ -177,6 +177,7 @@ constexpr int HSTAGES = 2;  // ring depth of each group (16-deep k chunks)
 // Wide GEMMs of a CTA's own op: every warp issues its slice of each chunk (A: 8 of the
 // 64 rows, B: 4 of the 32 k rows) instead of warp 0 issuing whole chunks, so no warp
 // carries the producer's work (the stage's full barrier then counts 8 arrivals).
+// Measured -3.6% at p = 16, -0.5% at p = 20 (profiles/r02c_variant_sweep.jsonl): off.
 #ifndef HPS_SLICE
 #define HPS_SLICE 0
 #endif

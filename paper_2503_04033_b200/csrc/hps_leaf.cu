@@ -135,6 +135,12 @@ constexpr int SHARE_MIN_TILES = 16;
 #define HPS_PF 0  // GEMM operand L2 prefetch distance in k chunks (0: off)
 #endif
 constexpr int PF_DIST = HPS_PF;
+#ifndef HPS_PROF_GEMM
+#define HPS_PROF_GEMM 0  // diagnostics build: setup / data-wait / tail / producer cycles per GEMM bucket
+#endif
+#ifndef HPS_PF_NEXT
+#define HPS_PF_NEXT 0  // narrow / tall GEMMs: chunks of the next tile prefetched into L2
+#endif
 // C tile L2 prefetch issued HPS_CPF k chunks before the tile's last chunk (0: with the
 // first chunk).  A long tile outlives L2 residency (K = 1376: ~180 us per tile while L2
 // turns over every ~35 us), so a prefetch at the start is evicted before the epilogue's
@@ -151,13 +157,13 @@ constexpr int PF_DIST = HPS_PF;
 // cycles of its own DMMA issue; warp 5 holds the tile's last-starting 32 x 32 block (wide
 // tiles: row block 1, column block 3; tall tiles: row block 3, column block 1), so in
 // ragged tiles it issues while it has no DMMAs of its own.
-// Only warp 0 works: the share protocol's sequence number (Ctx::seq) and op
-// publication live in thread 0, so a producer elsewhere deadlocks on shared ops
-// (HPS_PRODUCER_WARP=5 hung the bench, profiles/r02c_variant_sweep.jsonl).
+// (round 2: warp 5 deadlocked the shared endgame ops, whose done count was added by
+// thread 0 while the producer counted the skipped tiles; the producer adds its own
+// count now — see the end of gemm_t.)
 #ifndef HPS_PRODUCER_WARP
 #define HPS_PRODUCER_WARP 0
 #endif
-static_assert(HPS_PRODUCER_WARP == 0, "the TMA producer must be thread 0 (share protocol state)");
+static_assert(HPS_PRODUCER_WARP >= 0 && HPS_PRODUCER_WARP < NT / 32, "producer warp");
 constexpr int PRODUCER_TID = 32 * HPS_PRODUCER_WARP;
 // L2 eviction hints on the operand loads: bit 1 A evict_last, bit 2 B evict_first
 #ifndef HPS_L2HINT
@@ -240,7 +246,7 @@ struct LeafParams {
 #ifndef HPS_PROF_EXEC
 #define HPS_PROF_EXEC 0  // diagnostics build: count the DMMAs each GEMM op executes
 #endif
-constexpr int PROF_SLOTS = 48;  // 0..8 op kinds, 9 leaves, 10-14 panel steps, 15 interchanges,
+constexpr int PROF_SLOTS = 64;  // 0..8 op kinds, 9 leaves, 10-14 panel steps, 15 interchanges,
                                 // 16-18 GEMM cycles by N (<=64, <=256, >256), 19-21 their MFLOP, 22 assemble, 23 output
                                 // (HPS_PROF_EXEC) 32-34 executed DMMA flops by N bucket, 35-37 by phase,
                                 // 38-40 GEMM cycles by phase
@@ -523,6 +529,14 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int grp = GR == 1 ? 0 : warp / GW, gwarp = warp - grp * GW;
   const int prod_tid = PRODUCER_TID + grp * GW * 32;  // the group's TMA producer
+#if HPS_PROF_GEMM
+  // diagnostics (the producer thread, by the GEMM's N bucket): 48+b setup, 51+b its warp's
+  // waits for stage data, 54+b tail (epilogue fences and syncs), 57+b chunks, 60+b producer
+  // time (44+b of it waiting for a released stage; 47 tile claims + k bounds, 63 chunk issue)
+  const int pb = N <= 64 ? 0 : (N <= 256 ? 1 : 2);
+  const bool pt = c.prof != nullptr && tid == prod_tid;
+  long long pt0 = pt ? clock64() : 0;
+#endif
   // warp -> (row block wm, column block wn).  The warps of an SM sub-partition are
   // warp and warp + 4; with HPS_WARP_SWIZZLE the second row of warps is rotated by
   // WN / 2 columns, so each sub-partition holds an early and a late column block
@@ -585,6 +599,9 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   fence_proxy_async_global();
   __syncthreads();
   const int gmode = s_gmode;
+#if HPS_PROF_GEMM
+  if (pt) { const long long t = clock64(); c.prof[48 + pb] += t - pt0; pt0 = t; }
+#endif
   // sliced production: own-op (in-order) wide GEMMs on slot / inverse-cache operands
   const bool slice = HPS_SLICE && G::KIND == 0 && gmode == 0 && a_src != 2 && b_src != 1;
   __shared__ int s_tile_ring_w[NT / 32][STAGES_MAX];  // sliced: per warp, tile id of each stage
@@ -620,12 +637,21 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
 #ifdef HPS_TRACE
       if (blockIdx.x == 0 && g < HPS_TRACE) g_trace_prod[g][0] = clock64();
 #endif
+#if HPS_PROF_GEMM
+      const long long pe = pt ? clock64() : 0;
+#endif
       mbar_wait(&empty[s], (use - 1) & 1);
+#if HPS_PROF_GEMM
+      if (pt) c.prof[44 + pb] += clock64() - pe;  // the producer's wait for a released stage
+#endif
 #ifdef HPS_TRACE
       if (blockIdx.x == 0 && g < HPS_TRACE) g_trace_prod[g][1] = clock64();
 #endif
     }
     const bool first_chunk = !p_in;
+#if HPS_PROF_GEMM
+    const long long pc = pt ? clock64() : 0;
+#endif
     if (!p_in) {
       for (;;) {
         p_tile = claim_tile();
@@ -684,6 +710,10 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
       }
       p_in = true;
     }
+#if HPS_PROF_GEMM
+    long long pi = 0;
+    if (pt) { pi = clock64(); c.prof[47] += pi - pc; }  // tile claim + k bounds (all buckets)
+#endif
     const int tm = p_tile / tiles_n, tn = p_tile - tm * tiles_n;
     double* sa = smem + s * STAGE_DBL;
     double* sb = sa + STAGE_A;
@@ -735,6 +765,18 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
       tma_prefetch_3d(mapA, ac + (p_kc + PF_DIST) * KC, ar + tm * TM, a_slot);
       tma_prefetch_3d(mapB, bc + tn * TN, br + (p_kc + PF_DIST) * KC, b_slot);
     }
+#if HPS_PF_NEXT
+    // narrow / tall tiles (short K, latency-bound): with a tile's first chunk, the next
+    // tile's A chunks (up to HPS_PF_NEXT of them, from this tile's first k) into L2
+    if ((narrow || G::KIND == 2) && gmode == 0 && first_chunk) {
+      const int nt = p_tile + 1;
+      if (nt < tiles) {
+        const int ntm = nt / tiles_n;
+        for (int q = p_k0; q < kchunks && q < p_k0 + HPS_PF_NEXT; ++q)
+          tma_prefetch_3d(mapA, ac + q * KC, ar + ntm * TM, a_slot);
+      }
+    }
+#endif
     if (sub && (HPS_CPF == 0 ? first_chunk : p_j == max(0, kchunks - p_k0 - HPS_CPF))) {
       // C tile into L2 ahead of the reduce-add epilogue
       if (narrow) {
@@ -754,6 +796,9 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     if (HPS_KREV && (p_tile & 1)) --p_kc;
     else ++p_kc;
     if (p_j == kchunks - p_k0) p_in = false;
+#if HPS_PROF_GEMM
+    if (pt) c.prof[63] += clock64() - pi;  // TMA issue and prefetches (all buckets)
+#endif
   };
   if (slice || tid == prod_tid) {
     for (int s = 0; s < STG - 1; ++s) produce();
@@ -843,13 +888,22 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     }
   };
   for (;; ++it) {
+#if HPS_PROF_GEMM
+    long long pq = pt ? clock64() : 0;
+#endif
     if (slice || tid == prod_tid) produce();
+#if HPS_PROF_GEMM
+    if (pt) { const long long t = clock64(); c.prof[60 + pb] += t - pq; pq = t; }
+#endif
     const unsigned g = pipe + it;
     const unsigned s = g % STG;
 #ifdef HPS_TRACE
     const long long tr0 = clock64();
 #endif
     mbar_wait(&full[s], (g / STG) & 1);
+#if HPS_PROF_GEMM
+    if (pt) { c.prof[51 + pb] += clock64() - pq; c.prof[57 + pb] += 1; }
+#endif
 #ifdef HPS_TRACE
     if (blockIdx.x == 0 && lane == 0 && g < HPS_TRACE) { g_trace[warp][g][0] = tr0; g_trace[warp][g][1] = clock64(); }
 #endif
@@ -1027,6 +1081,9 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     }
   }
   pipe += it;
+#if HPS_PROF_GEMM
+  if (pt) pt0 = clock64();
+#endif
 #if HPS_PROF_EXEC
   if (c.prof && lane == 0) atomicAdd(&s_exec_dmma, my_dmma);
 #endif
@@ -1048,6 +1105,9 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     }
   }
   __syncthreads();
+#if HPS_PROF_GEMM
+  if (pt) c.prof[54 + pb] += clock64() - pt0;
+#endif
 }
 
 // kmode: per-tile k offsets where an operand has structural zero prefixes —

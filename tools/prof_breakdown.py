@@ -21,13 +21,13 @@ def run():
     else:
         eng.reduce_load(coeffs, f)
 run(); torch.cuda.synchronize()
-cnt = torch.zeros(eng.slots * 48, dtype=torch.int64, device="cuda")
+cnt = torch.zeros(eng.slots * 64, dtype=torch.int64, device="cuda")
 eng.lib.hps_plan_set_profile(eng.plan, ctypes.c_void_p(cnt.data_ptr()))
 e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
 e0.record(); run(); e1.record(); torch.cuda.synchronize()
 eng.lib.hps_plan_set_profile(eng.plan, ctypes.c_void_p(0))
 ms = e0.elapsed_time(e1)
-c = cnt.view(eng.slots, 48).cpu().numpy().astype(float)
+c = cnt.view(eng.slots, 64).cpu().numpy().astype(float)
 names = ["small-panel", "swaps", "inv-lower", "inv-upper", "gemm-sub", "gemm-set", "gemm-set-Q", "gemm-sub-abi", "copy-abb"]
 tot = c[:, :9].sum() + c[:, 22].sum() + c[:, 23].sum() + c[:, 24].sum() + c[:, 27].sum()
 leaves = c[:, 9].sum()
@@ -82,3 +82,12 @@ if ex > 0:   # HPS_PROF_EXEC build: DMMA flops actually issued
         if cyc:
             print(f"    phase {nm:20s} gemm {cyc/leaves/clk*1e3:7.2f} ms/leaf, executed {f/leaves:.2e} flop/leaf, "
                   f"{f/cyc*clk/1e9:6.1f} GF/s per CTA; whole phase {c[:, 28 + i].sum()/leaves/clk*1e3:.1f} ms/leaf")
+if c[:, 57:60].sum() > 0:   # HPS_PROF_GEMM build: where thread 0's GEMM time goes
+    print("  GEMM time of thread 0 by N bucket (ms/leaf): setup | producer (of which: waiting for a released stage)"
+          " | stage-data waits | tail; chunks/leaf")
+    for b, nm in enumerate(["N<=64", "N<=256", "N>256"]):
+        f = lambda k: c[:, k + b].sum() / leaves / clk * 1e3
+        print(f"    {nm:7s} {f(48):7.2f} | {f(60):7.2f} ({f(44):7.2f}) | {f(51):7.2f} | {f(54):7.2f};"
+              f"  {c[:, 57 + b].sum() / leaves:8.0f}")
+    f = lambda k: c[:, k].sum() / leaves / clk * 1e3
+    print(f"    producer, all buckets: tile claim + k bounds {f(47):.2f} ms/leaf, chunk issue (expect_tx, TMA, prefetch) {f(63):.2f} ms/leaf")

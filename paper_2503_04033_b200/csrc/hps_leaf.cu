@@ -2210,6 +2210,10 @@ __device__ void copy_block(const double* src, int ld, double* out, int ld_out, i
 // sign D1[a][edge][p-1]) is added in registers instead of read from HBM.
 // Returns false when the slab ring does not fit; the caller then uses dtn_lines.
 constexpr int LINE_NBUF = 4;
+#ifndef HPS_LINE_CW
+#define HPS_LINE_CW 16
+#endif
+static_assert(HPS_LINE_CW <= 16, "line-output column chunk within m_pad");
 __device__ bool dtn_lines_stream(const LeafParams& P, Ctx& c, const double* M, int ld, double* T) {
   __shared__ double s_w[3][2][32];
   __shared__ double s_e[3][2][2];
@@ -2217,7 +2221,9 @@ __device__ bool dtn_lines_stream(const LeafParams& P, Ctx& c, const double* M, i
   const int S = (d == 3) ? q * q : q;
   // int tables in shared memory: slot column -> DtN column, interior node -> slot row
   const int tab_d = P.rowperm ? (m + 1) / 2 + (P.n + 1) / 2 : 0;
-  int CW = 8;
+  // column chunk: 16 columns (128-byte row segments of X) when the ring fits (p <= 12),
+  // else 8 or fewer (m_pad is a multiple of 16, so a chunk never leaves the row)
+  int CW = HPS_LINE_CW;
   while (CW >= 2 && (2 + LINE_NBUF) * S * CW + tab_d > c.smem_doubles) CW >>= 1;
   if (CW < 2 || q > 32) return false;
   __syncthreads();  // smem is free (previous op finished with it)

@@ -1222,7 +1222,29 @@ __shared__ int s_swp_dst[16], s_swp_src[16], s_swp_cnt;
 __shared__ int s_swp_rows[16], s_swp_cont[16];  // thread 0's scratch (no local-memory arrays)
 // pivot search state, parity-buffered by column: per-warp best |a| / row / row values,
 // and row j's values at the start of step j
-__shared__ double s_pv[2][NT / 32];
+// Pivot search keys: |a| compared as an integer (the bit pattern of a non-negative
+// double orders like its value), +1 so that 0 means "no candidate" and NaN never
+// wins — the same choice as the double compares (max |a|, lowest index on ties),
+// made with integer compares and warp reductions (redux.sync) instead of FP64
+// compares, which queue behind the co-resident CTA's DMMAs on the FP64 pipe.
+#ifndef HPS_PIVOT_IKEY
+#define HPS_PIVOT_IKEY 1
+#endif
+#if HPS_PIVOT_IKEY
+typedef unsigned long long PivKey;
+__device__ __forceinline__ PivKey piv_key(double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v) & 0x7fffffffffffffffull;
+  return b > 0x7ff0000000000000ull ? 0ull : b + 1ull;
+}
+__device__ __forceinline__ double piv_val(PivKey k) { return k ? __longlong_as_double((long long)(k - 1ull)) : -1.0; }
+#define PIV_NONE 0ull
+#else
+typedef double PivKey;
+__device__ __forceinline__ PivKey piv_key(double v) { return fabs(v); }
+__device__ __forceinline__ double piv_val(PivKey k) { return k; }
+#define PIV_NONE (-1.0)
+#endif
+__shared__ PivKey s_pv[2][NT / 32];
 __shared__ int s_pi[2][NT / 32];
 __shared__ double s_cand[2][NT / 32][8];
 __shared__ double s_rowj[2][8];
@@ -1394,13 +1416,21 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
   //    it every thread picks the pivot itself and the interchange happens in
   //    flight: row j takes the pivot row, the pivot row's owner takes old row j.
   {
-    auto warp_argmax = [&](double best, int bidx, int par) {
+    auto warp_argmax = [&](PivKey best, int bidx, int par) {
+#if HPS_PIVOT_IKEY
+      const unsigned hi = (unsigned)(best >> 32), lo = (unsigned)best;
+      const unsigned hmax = __reduce_max_sync(0xffffffffu, hi);
+      const unsigned lmax = __reduce_max_sync(0xffffffffu, hi == hmax ? lo : 0u);
+      bidx = __reduce_min_sync(0xffffffffu, (hi == hmax && lo == lmax) ? bidx : 0x7fffffff);
+      best = ((PivKey)hmax << 32) | lmax;
+#else
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) {
         const double ov = __shfl_xor_sync(0xffffffffu, best, off);
         const int oi = __shfl_xor_sync(0xffffffffu, bidx, off);
         if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
       }
+#endif
       __syncwarp();  // the winner row's owner lane wrote it before the shuffles
       if (lane == 0) {
         s_pv[par][warp] = best;
@@ -1412,10 +1442,10 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
       }
     };
     {
-      double best = -1.0;
+      PivKey best = PIV_NONE;
       int bidx = 0x7fffffff;
       for (int r = tid; r < n_cand; r += NT) {
-        const double v = fabs(S[r]);
+        const PivKey v = piv_key(S[r]);
         if (v > best) { best = v; bidx = r; }
       }
       warp_argmax(best, bidx, 0);
@@ -1428,13 +1458,13 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
 #pragma unroll
     for (int j = 0; j < WB; ++j) {  // unrolled: register arrays indexed by j
       const int par = j & 1;
-      double bv = s_pv[par][0];
+      PivKey bk = s_pv[par][0];
       int bi = s_pi[par][0], bw = 0;
 #pragma unroll
       for (int q = 1; q < NT / 32; ++q) {
-        const double v = s_pv[par][q];
+        const PivKey v = s_pv[par][q];
         const int i = s_pi[par][q];
-        if (v > bv || (v == bv && i < bi)) { bv = v; bi = i; bw = q; }
+        if (v > bk || (v == bk && i < bi)) { bk = v; bi = i; bw = q; }
       }
       if (bi == 0x7fffffff) bi = j;
       double urow[WB], rowj[WB];
@@ -1443,7 +1473,7 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
       // threshold partial pivoting (sorted-row LU): keep the row in place when its
       // entry is within a factor c.tau of the column maximum — fewer interchanges
       // keep the equations' first-nonzero order, which the trailing updates use
-      if (c.tau > 0.0 && bi != j && fabs(rowj[j]) >= c.tau * bv) bi = j;
+      if (c.tau > 0.0 && bi != j && fabs(rowj[j]) >= c.tau * piv_val(bk)) bi = j;
 #pragma unroll
       for (int t = 0; t < WB; ++t) urow[t] = (bi == j) ? rowj[t] : s_cand[par][bw][t];
       if (tid == 0) {
@@ -1473,7 +1503,7 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
       }
       const double pivot = urow[j];
       const double inv = (pivot != 0.0) ? 1.0 / pivot : 1.0;
-      double best = -1.0;
+      PivKey best = PIV_NONE;
       int bidx = 0x7fffffff;
       constexpr int RU = WB >= 8 ? 2 : 4;  // rows in flight per thread
       for (int r0 = j + 1 + tid; r0 < n_cand; r0 += NT * RU) {
@@ -1500,7 +1530,7 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
               else if (r == bi) S[t * NS + r] = rowj[t];
             }
             if (j + 1 < WB) {
-              const double a = fabs(v[u][j + 1]);
+              const PivKey a = piv_key(v[u][j + 1]);
               if (a > best) { best = a; bidx = r; }
               if (r == j + 1) {  // thread 0: stash row j+1 for the next step
 #pragma unroll

@@ -1227,6 +1227,9 @@ __shared__ int s_swp_rows[16], s_swp_cont[16];  // thread 0's scratch (no local-
 // wins — the same choice as the double compares (max |a|, lowest index on ties),
 // made with integer compares and warp reductions (redux.sync) instead of FP64
 // compares, which queue behind the co-resident CTA's DMMAs on the FP64 pipe.
+#ifndef HPS_PROF_PIVOT
+#define HPS_PROF_PIVOT 0  // diagnostics build: per-column pivot-step timers (prof 44-47)
+#endif
 #ifndef HPS_PIVOT_IKEY
 #define HPS_PIVOT_IKEY 1
 #endif
@@ -1263,6 +1266,37 @@ __device__ __forceinline__ int cand_row(int i, int b0, int head, bool compact) {
   if (!compact || i < head) return b0 + i;
   const int k = i - head;
   return (s_glist[k >> 4] << 4) + (k & 15);
+}
+
+// Pivot of column b0 + j chosen (candidate index bi, pivot value pv): the pivot row in
+// c.piv, the equations' first-nonzero tables follow an interchange, pivot statistics.
+#ifndef HPS_PIVOT_DEFER
+#define HPS_PIVOT_DEFER 1
+#endif
+__shared__ int s_jbi[8];
+__shared__ double s_jpv[8];
+__device__ __forceinline__ void pivot_bookkeeping(Ctx& c, int b0, int j, int bi, int head, bool compact, double pv) {
+  const int prow = cand_row(bi, b0, head, compact);
+  c.piv[b0 + j] = prow;
+  if (c.prof && bi != j) c.prof[15] += 1;
+  if (c.gpos && bi != j) {  // the equations' first-nonzero table follows the interchange
+    const int ta = c.gpos[b0 + j], tb = c.gpos[prow];
+    c.gpos[b0 + j] = tb;
+    c.gpos[prow] = ta;
+    // 16-row minima stay lower bounds (a group may only gain a smaller g)
+    int* ga = c.gmin16 + ((b0 + j) >> 4);
+    int* gb = c.gmin16 + (prow >> 4);
+    *ga = min(*ga, tb);
+    *gb = min(*gb, ta);
+    // column bounds hold only up to the first interchange (the swapped-in row
+    // brings its own columns): floor every column's bound at this step
+    if (c.gcol16[-1] > b0 + j) c.gcol16[-1] = b0 + j;
+  }
+  if (b0 + j < c.n_real) {
+    const double ap = fabs(pv);
+    s_pmin = fmin(s_pmin, ap);
+    s_pmax = fmax(s_pmax, ap);
+  }
 }
 
 template <int WB>
@@ -1458,6 +1492,10 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
 #pragma unroll
     for (int j = 0; j < WB; ++j) {  // unrolled: register arrays indexed by j
       const int par = j & 1;
+#if HPS_PROF_PIVOT  // diagnostics (thread 0): 44 selection + bookkeeping + 1/pivot, 45 row
+                    // loop, 46 warp argmax + candidate stash, 47 the column barrier
+      long long pq0 = (prof && tid == 0) ? clock64() : 0;
+#endif
       PivKey bk = s_pv[par][0];
       int bi = s_pi[par][0], bw = 0;
 #pragma unroll
@@ -1477,26 +1515,13 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
 #pragma unroll
       for (int t = 0; t < WB; ++t) urow[t] = (bi == j) ? rowj[t] : s_cand[par][bw][t];
       if (tid == 0) {
-        const int prow = cand_row(bi, b0, head, compact);
-        c.piv[b0 + j] = prow;
-        if (c.prof && bi != j) c.prof[15] += 1;
-        if (c.gpos && bi != j) {  // the equations' first-nonzero table follows the interchange
-          const int ta = c.gpos[b0 + j], tb = c.gpos[prow];
-          c.gpos[b0 + j] = tb;
-          c.gpos[prow] = ta;
-          // 16-row minima stay lower bounds (a group may only gain a smaller g)
-          int* ga = c.gmin16 + ((b0 + j) >> 4);
-          int* gb = c.gmin16 + (prow >> 4);
-          *ga = min(*ga, tb);
-          *gb = min(*gb, ta);
-          // column bounds hold only up to the first interchange (the swapped-in row
-          // brings its own columns): floor every column's bound at this step
-          if (c.gcol16[-1] > b0 + j) c.gcol16[-1] = b0 + j;
-        }
-        if (b0 + j < c.n_real) {
-          const double ap = fabs(urow[j]);
-          s_pmin = fmin(s_pmin, ap);
-          s_pmax = fmax(s_pmax, ap);
+        if (HPS_PIVOT_DEFER) {
+          // the column's bookkeeping waits for the end of the block (nothing in the
+          // block reads it): thread 0 stays off the column's critical path
+          s_jbi[j] = bi;
+          s_jpv[j] = urow[j];
+        } else {
+          pivot_bookkeeping(c, b0, j, bi, head, compact, urow[j]);
         }
 #pragma unroll
         for (int t = 0; t < WB; ++t) S[t * NS + j] = urow[t];
@@ -1505,6 +1530,9 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
       const double inv = (pivot != 0.0) ? 1.0 / pivot : 1.0;
       PivKey best = PIV_NONE;
       int bidx = 0x7fffffff;
+#if HPS_PROF_PIVOT
+      if (prof && tid == 0) { const long long t = clock64(); prof[44] += t - pq0; pq0 = t; }
+#endif
       constexpr int RU = WB >= 8 ? 2 : 4;  // rows in flight per thread
       for (int r0 = j + 1 + tid; r0 < n_cand; r0 += NT * RU) {
         double v[RU][WB];
@@ -1542,15 +1570,26 @@ __device__ void panel_block(Ctx& c, int c0, int w, int b0) {
         }
       }
       if (j + 1 < WB) {
+#if HPS_PROF_PIVOT
+        if (prof && tid == 0) { const long long t = clock64(); prof[45] += t - pq0; pq0 = t; }
+#endif
         if (j + 1 >= n_cand && tid == 0) {
 #pragma unroll
           for (int t = 0; t < WB; ++t) s_rowj[par ^ 1][t] = 0.0;
         }
         warp_argmax(best, bidx, par ^ 1);
+#if HPS_PROF_PIVOT
+        if (prof && tid == 0) { const long long t = clock64(); prof[46] += t - pq0; pq0 = t; }
+#endif
       }
       __syncthreads();
+#if HPS_PROF_PIVOT
+      if (prof && tid == 0) prof[47] += clock64() - pq0;
+#endif
     }
   }
+  if (HPS_PIVOT_DEFER && tid == 0)
+    for (int j = 0; j < WB; ++j) pivot_bookkeeping(c, b0, j, s_jbi[j], head, compact, s_jpv[j]);
   PANEL_TICK(12)
   // 4. write-back; non-candidate rows L = A U^{-1}
   for (int e = tid; e < n_cand * WB; e += NT) {

@@ -91,3 +91,7 @@ if c[:, 57:60].sum() > 0:   # HPS_PROF_GEMM build: where thread 0's GEMM time go
               f"  {c[:, 57 + b].sum() / leaves:8.0f}")
     f = lambda k: c[:, k].sum() / leaves / clk * 1e3
     print(f"    producer, all buckets: tile claim + k bounds {f(47):.2f} ms/leaf, chunk issue (expect_tx, TMA, prefetch) {f(63):.2f} ms/leaf")
+if c[:, 44:48].sum() > 0 and c[:, 57:60].sum() == 0:   # HPS_PROF_PIVOT build
+    f = lambda k: c[:, k].sum() / leaves / clk * 1e3
+    print(f"  pivot columns (thread 0, ms/leaf): selection + bookkeeping + 1/pivot {f(44):.2f}, row updates {f(45):.2f},"
+          f" warp argmax + stash {f(46):.2f}, column barrier {f(47):.2f}")

@@ -231,12 +231,14 @@ class ClockSampler:
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        pw = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = [nm for i, nm in enumerate(names) if any(r[3 + i] == "Active" for r in rows)]
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
                 "reasons": reasons, "samples": len(rows),
-                "power_w_max": max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())}
+                "power_w_max": max(pw) if pw else None,
+                "power_w_median": float(np.median(pw)) if pw else None}
 
 
 def traffic_per_leaf(p):

@@ -3508,7 +3508,12 @@ static int build_orderings(hps_plan_s* P) {
   cudaMemcpy(P->eqpos, eqpos.data(), (size_t)n * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(P->gsorted, P->h_gsorted.data(), (size_t)P->n_pad * 4, cudaMemcpyHostToDevice);
   // W blocks pay off from p ~ 15 on (small leaves: the per-block op overheads dominate)
-  P->wt = (dbg && (atoi(dbg) & 64)) ? 0 : (P->n_pad >= 2048 ? 1 : 0);
+  // W-block Schur complement from n_pad >= HPS_WT_MIN_N (default 1536: p >= 14; p = 14
+  // +2.3% with it, p = 12 -6%, p = 10 -11%: profiles/r02c_variant_sweep.jsonl); below it
+  // the backward solve and the line-sparse output phase are faster
+  const char* wte = getenv("HPS_WT_MIN_N");
+  const int wt_min = wte ? atoi(wte) : 1536;
+  P->wt = (dbg && (atoi(dbg) & 64)) ? 0 : (P->n_pad >= wt_min ? 1 : 0);
   P->RW = P->m_pad < HPS_RW ? P->m_pad : HPS_RW;
   cudaMemcpy(P->rowpos, rowpos.data(), (size_t)n * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(P->colpos, colpos.data(), (size_t)m * 4, cudaMemcpyHostToDevice);

@@ -18,6 +18,8 @@ library every call raises :class:`NativeUnavailableError`.
 
 from __future__ import annotations
 
+import os
+
 import ctypes
 import functools
 from typing import Optional, Tuple
@@ -461,8 +463,8 @@ def dtn_flops_executed(n: int, m: int, q: int, d: int = 3, skip_prefix: bool = T
         return 2.0 / 3.0 * n ** 3 + 2.0 * n * n * m + 2.0 * q * m * m
     w = leaf_work_model(q, d)
     lu_fwd = w["panel"] + w["lu_trsm"] + w["lu_update"] + w["forward"]
-    if (n + 15) // 16 * 16 < 2048:   # the engine uses W blocks from n_pad >= 2048 on
-        wtrick = False
+    if (n + 15) // 16 * 16 < int(os.environ.get("HPS_WT_MIN_N", "1536")):
+        wtrick = False               # the engine uses W blocks from n_pad >= 1536 (p >= 14) on
     if not wtrick:
         return lu_fwd + float(n) * n * m + 2.0 * q * m * m
     return lu_fwd + w["W"] + w["T"]

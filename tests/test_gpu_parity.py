@@ -81,7 +81,7 @@ def bump_pack(p, leaves, kappa, seed=0, d=3):
     return tpl, pack
 
 
-@pytest.mark.parametrize("p,leaves", [(6, 300), (12, 6), (16, 2), (18, 2), (20, 1)])
+@pytest.mark.parametrize("p,leaves", [(6, 300), (12, 6), (13, 3), (14, 3), (16, 2), (18, 2), (20, 1)])
 def test_batched_dtn_vs_oracle(p, leaves):
     from paper_2503_04033_b200.engine import LeafEngine
     tpl, pack = bump_pack(p, leaves, kappa=40.0, seed=p)

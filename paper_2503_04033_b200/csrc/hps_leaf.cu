@@ -3514,7 +3514,12 @@ static int build_orderings(hps_plan_s* P) {
   const char* wte = getenv("HPS_WT_MIN_N");
   const int wt_min = wte ? atoi(wte) : 1536;
   P->wt = (dbg && (atoi(dbg) & 64)) ? 0 : (P->n_pad >= wt_min ? 1 : 0);
-  P->RW = P->m_pad < HPS_RW ? P->m_pad : HPS_RW;
+  {
+    // boundary rows per W block (HPS_RW_ROWS overrides the compile-time default, for tuning)
+    const char* rwe = getenv("HPS_RW_ROWS");
+    const int rw = rwe ? std::max(16, atoi(rwe) / 16 * 16) : HPS_RW;
+    P->RW = P->m_pad < rw ? P->m_pad : rw;
+  }
   cudaMemcpy(P->rowpos, rowpos.data(), (size_t)n * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(P->colpos, colpos.data(), (size_t)m * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(P->colnat, colnat.data(), (size_t)m * 4, cudaMemcpyHostToDevice);

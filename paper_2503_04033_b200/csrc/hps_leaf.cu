@@ -138,6 +138,12 @@ constexpr int PF_DIST = HPS_PF;
 #ifndef HPS_PROF_GEMM
 #define HPS_PROF_GEMM 0  // diagnostics build: setup / data-wait / tail / producer cycles per GEMM bucket
 #endif
+#ifndef HPS_WARP_PRODUCER
+#define HPS_WARP_PRODUCER 1  // the producer warp's 32 lanes share the tile claims / k bounds
+#endif
+#ifndef HPS_WARP_BOUNDS
+#define HPS_WARP_BOUNDS 1  // each warp's own k bounds at a tile start: table loads one per lane
+#endif
 #ifndef HPS_PF_NEXT
 #define HPS_PF_NEXT 0  // narrow / tall GEMMs: chunks of the next tile prefetched into L2
 #endif
@@ -609,7 +615,11 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   // producer state (thread 0 only)
   int p_it = 0, p_tile = 0, p_kc = 0, p_next = 0, p_skipped = 0, p_k0 = 0, p_j = 0;
   bool p_end = false, p_in = false;
-  auto claim_tile = [&]() -> int {
+  // warp producer: the whole producer warp runs the tile claims and k bounds (the 16-row /
+  // 16-column table loads one per lane, min by redux.sync) and lane 0 issues the chunks
+  constexpr bool WPM = HPS_WARP_PRODUCER && GR == 1;
+  const bool wp = WPM && !slice;
+  auto claim_tile1 = [&]() -> int {
     if (gmode == 0) {
       if (GR == 1) return p_next < tiles ? p_next++ : -1;
       const int t = atomicAdd(&s_next_tile, 1);
@@ -627,6 +637,12 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
       if (prev == old) return (int)(old & 0xffffffffull);
       old = prev;
     }
+  };
+  auto claim_tile = [&]() -> int {
+    if (!wp || gmode == 0) return claim_tile1();  // (in-order claims: the same sequence in every lane)
+    int t = 0;
+    if (lane == 0) t = claim_tile1();
+    return __shfl_sync(0xffffffffu, t, 0);
   };
   // the next chunk into its stage, once every warp has released the stage's last use
   auto produce = [&]() {
@@ -665,20 +681,33 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
         if (kmode & 8) {  // columns of the tile: first row of U with a nonzero (16-column minima)
           const int cb = bc + (p_tile % tiles_n) * TN;
           int gm = c.gcol16[-1];
-          for (int cq = cb; cq < cb + TN && cq < bc + N; cq += 16) gm = min(gm, c.gcol16[cq >> 4]);
+          if (wp) {
+            const int cq = cb + 16 * lane;
+            const int v = (lane < TN / 16 && cq < bc + N) ? c.gcol16[cq >> 4] : 0x7fffffff;
+            gm = min(gm, __reduce_min_sync(0xffffffffu, v));
+          } else {
+            for (int cq = cb; cq < cb + TN && cq < bc + N; cq += 16) gm = min(gm, c.gcol16[cq >> 4]);
+          }
           kk = max(kk, gm - br);
         }
         if (kmode & 4) {  // rows of the tile: first nonzero column (16-row group minima)
           const int r0 = ar + (p_tile / tiles_n) * TM;
           int gm = 0x7fffffff;
-          for (int r = r0; r < r0 + TM && r < ar + M; r += 16) gm = min(gm, c.gmin16[r >> 4]);
+          if (wp) {
+            const int r = r0 + 16 * lane;
+            const int v = (lane < TM / 16 && r < ar + M) ? c.gmin16[r >> 4] : 0x7fffffff;
+            gm = __reduce_min_sync(0xffffffffu, v);
+          } else {
+            for (int r = r0; r < r0 + TM && r < ar + M; r += 16) gm = min(gm, c.gmin16[r >> 4]);
+          }
           kk = max(kk, gm - ac);
           if (kk >= K) {  // the tile's rows are zero over the whole k range: C unchanged
             ++p_skipped;
-            if (c.prof && (!slice || tid == 0)) c.prof[31] += ((unsigned long long)K * TM * TN * 2) >> 20;
+            if (c.prof && (!(slice || wp) || lane == 0) && (!slice || tid == 0))
+              c.prof[31] += ((unsigned long long)K * TM * TN * 2) >> 20;
             continue;
           }
-          if (c.prof && kk > 0 && (!slice || tid == 0))
+          if (c.prof && kk > 0 && (!(slice || wp) || lane == 0) && (!slice || tid == 0))
             c.prof[31] += ((unsigned long long)(kk / KC) * KC * TM * TN * 2) >> 20;
         }
         const int k0 = kk / KC;
@@ -690,14 +719,14 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
       if (HPS_KREV && (p_tile & 1)) p_kc = kchunks - 1;
       if (slice) {
         if (lane == 0) s_tile_ring_w[warp][s] = p_tile;
-      } else {
+      } else if (!wp || lane == 0) {
         s_tile_ring[grp][s] = p_tile;
       }
       if (p_tile < 0) {  // end marker: a stage with no data
         p_end = true;
         if (slice) {
           if (lane == 0) mbar_arrive(&full[s]);
-        } else {
+        } else if (!wp || lane == 0) {
           mbar_arrive_cnt(&full[s], FULL_COUNT);
         }
         ++p_it;
@@ -705,7 +734,7 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
       }
       if (slice) {
         if (lane == 0) s_kc0_ring_w[warp][s] = p_k0;
-      } else {
+      } else if (!wp || lane == 0) {
         s_kc0_ring[grp][s] = p_k0;
       }
       p_in = true;
@@ -714,6 +743,14 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     long long pi = 0;
     if (pt) { pi = clock64(); c.prof[47] += pi - pc; }  // tile claim + k bounds (all buckets)
 #endif
+    if (wp && lane != 0) {  // lanes 1..31 of the producer warp: state only, lane 0 issues
+      ++p_it;
+      ++p_j;
+      if (HPS_KREV && (p_tile & 1)) --p_kc;
+      else ++p_kc;
+      if (p_j == kchunks - p_k0) p_in = false;
+      return;
+    }
     const int tm = p_tile / tiles_n, tn = p_tile - tm * tiles_n;
     double* sa = smem + s * STAGE_DBL;
     double* sb = sa + STAGE_A;
@@ -800,7 +837,8 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     if (pt) c.prof[63] += clock64() - pi;  // TMA issue and prefetches (all buckets)
 #endif
   };
-  if (slice || tid == prod_tid) {
+  const bool is_prod = slice || (wp ? (tid >> 5) == (prod_tid >> 5) : tid == prod_tid);
+  if (is_prod) {
     for (int s = 0; s < STG - 1; ++s) produce();
   }
 
@@ -838,18 +876,33 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
       if (kmode & 2) {  // W rows: per-row first nonzero, warp-reduced
         int f = 0x7fffffff;
         for (int r = r0 + lane; r < r1; r += 32) f = min(f, c.wf[r - c.n_piv]);
+        if (HPS_WARP_BOUNDS) {
+          f = __reduce_min_sync(0xffffffffu, f);
+        } else {
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) f = min(f, __shfl_xor_sync(0xffffffffu, f, off));
+          for (int off = 16; off > 0; off >>= 1) f = min(f, __shfl_xor_sync(0xffffffffu, f, off));
+        }
         wk = max(wk, f - ac);
       }
       if (kmode & 4) {
         int gm = 0x7fffffff;
-        for (int r = r0; r < r1; r += 16) gm = min(gm, c.gmin16[r >> 4]);
+        if (HPS_WARP_BOUNDS) {  // the 16-row groups of the warp's rows, one per lane
+          const int r = r0 + 16 * lane;
+          gm = __reduce_min_sync(0xffffffffu, (lane < MI * 8 / 16 + 1 && r < r1) ? c.gmin16[r >> 4] : 0x7fffffff);
+        } else {
+          for (int r = r0; r < r1; r += 16) gm = min(gm, c.gmin16[r >> 4]);
+        }
         wk = max(wk, gm - ac);
       }
       if (kmode & 8) {
         int gm = c.gcol16[-1];
-        for (int cq = bc + c0w; cq < bc + c1w; cq += 16) gm = min(gm, c.gcol16[cq >> 4]);
+        if (HPS_WARP_BOUNDS) {
+          const int cq = bc + c0w + 16 * lane;
+          gm = min(gm, __reduce_min_sync(0xffffffffu,
+                                         (lane < NJ * 8 / 16 + 1 && c0w + 16 * lane < c1w) ? c.gcol16[cq >> 4] : 0x7fffffff));
+        } else {
+          for (int cq = bc + c0w; cq < bc + c1w; cq += 16) gm = min(gm, c.gcol16[cq >> 4]);
+        }
         wk = max(wk, gm - br);
       }
     }
@@ -891,7 +944,7 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
 #if HPS_PROF_GEMM
     long long pq = pt ? clock64() : 0;
 #endif
-    if (slice || tid == prod_tid) produce();
+    if (is_prod) produce();
 #if HPS_PROF_GEMM
     if (pt) { const long long t = clock64(); c.prof[60 + pb] += t - pq; pq = t; }
 #endif

@@ -141,6 +141,12 @@ constexpr int PF_DIST = HPS_PF;
 #ifndef HPS_WARP_PRODUCER
 #define HPS_WARP_PRODUCER 1  // the producer warp's 32 lanes share the tile claims / k bounds
 #endif
+#ifndef HPS_SHARE_FENCE
+#define HPS_SHARE_FENCE 1  // all threads' writes performed (membar.gl) before an op is published
+#endif
+#ifndef HPS_BOUNDS_ONEPASS
+#define HPS_BOUNDS_ONEPASS 1  // all of a tile's bound-table loads issued before the reductions
+#endif
 #ifndef HPS_WARP_BOUNDS
 #define HPS_WARP_BOUNDS 1  // each warp's own k bounds at a tile start: table loads one per lane
 #endif
@@ -582,13 +588,29 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
   __shared__ int s_tile_ring[2][STAGES_MAX];  // per group: tile id started in each stage (-1: end)
   __shared__ int s_kc0_ring[2][STAGES_MAX];   // its first k-chunk
   __shared__ int s_next_tile;                 // half tiles, in-order mode: next unclaimed tile
+  // An op published for sharing is read by other CTAs' TMA loads: every thread's earlier
+  // global writes (the previous ops' f64 reductions and stores, which bar.sync does not
+  // wait for) must be performed GPU-wide before thread 0 publishes.
+  __shared__ int s_pub;
+  bool pub = false;
+  if (HPS_SHARE_FENCE && c.role != 2 && c.sh && tiles >= SHARE_MIN_TILES) {
+    if (tid == 0) s_pub = *reinterpret_cast<const volatile int*>(c.leaf_counter) >= c.n_leaves;
+    __syncthreads();
+    pub = s_pub != 0;
+    if (pub) {
+      __threadfence();
+      fence_proxy_async_global();
+      __syncthreads();
+    }
+  }
   if (tid == 0) {
     int m = 0;
     s_next_tile = 0;
     if (c.role == 2) {
       m = 2;
-    } else if (c.sh && tiles >= SHARE_MIN_TILES &&
-               *reinterpret_cast<const volatile int*>(c.leaf_counter) >= c.n_leaves) {
+    } else if (HPS_SHARE_FENCE ? pub
+                               : (c.sh && tiles >= SHARE_MIN_TILES &&
+                                  *reinterpret_cast<const volatile int*>(c.leaf_counter) >= c.n_leaves)) {
       m = 1;
       ShareSlot* sh = c.sh;
       c.seq += 1;
@@ -676,6 +698,33 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
         if (!kmode) break;
         // first k with a nonzero in this tile's B columns / A rows
         int kk = 0;
+        if (wp && HPS_BOUNDS_ONEPASS) {
+          // every table load of the tile issued before any is consumed: one L2 round trip
+          int vr = 0, vw = 0, vc1 = 0x7fffffff, vc = 0x7fffffff, vg = 0x7fffffff;
+          const int cb = bc + (p_tile % tiles_n) * TN, r0 = ar + (p_tile / tiles_n) * TM;
+          if (kmode & 1) vr = c.rhs_g[(p_tile % tiles_n) * TN];
+          if (kmode & 2) vw = c.wf[r0 - c.n_piv];
+          if (kmode & 8) {
+            vc1 = c.gcol16[-1];
+            if (lane < TN / 16 && cb + 16 * lane < bc + N) vc = c.gcol16[(cb + 16 * lane) >> 4];
+          }
+          if ((kmode & 4) && lane < TM / 16 && r0 + 16 * lane < ar + M) vg = c.gmin16[(r0 + 16 * lane) >> 4];
+          if (kmode & 1) kk = max(kk, vr - br);
+          if (kmode & 2) kk = max(kk, vw - ac);
+          if (kmode & 8) kk = max(kk, min(vc1, __reduce_min_sync(0xffffffffu, vc)) - br);
+          if (kmode & 4) {
+            kk = max(kk, __reduce_min_sync(0xffffffffu, vg) - ac);
+            if (kk >= K) {
+              ++p_skipped;
+              if (c.prof && lane == 0) c.prof[31] += ((unsigned long long)K * TM * TN * 2) >> 20;
+              continue;
+            }
+            if (c.prof && kk > 0 && lane == 0) c.prof[31] += ((unsigned long long)(kk / KC) * KC * TM * TN * 2) >> 20;
+          }
+          const int k0 = kk / KC;
+          p_kc = k0 > kchunks - 1 ? kchunks - 1 : k0;
+          break;
+        }
         if (kmode & 1) kk = max(kk, c.rhs_g[(p_tile % tiles_n) * TN] - br);
         if (kmode & 2) kk = max(kk, c.wf[ar + (p_tile / tiles_n) * TM - c.n_piv] - ac);
         if (kmode & 8) {  // columns of the tile: first row of U with a nonzero (16-column minima)
@@ -872,38 +921,54 @@ __device__ __forceinline__ void gemm_t(Ctx& c, const bool sub, const int a_src, 
     if (kmode && mv > 0 && nv > 0) {
       const int r0 = ar + tm * TM + wm * (MI * 8), r1 = min(r0 + MI * 8, ar + M);
       const int c0w = tn * TN + wn * (NJ * 8), c1w = min(c0w + NJ * 8, N);
-      if (kmode & 1) wk = max(wk, c.rhs_g[c0w] - br);  // suffix minima: first column is the min
-      if (kmode & 2) {  // W rows: per-row first nonzero, warp-reduced
-        int f = 0x7fffffff;
-        for (int r = r0 + lane; r < r1; r += 32) f = min(f, c.wf[r - c.n_piv]);
-        if (HPS_WARP_BOUNDS) {
-          f = __reduce_min_sync(0xffffffffu, f);
-        } else {
+      if (HPS_WARP_BOUNDS && HPS_BOUNDS_ONEPASS) {
+        // every table load of the warp's block issued before any is consumed
+        int vr = 0, vw = 0x7fffffff, vg = 0x7fffffff, vc1 = 0x7fffffff, vc = 0x7fffffff;
+        if (kmode & 1) vr = c.rhs_g[c0w];
+        if ((kmode & 2) && r0 + lane < r1) vw = c.wf[r0 + lane - c.n_piv];
+        if ((kmode & 4) && lane < MI * 8 / 16 + 1 && r0 + 16 * lane < r1) vg = c.gmin16[(r0 + 16 * lane) >> 4];
+        if (kmode & 8) {
+          vc1 = c.gcol16[-1];
+          if (lane < NJ * 8 / 16 + 1 && c0w + 16 * lane < c1w) vc = c.gcol16[(bc + c0w + 16 * lane) >> 4];
+        }
+        if (kmode & 1) wk = max(wk, vr - br);
+        if (kmode & 2) wk = max(wk, __reduce_min_sync(0xffffffffu, vw) - ac);
+        if (kmode & 4) wk = max(wk, __reduce_min_sync(0xffffffffu, vg) - ac);
+        if (kmode & 8) wk = max(wk, min(vc1, __reduce_min_sync(0xffffffffu, vc)) - br);
+      } else {
+        if (kmode & 1) wk = max(wk, c.rhs_g[c0w] - br);  // suffix minima: first column is the min
+        if (kmode & 2) {  // W rows: per-row first nonzero, warp-reduced
+          int f = 0x7fffffff;
+          for (int r = r0 + lane; r < r1; r += 32) f = min(f, c.wf[r - c.n_piv]);
+          if (HPS_WARP_BOUNDS) {
+            f = __reduce_min_sync(0xffffffffu, f);
+          } else {
 #pragma unroll
-          for (int off = 16; off > 0; off >>= 1) f = min(f, __shfl_xor_sync(0xffffffffu, f, off));
+            for (int off = 16; off > 0; off >>= 1) f = min(f, __shfl_xor_sync(0xffffffffu, f, off));
+          }
+          wk = max(wk, f - ac);
         }
-        wk = max(wk, f - ac);
-      }
-      if (kmode & 4) {
-        int gm = 0x7fffffff;
-        if (HPS_WARP_BOUNDS) {  // the 16-row groups of the warp's rows, one per lane
-          const int r = r0 + 16 * lane;
-          gm = __reduce_min_sync(0xffffffffu, (lane < MI * 8 / 16 + 1 && r < r1) ? c.gmin16[r >> 4] : 0x7fffffff);
-        } else {
-          for (int r = r0; r < r1; r += 16) gm = min(gm, c.gmin16[r >> 4]);
+        if (kmode & 4) {
+          int gm = 0x7fffffff;
+          if (HPS_WARP_BOUNDS) {  // the 16-row groups of the warp's rows, one per lane
+            const int r = r0 + 16 * lane;
+            gm = __reduce_min_sync(0xffffffffu, (lane < MI * 8 / 16 + 1 && r < r1) ? c.gmin16[r >> 4] : 0x7fffffff);
+          } else {
+            for (int r = r0; r < r1; r += 16) gm = min(gm, c.gmin16[r >> 4]);
+          }
+          wk = max(wk, gm - ac);
         }
-        wk = max(wk, gm - ac);
-      }
-      if (kmode & 8) {
-        int gm = c.gcol16[-1];
-        if (HPS_WARP_BOUNDS) {
-          const int cq = bc + c0w + 16 * lane;
-          gm = min(gm, __reduce_min_sync(0xffffffffu,
-                                         (lane < NJ * 8 / 16 + 1 && c0w + 16 * lane < c1w) ? c.gcol16[cq >> 4] : 0x7fffffff));
-        } else {
-          for (int cq = bc + c0w; cq < bc + c1w; cq += 16) gm = min(gm, c.gcol16[cq >> 4]);
+        if (kmode & 8) {
+          int gm = c.gcol16[-1];
+          if (HPS_WARP_BOUNDS) {
+            const int cq = bc + c0w + 16 * lane;
+            gm = min(gm, __reduce_min_sync(0xffffffffu,
+                                           (lane < NJ * 8 / 16 + 1 && c0w + 16 * lane < c1w) ? c.gcol16[cq >> 4] : 0x7fffffff));
+          } else {
+            for (int cq = bc + c0w; cq < bc + c1w; cq += 16) gm = min(gm, c.gcol16[cq >> 4]);
+          }
+          wk = max(wk, gm - br);
         }
-        wk = max(wk, gm - br);
       }
     }
     sub_final = 0;

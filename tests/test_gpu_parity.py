@@ -151,6 +151,24 @@ def test_endgame_gemm_sharing_is_exact(monkeypatch):
         assert rel(shared[k], ref) <= TOL
 
 
+def test_endgame_sharing_is_deterministic():
+    """Leaves helped by other CTAs in the endgame come out bit-identical run after
+    run: an owner publishes a GEMM op only after every thread's earlier reductions
+    are performed GPU-wide (a missing fence there corrupted ~1 leaf in 4500 at p = 20,
+    profiles/r02c_determinism_p20.jsonl)."""
+    import torch
+    from paper_2503_04033_b200.engine import LeafEngine
+    tpl0, _ = bump_pack(12, 1, kappa=25.0)
+    slots = LeafEngine(tpl0, False, True, device=0).slots
+    L = slots + 64
+    tpl, pack = bump_pack(12, L, kappa=25.0, seed=9)
+    eng = LeafEngine(tpl, False, True, device=0)
+    coeffs = torch.from_numpy(pack).cuda()
+    ref = eng.dtn(coeffs)[0].cpu().numpy()
+    for _ in range(4):
+        assert np.array_equal(eng.dtn(coeffs)[0].cpu().numpy(), ref)
+
+
 def test_two_dimensional_batch_vs_oracle():
     from paper_2503_04033_b200.engine import LeafEngine
     tpl, pack = bump_pack(9, 5, kappa=15.0, seed=4, d=2)

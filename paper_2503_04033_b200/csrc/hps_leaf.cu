@@ -3444,8 +3444,11 @@ static int launch(hps_plan_s* P, int mode, int n_leaves, const double* coeffs, c
   L.done_chunk = done_chunk;
   CK(cudaMemsetAsync(P->leaf_counter, 0, 64 * sizeof(int), stream));
   {
+    // Endgame GEMM sharing is opt-in (HPS_SHARE=1): repeated runs at p = 20 with it on
+    // changed ~1 leaf in 5000 (profiles/r02c_determinism_p20.jsonl), never with it off
     const char* dbg = getenv("HPS_DEBUG");
-    const bool share_off = dbg && (atoi(dbg) & 16);
+    const char* shr = getenv("HPS_SHARE");
+    const bool share_off = (dbg && (atoi(dbg) & 16)) || !(shr && atoi(shr) == 1);
     if (!share_off) {
       if (P->share_cap < slots) {
         cudaFree(P->share);

@@ -243,7 +243,7 @@ class ClockSampler:
 
 def traffic_per_leaf(p):
     """DRAM bytes per leaf from the committed ncu --set full capture at this order."""
-    for name in (f"r02c_final5_ncu_summary_p{p}.json", f"r02c_final4_ncu_summary_p{p}.json", f"r02c_final2_ncu_summary_p{p}.json", f"r02c_final_ncu_summary_p{p}.json", f"r02c_ncu_summary_p{p}.json", f"r02b_ncu_summary_p{p}.json",
+    for name in (f"r02c_final6_ncu_summary_p{p}.json", f"r02c_final5_ncu_summary_p{p}.json", f"r02c_final4_ncu_summary_p{p}.json", f"r02c_final2_ncu_summary_p{p}.json", f"r02c_final_ncu_summary_p{p}.json", f"r02c_ncu_summary_p{p}.json", f"r02b_ncu_summary_p{p}.json",
                  f"r02_ncu_summary_p{p}.json",
                  "r01_ncu_summary.json"):
         path = os.path.join(ROOT, "profiles", name)
